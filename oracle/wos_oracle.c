@@ -1,0 +1,551 @@
+/*
+ * wos_oracle.c — TEST INFRASTRUCTURE ONLY. Never linked into, loaded by, or
+ * called from the product path (paper_2603_01193_b200/). Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs use it,
+ * and only as the checker or the timed CPU baseline.
+ *
+ * A plain-C, fp64, scalar restatement of the reference's Walk-on-Spheres path
+ * (arxiv 2603.01193, package `spherewalk`, read-only at /root/reference/pkg/src):
+ *
+ *   philox4x64 ........ rng.philox4x64            rng.py:57-82 (_mulhilo rng.py:44-54)
+ *   u53 ............... rng.to_uniform            rng.py:100-102 (_kernels._u01 :85-87)
+ *   nonzero_u ......... walker._redraw_zeros      walker.py:232-242 (_kernels._nonzero_u :90-102)
+ *   ball_query ........ BallDomain.boundary_query geometry.py:196-206
+ *   walk_ref_one ...... walker._poisson_generic   walker.py:257-314 (one row; the
+ *                       vectorized loop's per-lane arithmetic in the same order)
+ *   oracle_estimate ... estimator._estimate_block estimator.py:119-141 +
+ *                       PointEstimate.from_values estimator.py:106-110 (two-pass)
+ *
+ * Box and polygon domains, and the sine / Gaussian / Fourier / arc-length /
+ * quadratic problem terms, do not exist in the reference; they are the BASELINE
+ * configs' problem data, passed to the reference through the duck-typed domain
+ * protocol (dim, contains, boundary_query, bounding_radius) and Python callables
+ * by tests/golden/make_golden.py, whose outputs pin this file
+ * (tests/test_oracle_golden.py).
+ *
+ * oracle_walk_rows_native restates the product's NATIVE_F32 estimator
+ * (Philox4x32-10 stream layout + Green's-function importance sampling) in fp64 so
+ * the native kernel can be checked walk by walk, not only statistically.
+ *
+ * Build: oracle/Makefile -> oracle/_build/libwos_oracle.so
+ */
+#include "../include/wos_b200.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define TWO_PI 6.283185307179586
+#define INV_TWO_PI (1.0 / TWO_PI)
+#define INV_FOUR_PI (1.0 / (4.0 * 3.141592653589793))
+#define PI 3.141592653589793
+
+/* ------------------------------------------------------------------ */
+/* Philox 4x64-10 (rng.py:31-41 constants, :76-81 round)               */
+/* ------------------------------------------------------------------ */
+static void philox4x64(const uint64_t c[4], uint64_t k0, uint64_t k1, uint64_t out[4]) {
+  uint64_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
+  for (int r = 0; r < 10; ++r) {
+    unsigned __int128 p0 = (unsigned __int128)0xD2E7470EE14C6C93ull * x0;
+    unsigned __int128 p1 = (unsigned __int128)0xCA5A826395121157ull * x2;
+    uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+    uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+    uint64_t n0 = hi1 ^ x1 ^ k0, n2 = hi0 ^ x3 ^ k1;
+    x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+void oracle_philox4x64(int64_t n, const uint64_t* ctr, uint64_t k0, uint64_t k1, uint64_t* out) {
+  for (int64_t i = 0; i < n; ++i) philox4x64(ctr + 4 * i, k0, k1, out + 4 * i);
+}
+
+/* Philox 4x32-10 (Random123 constants) — the NATIVE_F32 generator. */
+static void philox4x32(const uint32_t c[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+  uint32_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * x0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * x2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ x1 ^ k0, n2 = hi0 ^ x3 ^ k1;
+    x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+void oracle_philox4x32(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
+  for (int64_t i = 0; i < n; ++i) philox4x32(ctr + 4 * i, k0, k1, out + 4 * i);
+}
+
+static double u53(uint64_t w) { return (double)(w >> 11) * 1.1102230246251565e-16; }
+
+/* rejected zero uniform -> redraw at tag 1, 2, ... (walker.py:232-242) */
+static double nonzero_u(double u, uint64_t draw, uint64_t pid, uint64_t tid, uint64_t k0,
+                        uint64_t k1) {
+  uint64_t tag = 1;
+  while (u == 0.0) {
+    uint64_t c[4] = {draw, pid, tid, tag}, w[4];
+    philox4x64(c, k0, k1, w);
+    u = u53(w[0]);
+    tag += 1;
+  }
+  return u;
+}
+
+/* ------------------------------------------------------------------ */
+/* Domains: distance to the boundary and the closest boundary point    */
+/* ------------------------------------------------------------------ */
+static double query(const wos_problem* pb, const double* x, double* q) {
+  const int dim = pb->dim;
+  const double* P = pb->dom;
+  if (pb->dom_kind == WOS_DOM_BALL) {
+    /* geometry.py:196-206 */
+    double u[3], s = 0.0;
+    for (int i = 0; i < dim; ++i) { u[i] = x[i] - P[i]; s += u[i] * u[i]; }
+    double rho = sqrt(s), R = P[dim];
+    double d = fabs(R - rho);
+    for (int i = 0; i < dim; ++i) {
+      double dir = (rho == 0.0) ? (i == 0 ? 1.0 : 0.0) : u[i] / rho;
+      q[i] = P[i] + R * dir;
+    }
+    return d;
+  }
+  if (pb->dom_kind == WOS_DOM_BOX) {
+    /* min over faces; first nearest face wins (axis order, lower before upper) */
+    double best = INFINITY;
+    int axis = 0;
+    double face = 0.0;
+    for (int i = 0; i < dim; ++i) {
+      double dl = x[i] - P[i], du = P[dim + i] - x[i];
+      if (dl < best) { best = dl; axis = i; face = P[i]; }
+      if (du < best) { best = du; axis = i; face = P[dim + i]; }
+    }
+    for (int i = 0; i < dim; ++i) q[i] = x[i];
+    q[axis] = face;
+    return best;
+  }
+  /* WOS_DOM_POLYGON */
+  const int n = (int)P[0];
+  const double* V = P + 1;
+  double best = INFINITY, bx = 0.0, by = 0.0;
+  for (int i = 0; i < n; ++i) {
+    int j = (i + 1 == n) ? 0 : i + 1;
+    double ax = V[2 * i], ay = V[2 * i + 1];
+    double ex = V[2 * j] - ax, ey = V[2 * j + 1] - ay;
+    double wx = x[0] - ax, wy = x[1] - ay;
+    double t = (wx * ex + wy * ey) / (ex * ex + ey * ey);
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    double cx = ax + t * ex, cy = ay + t * ey;
+    double dx = x[0] - cx, dy = x[1] - cy;
+    double d2 = dx * dx + dy * dy;
+    if (d2 < best) { best = d2; bx = cx; by = cy; }
+  }
+  q[0] = bx; q[1] = by;
+  return sqrt(best);
+}
+
+int oracle_contains(const wos_problem* pb, const double* x) {
+  const int dim = pb->dim;
+  const double* P = pb->dom;
+  if (pb->dom_kind == WOS_DOM_BALL) {
+    double s = 0.0;
+    for (int i = 0; i < dim; ++i) s += (x[i] - P[i]) * (x[i] - P[i]);
+    return sqrt(s) < P[dim];
+  }
+  if (pb->dom_kind == WOS_DOM_BOX) {
+    for (int i = 0; i < dim; ++i)
+      if (!(x[i] > P[i] && x[i] < P[dim + i])) return 0;
+    return 1;
+  }
+  const int n = (int)P[0];
+  const double* V = P + 1;
+  int inside = 0;
+  for (int i = 0; i < n; ++i) {
+    int j = (i + 1 == n) ? 0 : i + 1;
+    double ax = V[2 * i], ay = V[2 * i + 1], bx = V[2 * j], by = V[2 * j + 1];
+    if ((ay > x[1]) != (by > x[1])) {
+      double xc = ax + (x[1] - ay) * (bx - ax) / (by - ay);
+      if (x[0] < xc) inside = !inside;
+    }
+  }
+  return inside;
+}
+
+/* ------------------------------------------------------------------ */
+/* Problem terms                                                        */
+/* ------------------------------------------------------------------ */
+static double source(const wos_problem* pb, const double* y) {
+  const int dim = pb->dim;
+  const double* S = pb->src;
+  switch (pb->src_kind) {
+    case WOS_SRC_CONST:
+      return S[0];
+    case WOS_SRC_RBF2: { /* _kernels.py:248-259 */
+      double d1x = y[0] - S[2], d1y = y[1] - S[3], d2x = y[0] - S[4], d2y = y[1] - S[5];
+      return S[0] * exp(-(d1x * d1x + d1y * d1y)) + S[1] * exp(-(d2x * d2x + d2y * d2y));
+    }
+    case WOS_SRC_SINE: {
+      const int K = (int)S[0];
+      const double* a = S + 1;
+      double sv[3][16];
+      for (int i = 0; i < dim; ++i)
+        for (int k = 0; k < K; ++k) sv[i][k] = sin((double)(k + 1) * PI * y[i]);
+      double f = 0.0;
+      if (dim == 2) {
+        for (int k = 0; k < K; ++k)
+          for (int l = 0; l < K; ++l) f += a[k * K + l] * sv[0][k] * sv[1][l];
+      } else {
+        for (int k = 0; k < K; ++k)
+          for (int l = 0; l < K; ++l)
+            for (int m = 0; m < K; ++m)
+              f += a[(k * K + l) * K + m] * sv[0][k] * sv[1][l] * sv[2][m];
+      }
+      return f;
+    }
+    case WOS_SRC_GAUSS: {
+      double r2 = 0.0;
+      for (int i = 0; i < dim; ++i) r2 += (y[i] - S[2 + i]) * (y[i] - S[2 + i]);
+      return S[0] * exp(-r2 / (2.0 * S[1] * S[1]));
+    }
+    default:
+      return 0.0;
+  }
+}
+
+static double boundary(const wos_problem* pb, const double* q) {
+  const int dim = pb->dim;
+  const double* B = pb->bnd;
+  switch (pb->bnd_kind) {
+    case WOS_BND_CONST:
+      return B[0];
+    case WOS_BND_LINEAR:
+      if (dim == 2) return B[0] * q[0] + B[1] * q[1] + B[2];
+      return B[0] * q[0] + B[1] * q[1] + B[2] * q[2] + B[3];
+    case WOS_BND_FOURIER5: { /* _kernels.py:262-278 */
+      double r = sqrt(q[0] * q[0] + q[1] * q[1]);
+      double c = (r == 0.0) ? 1.0 : q[0] / r, s = (r == 0.0) ? 0.0 : q[1] / r;
+      return B[0] + B[1] * c + B[2] * s + B[3] * (c * c - s * s) + B[4] * (2.0 * c * s);
+    }
+    case WOS_BND_FOURIER: {
+      const int M = (int)B[0];
+      double t = atan2(q[1], q[0]);
+      double g = B[1];
+      for (int m = 1; m <= M; ++m) g += B[1 + m] * cos(m * t) + B[1 + M + m] * sin(m * t);
+      return g;
+    }
+    case WOS_BND_SQUARE_ARCSINE: {
+      double x0 = B[0], y0 = B[1], side = B[2];
+      const int M = (int)B[3];
+      double u = (q[0] - x0) / side, v = (q[1] - y0) / side;
+      /* nearest edge of the unit square in (u, v); CCW arc length in units of side */
+      double db = fabs(v), dr = fabs(1.0 - u), dt = fabs(1.0 - v), dl = fabs(u);
+      double s;
+      if (db <= dr && db <= dt && db <= dl) s = u;
+      else if (dr <= dt && dr <= dl) s = 1.0 + v;
+      else if (dt <= dl) s = 2.0 + (1.0 - u);
+      else s = 3.0 + (1.0 - v);
+      double g = 0.0;
+      for (int m = 1; m <= M; ++m) g += B[3 + m] * sin(TWO_PI * m * s / 4.0);
+      return g;
+    }
+    case WOS_BND_QUADRATIC:
+      return B[0] * q[0] * q[0] + B[1] * q[1] * q[1] + B[2] * q[0] * q[1] + B[3] * q[0] +
+             B[4] * q[1] + B[5];
+    default:
+      return 0.0;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* One reference-form trajectory (walker.py:257-314)                   */
+/* ------------------------------------------------------------------ */
+static void walk_ref_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
+                         double sgn, uint64_t seed, double eps, int64_t max_steps,
+                         double* value, int64_t* steps, uint8_t* hit) {
+  const int dim = pb->dim;
+  const int has_src = pb->src_kind != WOS_SRC_NONE;
+  const uint64_t k0 = seed, k1 = pb->instance_key;
+  double x[3] = {0, 0, 0}, q[3], acc = 0.0;
+  for (int i = 0; i < dim; ++i) x[i] = x0[i];
+  for (int64_t step = 0;; ++step) {
+    double d = query(pb, x, q);
+    int shell = d < eps;
+    if (shell || step >= max_steps) { /* walker.py:275-281 */
+      *value = acc + boundary(pb, q);
+      *steps = step;
+      *hit = (uint8_t)shell;
+      return;
+    }
+    uint64_t draw = 2 * (uint64_t)step;
+    uint64_t c[4] = {draw, pid, tid, 0}, w[4];
+    philox4x64(c, k0, k1, w); /* walker.py:289 */
+    double dir[3];
+    if (dim == 2) {
+      double theta = TWO_PI * u53(w[0]); /* _sphere_dirs_2d, walker.py:245-247 */
+      dir[0] = cos(theta);
+      dir[1] = sin(theta);
+      if (has_src) { /* walker.py:292-298 */
+        double u_rad = nonzero_u(u53(w[2]), draw, pid, tid, k0, k1);
+        double rad = d * sqrt(u_rad);
+        double phi = TWO_PI * u53(w[1]);
+        double g[2] = {x[0] + sgn * rad * cos(phi), x[1] + sgn * rad * sin(phi)};
+        double green = INV_TWO_PI * log(d / rad);
+        acc -= PI * d * d * source(pb, g) * green;
+      }
+    } else {
+      double z = 2.0 * u53(w[0]) - 1.0; /* _sphere_dirs_3d, walker.py:250-254 */
+      double s = sqrt(fmax(0.0, 1.0 - z * z));
+      double phi = TWO_PI * u53(w[1]);
+      dir[0] = s * cos(phi);
+      dir[1] = s * sin(phi);
+      dir[2] = z;
+      if (has_src) { /* walker.py:300-311 */
+        uint64_t cb[4] = {draw + 1, pid, tid, 0}, wb[4];
+        philox4x64(cb, k0, k1, wb);
+        double u_rad = nonzero_u(u53(wb[0]), draw + 1, pid, tid, k0, k1);
+        double rad = d * cbrt(u_rad);
+        double vz = 2.0 * u53(w[2]) - 1.0;
+        double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
+        double vphi = TWO_PI * u53(w[3]);
+        double g[3] = {x[0] + sgn * rad * (vs * cos(vphi)), x[1] + sgn * rad * (vs * sin(vphi)),
+                       x[2] + sgn * rad * vz};
+        double green = INV_FOUR_PI * (1.0 / rad - 1.0 / d);
+        double vol = (4.0 / 3.0) * PI * pow(d, 3.0);
+        acc -= vol * source(pb, g) * green;
+      }
+    }
+    for (int i = 0; i < dim; ++i) x[i] += sgn * d * dir[i]; /* walker.py:312 */
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* One NATIVE_F32-form trajectory, fp64 arithmetic                     */
+/* ------------------------------------------------------------------ */
+static double u23(uint32_t w) { return (double)(w >> 9) * (1.0 / 8388608.0); }
+
+void oracle_native_keys(uint64_t seed, uint64_t ikey, uint32_t* k0, uint32_t* k1) {
+  *k0 = (uint32_t)seed;
+  *k1 = (uint32_t)(seed >> 32) ^ (uint32_t)ikey ^ ((uint32_t)(ikey >> 32) * 0x9E3779B9u);
+}
+
+static double med3(double a, double b, double c) {
+  double lo = fmin(a, b), hi = fmax(a, b);
+  return fmax(lo, fmin(hi, c));
+}
+
+static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
+                            double sgn, uint64_t seed, double eps, int64_t max_steps,
+                            double* value, int64_t* steps, uint8_t* hit) {
+  const int dim = pb->dim;
+  const int has_src = pb->src_kind != WOS_SRC_NONE;
+  uint32_t k0, k1;
+  oracle_native_keys(seed, pb->instance_key, &k0, &k1);
+  const uint32_t c1 = (uint32_t)pid, c2 = (uint32_t)tid;
+  const uint32_t c3 = (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu);
+  double x[3] = {0, 0, 0}, q[3], acc = 0.0;
+  for (int i = 0; i < dim; ++i) x[i] = x0[i];
+  for (int64_t step = 0;; ++step) {
+    double d = query(pb, x, q);
+    int shell = d < eps;
+    if (shell || step >= max_steps) {
+      *value = acc + boundary(pb, q);
+      *steps = step;
+      *hit = (uint8_t)shell;
+      return;
+    }
+    /* block A = Philox4x32(2*step, ...), block B = Philox4x32(2*step+1, ...) (3D source only) */
+    uint32_t u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    {
+      uint32_t ca[4] = {(uint32_t)(2 * step), c1, c2, c3};
+      philox4x32(ca, k0, k1, u);
+      if (dim == 3 && has_src) {
+        uint32_t cb[4] = {(uint32_t)(2 * step + 1), c1, c2, c3};
+        philox4x32(cb, k0, k1, u + 4);
+      }
+    }
+    double dir[3];
+    if (dim == 2) {
+      double th = TWO_PI * u23(u[0]);
+      dir[0] = cos(th);
+      dir[1] = sin(th);
+      if (has_src) {
+        double phi = TWO_PI * u23(u[1]);
+        double r = d * sqrt(u23(u[2]) * u23(u[3]));
+        double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
+        acc -= (d * d * 0.25) * source(pb, g);
+      }
+    } else {
+      double z = 2.0 * u23(u[0]) - 1.0;
+      double s = sqrt(fmax(0.0, 1.0 - z * z));
+      double phi = TWO_PI * u23(u[1]);
+      dir[0] = s * cos(phi);
+      dir[1] = s * sin(phi);
+      dir[2] = z;
+      if (has_src) {
+        double vz = 2.0 * u23(u[2]) - 1.0;
+        double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
+        double vphi = TWO_PI * u23(u[3]);
+        double r = d * med3(u23(u[4]), u23(u[5]), u23(u[6]));
+        double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
+                       x[2] + sgn * r * vz};
+        acc -= (d * d * (1.0 / 6.0)) * source(pb, g);
+      }
+    }
+    for (int i = 0; i < dim; ++i) x[i] += sgn * d * dir[i];
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* Threaded drivers                                                     */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const wos_problem* pb;
+  int native;
+  int64_t lo, hi;
+  const double* pts;
+  const uint64_t *pid, *tid;
+  const double* sgn;
+  uint64_t seed;
+  double eps;
+  int64_t max_steps;
+  double* values;
+  int64_t* steps;
+  uint8_t* hits;
+} rows_job;
+
+static void* rows_worker(void* arg) {
+  rows_job* j = (rows_job*)arg;
+  const int dim = j->pb->dim;
+  for (int64_t i = j->lo; i < j->hi; ++i) {
+    if (j->native)
+      walk_native_one(j->pb, j->pts + dim * i, j->pid[i], j->tid[i], j->sgn[i], j->seed, j->eps,
+                      j->max_steps, j->values + i, j->steps + i, j->hits + i);
+    else
+      walk_ref_one(j->pb, j->pts + dim * i, j->pid[i], j->tid[i], j->sgn[i], j->seed, j->eps,
+                   j->max_steps, j->values + i, j->steps + i, j->hits + i);
+  }
+  return NULL;
+}
+
+static int run_rows(const wos_problem* pb, int native, int64_t n, const double* pts,
+                    const uint64_t* pid, const uint64_t* tid, const double* sgn, uint64_t seed,
+                    double eps, int64_t max_steps, double* values, int64_t* steps, uint8_t* hits,
+                    int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  rows_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    rows_job j = {pb, native, n * t / nthreads, n * (t + 1) / nthreads, pts, pid, tid, sgn,
+                  seed, eps, max_steps, values, steps, hits};
+    jobs[t] = j;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, rows_worker, &jobs[t]);
+  rows_worker(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}
+
+/* walker.walk_poisson_values on the reference form (walker.py:181-229, generic path) */
+int oracle_walk_rows(const wos_problem* pb, int64_t n, const double* pts, const uint64_t* pid,
+                     const uint64_t* tid, const double* sgn, uint64_t seed, double eps,
+                     int64_t max_steps, double* values, int64_t* steps, uint8_t* hits,
+                     int nthreads) {
+  return run_rows(pb, 0, n, pts, pid, tid, sgn, seed, eps, max_steps, values, steps, hits,
+                  nthreads);
+}
+
+int oracle_walk_rows_native(const wos_problem* pb, int64_t n, const double* pts,
+                            const uint64_t* pid, const uint64_t* tid, const double* sgn,
+                            uint64_t seed, double eps, int64_t max_steps, double* values,
+                            int64_t* steps, uint8_t* hits, int nthreads) {
+  return run_rows(pb, 1, n, pts, pid, tid, sgn, seed, eps, max_steps, values, steps, hits,
+                  nthreads);
+}
+
+typedef struct {
+  const wos_problem* pbs;
+  int native;
+  int64_t lo, hi;
+  const double* pts;
+  const int64_t* pid;
+  const int32_t* inst;
+  int64_t L;
+  uint64_t traj_start;
+  int antithetic;
+  uint64_t seed;
+  double eps;
+  int64_t max_steps;
+  double *mean, *m2;
+  uint64_t total_steps;
+} est_job;
+
+static void* est_worker(void* arg) {
+  est_job* j = (est_job*)arg;
+  const int64_t L = j->L;
+  double* v = (double*)malloc(sizeof(double) * (size_t)L);
+  uint64_t tot = 0;
+  for (int64_t p = j->lo; p < j->hi; ++p) {
+    const wos_problem* pb = j->pbs + (j->inst ? j->inst[p] : 0);
+    const double* x0 = j->pts + pb->dim * p;
+    for (int64_t r = 0; r < L; ++r) {
+      uint64_t tid = j->antithetic ? j->traj_start + 2 * (uint64_t)(r / 2) : j->traj_start + (uint64_t)r;
+      double sgn = (j->antithetic && (r & 1)) ? -1.0 : 1.0;
+      int64_t st;
+      uint8_t h;
+      if (j->native)
+        walk_native_one(pb, x0, (uint64_t)j->pid[p], tid, sgn, j->seed, j->eps, j->max_steps,
+                        v + r, &st, &h);
+      else
+        walk_ref_one(pb, x0, (uint64_t)j->pid[p], tid, sgn, j->seed, j->eps, j->max_steps, v + r,
+                     &st, &h);
+      tot += (uint64_t)st;
+    }
+    int64_t n = L;
+    if (j->antithetic) { /* estimator.py:137-139: pair means */
+      n = L / 2;
+      for (int64_t k = 0; k < n; ++k) v[k] = (v[2 * k] + v[2 * k + 1]) / 2.0;
+    }
+    double s = 0.0; /* PointEstimate.from_values, estimator.py:106-110 */
+    for (int64_t k = 0; k < n; ++k) s += v[k];
+    double mean = s / (double)n, m2 = 0.0;
+    for (int64_t k = 0; k < n; ++k) m2 += (v[k] - mean) * (v[k] - mean);
+    j->mean[p] = mean;
+    j->m2[p] = m2;
+  }
+  free(v);
+  j->total_steps = tot;
+  return NULL;
+}
+
+/* estimator.estimate (estimator.py:144-181) over a multi-instance point list */
+int oracle_estimate(const wos_problem* pbs, int native, int64_t P, const double* pts,
+                    const int64_t* pid, const int32_t* inst, int64_t L, uint64_t traj_start,
+                    int antithetic, uint64_t seed, double eps, int64_t max_steps, double* mean,
+                    double* m2, uint64_t* total_steps, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  est_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    est_job j = {pbs, native, P * t / nthreads, P * (t + 1) / nthreads, pts, pid, inst, L,
+                 traj_start, antithetic, seed, eps, max_steps, mean, m2, 0};
+    jobs[t] = j;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, est_worker, &jobs[t]);
+  est_worker(&jobs[0]);
+  uint64_t tot = jobs[0].total_steps;
+  for (int t = 1; t < nthreads; ++t) {
+    pthread_join(th[t], NULL);
+    tot += jobs[t].total_steps;
+  }
+  if (total_steps) *total_steps = tot;
+  return 0;
+}

@@ -1,0 +1,48 @@
+"""B200-native Walk-on-Spheres label estimator (hot path of arxiv 2603.01193).
+
+Drop-in for the reference package ``spherewalk``'s estimator path:
+``WalkConfig``, ``Problem``, ``walk_poisson_values``, ``walk_poisson``,
+``walk_poisson_antithetic``, ``estimate``, ``PointEstimate`` — backed by
+hand-written sm_100a CUDA kernels in ``libwos_b200.so`` behind the C ABI of
+``include/wos_b200.h``. There is no CPU fallback.
+"""
+
+from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, estimate_tensors
+from .engine import UnsupportedProblemError
+from .geometry import BallDomain, BoxDomain, ExteriorQueryError, PolygonDomain, star_polygon
+from .walker import (
+    TERM_BOUNDARY,
+    TERM_MAX_STEPS,
+    Problem,
+    TrajectoryResult,
+    TrajectoryStream,
+    WalkConfig,
+    walk_poisson,
+    walk_poisson_antithetic,
+    walk_poisson_values,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BallDomain",
+    "BoxDomain",
+    "ExteriorQueryError",
+    "PointEstimate",
+    "PolygonDomain",
+    "Problem",
+    "TERM_BOUNDARY",
+    "TERM_MAX_STEPS",
+    "TrajectoryResult",
+    "TrajectoryStream",
+    "UnsupportedProblemError",
+    "WalkConfig",
+    "chan_merge",
+    "estimate",
+    "estimate_arrays",
+    "estimate_tensors",
+    "star_polygon",
+    "walk_poisson",
+    "walk_poisson_antithetic",
+    "walk_poisson_values",
+]

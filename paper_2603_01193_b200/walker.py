@@ -1,0 +1,196 @@
+"""Walk-on-spheres trajectories on the GPU — drop-in for ``spherewalk.walker``.
+
+Same names, arguments, return values and errors as the reference
+(``walker.py:55-116, 181-229, 426-462``); the walk itself runs in the sm_100a
+kernels of libwos_b200.so. Problems must be spec-coded (``boundary_spec`` /
+``source_spec`` plus a Ball/Box/Polygon domain); others raise
+``UnsupportedProblemError`` instead of falling back to a CPU path.
+
+``WalkConfig`` gains one field, ``mode``:
+
+* ``"replay"`` (= ``"replay_f64"``): the reference's own estimator and Philox4x64
+  draws, fp64 arithmetic — walk-for-walk equal to ``spherewalk`` within rounding.
+* ``"replay_f32"``: the same draws, fp32 arithmetic.
+* ``"native"``: the production estimator (Philox4x32, Green's-function importance
+  sampling, fp32 fast math) — statistically equal, much faster. Default.
+"""
+
+from __future__ import annotations
+
+from ctypes import byref, c_int64
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import (
+    ProblemSet,
+    UnsupportedProblemError,
+    get_context,
+    mode_code,
+    raise_exterior,
+    walk_config_struct,
+)
+from .geometry import ExteriorQueryError
+
+__all__ = [
+    "WalkConfig",
+    "TrajectoryResult",
+    "TrajectoryStream",
+    "Problem",
+    "UnsupportedProblemError",
+    "TERM_BOUNDARY",
+    "TERM_MAX_STEPS",
+    "walk_poisson",
+    "walk_poisson_antithetic",
+    "walk_poisson_values",
+]
+
+TERM_BOUNDARY = "boundary"
+TERM_MAX_STEPS = "max_steps"
+
+
+@dataclass(frozen=True)
+class WalkConfig:
+    """Knobs shared by every walker (walker.py:55-79) plus the numeric mode."""
+
+    eps_shell: float | None = None
+    max_steps: int = 1000
+    antithetic: bool = False
+    sigma_bar: float | None = None
+    rng_seed: int = 0
+    mode: str = "native"
+
+    def __post_init__(self):
+        if self.eps_shell is not None and self.eps_shell <= 0.0:
+            raise ValueError("eps_shell must be positive")
+        if self.max_steps < 1:
+            raise ValueError("max_steps must be at least 1")
+        mode_code(self.mode)
+
+    def resolve_eps(self, domain) -> float:
+        if self.eps_shell is not None:
+            return self.eps_shell
+        return 1.0e-3 * domain.bounding_radius()
+
+
+@dataclass(frozen=True)
+class TrajectoryResult:
+    value: float
+    steps_taken: int
+    terminated_by: str
+
+
+@dataclass(frozen=True)
+class TrajectoryStream:
+    """Which substream of the seed a trajectory draws from (walker.py:89-99)."""
+
+    point_id: int = 0
+    traj_id: int = 0
+    sign: float = 1.0
+
+
+@dataclass(frozen=True)
+class Problem:
+    """A Poisson problem: domain, boundary g, optional source f (walker.py:102-116).
+
+    ``boundary``/``source`` callables are accepted for signature compatibility
+    but the GPU walker reads only the ``*_spec`` codes.
+    """
+
+    domain: object
+    boundary: object = None
+    source: object = None
+    instance_key: int = 0
+    boundary_spec: tuple | None = None
+    source_spec: tuple | None = None
+
+
+def _cfg_of(cfg):
+    return cfg if cfg is not None else WalkConfig()
+
+
+def _streams_as_arrays(point_ids, traj_ids, signs, n):
+    # walker.py:139-145
+    pid = np.ascontiguousarray(np.asarray(point_ids).astype(np.int64).astype(np.uint64))
+    tid = np.ascontiguousarray(np.asarray(traj_ids).astype(np.int64).astype(np.uint64))
+    sgn = np.ascontiguousarray(np.asarray(signs, dtype=np.float64))
+    if not (pid.shape == tid.shape == sgn.shape == (n,)):
+        raise ValueError("stream arrays must match the number of start points")
+    return pid, tid, sgn
+
+
+def walk_poisson_values(inst, points, point_ids, traj_ids, signs, cfg):
+    """Values, step counts, and boundary-hit flags for a batch of walks.
+
+    One row per trajectory: points[i] walked under stream
+    (point_ids[i], traj_ids[i], signs[i]) — walker.py:181-229. Returns
+    (values float64 (n,), steps int64 (n,), hits uint8 (n,)).
+    """
+    inst = getattr(inst, "problem", inst)
+    cfg = _cfg_of(cfg)
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    if pts.ndim != 2:
+        raise ValueError("points must be an (n, d) array")
+    n = pts.shape[0]
+    pid, tid, sgn = _streams_as_arrays(point_ids, traj_ids, signs, n)
+    ctx = get_context()
+    pset = ProblemSet(ctx, [inst])
+    if pts.shape[1] != pset.dim:
+        raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
+    wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode, cfg.rng_seed)
+    values = np.empty(n, dtype=np.float64)
+    steps = np.empty(n, dtype=np.int64)
+    hits = np.empty(n, dtype=np.uint8)
+    if n:
+        _lib.check(
+            ctx._lib.wos_walk_rows_host(
+                ctx.handle, pset.handle, byref(wc), n, pts.ctypes.data, pid.ctypes.data,
+                tid.ctypes.data, sgn.ctypes.data, values.ctypes.data, steps.ctypes.data,
+                hits.ctypes.data,
+            )
+        )
+    return values, steps, hits
+
+
+def _require_interior(inst, xi):
+    """walker.py:426-428, evaluated on the GPU (wos_check_interior)."""
+    ctx = get_context()
+    pset = ProblemSet(ctx, [inst])
+    pts = np.ascontiguousarray(np.asarray(xi, dtype=np.float64).reshape(1, -1))
+    if pts.shape[1] != pset.dim:
+        raise ValueError(f"expected a point of dimension {pset.dim}")
+    first = c_int64(-1)
+    _lib.check(
+        ctx._lib.wos_check_interior_host(ctx.handle, pset.handle, 1, pts.ctypes.data, None, byref(first))
+    )
+    raise_exterior(pts, first.value)
+
+
+def _as_result(values, steps, hits, i=0):
+    term = TERM_BOUNDARY if hits[i] else TERM_MAX_STEPS
+    return TrajectoryResult(float(values[i]), int(steps[i]), term)
+
+
+def walk_poisson(inst, xi, cfg, stream: TrajectoryStream | None = None) -> TrajectoryResult:
+    """One walk-on-spheres trajectory from the interior point xi (walker.py:436-444)."""
+    inst = getattr(inst, "problem", inst)
+    _require_interior(inst, xi)
+    s = stream or TrajectoryStream()
+    out = walk_poisson_values(
+        inst, np.asarray(xi, dtype=np.float64)[None, :], [s.point_id], [s.traj_id], [s.sign], cfg
+    )
+    return _as_result(*out)
+
+
+def walk_poisson_antithetic(inst, xi, cfg, stream: TrajectoryStream | None = None):
+    """A mirrored pair of trajectories sharing one random stream (walker.py:447-462)."""
+    inst = getattr(inst, "problem", inst)
+    _require_interior(inst, xi)
+    s = stream or TrajectoryStream()
+    p = np.asarray(xi, dtype=np.float64)[None, :].repeat(2, axis=0)
+    out = walk_poisson_values(inst, p, [s.point_id] * 2, [s.traj_id] * 2, [1.0, -1.0], cfg)
+    return _as_result(*out, i=0), _as_result(*out, i=1)
+
+
+__all__ += ["ExteriorQueryError"]
