@@ -1,0 +1,918 @@
+// C ABI of libwos_b200.so (include/wos_b200.h): contexts, problem sets,
+// launches of the persistent walk kernel, RNG known-answer kernels, interior
+// check and the roofline probes.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/wos_b200.h"
+#include "wos_kernels.h"
+#include "wos_rng.cuh"
+#include "wos_types.h"
+
+using namespace wos;
+
+// ------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(WOS_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),   \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// ------------------------------------------------------------------------
+// context and problem set
+// ------------------------------------------------------------------------
+constexpr int kCounterRing = 256;
+
+struct wos_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;          // private stream of the *_host entry points
+  unsigned int* d_counters = nullptr;     // work counters, one per launch slot
+  std::atomic<unsigned> next_counter{0};
+  unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
+  unsigned long long* d_steps = nullptr;     // total-steps scratch of the *_host variants
+  int64_t host_exterior = -1;
+  void* d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int refill_min = 2;
+  int blocks_per_sm = 0;
+  std::mutex mu;  // serialises the *_host entry points' scratch
+};
+
+struct wos_problem_set {
+  wos_context* ctx = nullptr;
+  int n = 0, dim = 0, dom_kind = 0, src_kind = 0, bnd_kind = 0;
+  int sine_K = 0;   // padded sine order of the tables
+  int sine_K_native = 0, sk_native = 0;
+  int bnd_M = 0;
+  int stride = 0, bnd_off = 0;            // Real elements per row, boundary offset
+  size_t bytes_d = 0, bytes_f = 0;        // padded table bytes
+  double* d_table_d = nullptr;
+  float* d_table_f = nullptr;             // REPLAY_F32 table (replay layout, float)
+  float* d_table_n = nullptr;             // NATIVE table (native layout, float)
+  InstHdr* d_hdr = nullptr;
+  double* d_segs_d = nullptr;             // [nseg][ax, ay, ex, ey]
+  float* d_segs_f = nullptr;              // REPLAY_F32: same, float
+  float4* d_segs_n = nullptr;             // NATIVE: [nseg][2] float4
+};
+
+extern "C" int wos_abi_version(void) { return WOS_ABI_VERSION; }
+extern "C" const char* wos_last_error(void) { return g_err; }
+
+extern "C" int wos_context_create(int32_t device, wos_context** out) {
+  if (!out) return fail(WOS_ERR_INVALID, "null output pointer");
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(WOS_ERR_INVALID, "device %d out of range (%d)", device, n);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(WOS_ERR_UNSUPPORTED, "device %d is sm_%d%d; libwos_b200 is built for sm_100a",
+                device, prop.major, prop.minor);
+  wos_context* c = new wos_context();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, sizeof(unsigned) * kCounterRing);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_exterior, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_exterior, 0xff, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(WOS_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return WOS_OK;
+}
+
+extern "C" void wos_context_destroy(wos_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaFree(c->d_counters);
+  cudaFree(c->d_exterior);
+  cudaFree(c->d_steps);
+  cudaFree(c->d_scratch);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+extern "C" int wos_set_tuning(wos_context* c, int32_t refill_min, int32_t blocks_per_sm) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (refill_min < 1 || refill_min > 32) return fail(WOS_ERR_INVALID, "refill_min must be 1..32");
+  if (blocks_per_sm < 0 || blocks_per_sm > 32) return fail(WOS_ERR_INVALID, "blocks_per_sm must be 0..32");
+  c->refill_min = refill_min;
+  c->blocks_per_sm = blocks_per_sm;
+  return WOS_OK;
+}
+
+static int need(int got, int want, const char* what) {
+  if (got != want) return fail(WOS_ERR_INVALID, "%s expects %d parameters, got %d", what, want, got);
+  return WOS_OK;
+}
+
+static int validate(const wos_problem& p) {
+  if (p.dim != 2 && p.dim != 3) return fail(WOS_ERR_INVALID, "dim must be 2 or 3");
+  int r;
+  switch (p.dom_kind) {
+    case WOS_DOM_BALL:
+      if ((r = need(p.n_dom, p.dim + 1, "ball domain"))) return r;
+      if (!(p.dom[p.dim] > 0.0)) return fail(WOS_ERR_INVALID, "ball radius must be positive");
+      break;
+    case WOS_DOM_BOX:
+      if ((r = need(p.n_dom, 2 * p.dim, "box domain"))) return r;
+      for (int i = 0; i < p.dim; ++i)
+        if (!(p.dom[p.dim + i] > p.dom[i])) return fail(WOS_ERR_INVALID, "box must have positive extent");
+      break;
+    case WOS_DOM_POLYGON: {
+      if (p.dim != 2) return fail(WOS_ERR_INVALID, "polygon domains are 2D");
+      if (p.n_dom < 7) return fail(WOS_ERR_INVALID, "polygon needs >= 3 vertices");
+      int nv = (int)p.dom[0];
+      if (nv < 3 || p.n_dom != 1 + 2 * nv) return fail(WOS_ERR_INVALID, "polygon parameter count mismatch");
+      break;
+    }
+    case WOS_DOM_POLAR:
+      return fail(WOS_ERR_UNSUPPORTED, "PolarDomain has no GPU encoding");
+    default:
+      return fail(WOS_ERR_UNSUPPORTED, "unknown domain kind %d", p.dom_kind);
+  }
+  switch (p.src_kind) {
+    case WOS_SRC_NONE:
+      break;
+    case WOS_SRC_CONST:
+      if ((r = need(p.n_src, 1, "constant source"))) return r;
+      break;
+    case WOS_SRC_RBF2:
+      if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "RBF2 source is 2D only");
+      if ((r = need(p.n_src, 6, "RBF2 source"))) return r;
+      break;
+    case WOS_SRC_SINE: {
+      if (p.n_src < 2) return fail(WOS_ERR_INVALID, "sine source needs [K, coeffs...]");
+      int K = (int)p.src[0];
+      if (K < 1 || K > 16) return fail(WOS_ERR_UNSUPPORTED, "sine order K must be 1..16");
+      int nc = p.dim == 2 ? K * K : K * K * K;
+      if ((r = need(p.n_src, 1 + nc, "sine source"))) return r;
+      break;
+    }
+    case WOS_SRC_GAUSS:
+      if ((r = need(p.n_src, 2 + p.dim, "Gaussian source"))) return r;
+      if (!(p.src[1] > 0.0)) return fail(WOS_ERR_INVALID, "Gaussian sigma must be positive");
+      break;
+    default:
+      return fail(WOS_ERR_UNSUPPORTED, "unknown source kind %d", p.src_kind);
+  }
+  switch (p.bnd_kind) {
+    case WOS_BND_CONST:
+      if ((r = need(p.n_bnd, 1, "constant boundary"))) return r;
+      break;
+    case WOS_BND_LINEAR:
+      if ((r = need(p.n_bnd, p.dim + 1, "linear boundary"))) return r;
+      break;
+    case WOS_BND_FOURIER5:
+      if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "FOURIER5 boundary is 2D only");
+      if ((r = need(p.n_bnd, 5, "FOURIER5 boundary"))) return r;
+      break;
+    case WOS_BND_FOURIER: {
+      if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "Fourier boundary is 2D only");
+      if (p.n_bnd < 2) return fail(WOS_ERR_INVALID, "Fourier boundary needs [M, b0, ...]");
+      int M = (int)p.bnd[0];
+      if (M < 0 || M > 64) return fail(WOS_ERR_UNSUPPORTED, "Fourier order must be 0..64");
+      if ((r = need(p.n_bnd, 2 + 2 * M, "Fourier boundary"))) return r;
+      break;
+    }
+    case WOS_BND_SQUARE_ARCSINE: {
+      if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "arc-length boundary is 2D only");
+      if (p.n_bnd < 4) return fail(WOS_ERR_INVALID, "arc-length boundary needs [x0, y0, side, M, ...]");
+      int M = (int)p.bnd[3];
+      if (M < 0 || M > 64) return fail(WOS_ERR_UNSUPPORTED, "arc-length order must be 0..64");
+      if ((r = need(p.n_bnd, 4 + M, "arc-length boundary"))) return r;
+      break;
+    }
+    case WOS_BND_QUADRATIC:
+      if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "quadratic boundary is 2D only");
+      if ((r = need(p.n_bnd, 6, "quadratic boundary"))) return r;
+      break;
+    default:
+      return fail(WOS_ERR_UNSUPPORTED, "unknown boundary kind %d", p.bnd_kind);
+  }
+  return WOS_OK;
+}
+
+static int sine_native_order(int dim, int K, int* sk) {
+  // specialised kernels exist for 2D K in {4, 8} and 3D K = 3; smaller K pads up
+  if (dim == 2 && K <= 4) { *sk = 4; return 4; }
+  if (dim == 2 && K <= 8) { *sk = 8; return 8; }
+  if (dim == 3 && K <= 3) { *sk = 3; return 3; }
+  *sk = 0;
+  return K;
+}
+
+static size_t pad16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs, int32_t n,
+                                      wos_problem_set** out) {
+  if (!ctx || !probs || !out) return fail(WOS_ERR_INVALID, "null argument");
+  if (n < 1) return fail(WOS_ERR_INVALID, "need at least one problem");
+  for (int i = 0; i < n; ++i) {
+    int r = validate(probs[i]);
+    if (r) return r;
+    if (probs[i].dim != probs[0].dim || probs[i].dom_kind != probs[0].dom_kind ||
+        probs[i].src_kind != probs[0].src_kind || probs[i].bnd_kind != probs[0].bnd_kind)
+      return fail(WOS_ERR_INVALID, "a problem set needs one dimension and one domain/source/boundary kind");
+  }
+  const int dim = probs[0].dim;
+  wos_problem_set* s = new wos_problem_set();
+  s->ctx = ctx;
+  s->n = n;
+  s->dim = dim;
+  s->dom_kind = probs[0].dom_kind;
+  s->src_kind = probs[0].src_kind;
+  s->bnd_kind = probs[0].bnd_kind;
+  // uniform orders over the set (zero padding is exact)
+  int K = 0, M = 0;
+  for (int i = 0; i < n; ++i) {
+    if (s->src_kind == WOS_SRC_SINE) K = std::max(K, (int)probs[i].src[0]);
+    if (s->bnd_kind == WOS_BND_FOURIER) M = std::max(M, (int)probs[i].bnd[0]);
+    if (s->bnd_kind == WOS_BND_SQUARE_ARCSINE) M = std::max(M, (int)probs[i].bnd[3]);
+  }
+  int sk = 0;
+  int Kn = (s->src_kind == WOS_SRC_SINE) ? sine_native_order(dim, K, &sk) : 0;
+  const int Kt = std::max(K, Kn);  // table order (native may pad higher)
+  s->sine_K = K;
+  s->sine_K_native = Kn;
+  s->sk_native = sk;
+  s->bnd_M = M;
+  int ns = 0;
+  switch (s->src_kind) {
+    case WOS_SRC_CONST: ns = 1; break;
+    case WOS_SRC_RBF2: ns = 6; break;
+    case WOS_SRC_SINE: ns = dim == 2 ? Kt * Kt : Kt * Kt * Kt; break;
+    case WOS_SRC_GAUSS: ns = 2 + dim; break;
+    default: ns = 0;
+  }
+  int nb = 0;
+  switch (s->bnd_kind) {
+    case WOS_BND_CONST: nb = 1; break;
+    case WOS_BND_LINEAR: nb = dim + 1; break;
+    case WOS_BND_FOURIER5: nb = 5; break;
+    case WOS_BND_FOURIER: nb = 2 + 2 * M; break;
+    case WOS_BND_SQUARE_ARCSINE: nb = 4 + M; break;
+    case WOS_BND_QUADRATIC: nb = 6; break;
+  }
+  s->bnd_off = kSrcOff + ns;
+  s->stride = (kSrcOff + ns + nb + 3) & ~3;
+  const int stride = s->stride;
+  std::vector<double> td((size_t)n * stride, 0.0);   // replay layout
+  std::vector<float> tn((size_t)n * stride, 0.0f);   // native layout
+  std::vector<InstHdr> hd(n);
+  std::vector<double> segd;
+  std::vector<float4> segn;
+  for (int i = 0; i < n; ++i) {
+    const wos_problem& p = probs[i];
+    double* rd = td.data() + (size_t)i * stride;
+    float* rn = tn.data() + (size_t)i * stride;
+    memset(&hd[i], 0, sizeof(InstHdr));
+    hd[i].ikey = p.instance_key;
+    hd[i].nkey1 = (uint32_t)p.instance_key ^ ((uint32_t)(p.instance_key >> 32) * 0x9E3779B9u);
+    // domain
+    if (p.dom_kind == WOS_DOM_BALL) {
+      for (int k = 0; k < dim; ++k) rd[k] = p.dom[k];
+      rd[3] = p.dom[dim];
+    } else if (p.dom_kind == WOS_DOM_BOX) {
+      for (int k = 0; k < dim; ++k) {
+        rd[k] = p.dom[k];
+        rd[4 + k] = p.dom[dim + k];
+      }
+    } else {
+      const int nv = (int)p.dom[0];
+      const double* V = p.dom + 1;
+      hd[i].seg_off = (int)(segd.size() / 4);
+      hd[i].n_seg = nv;
+      for (int k = 0; k < nv; ++k) {
+        const int j = (k + 1 == nv) ? 0 : k + 1;
+        const double ax = V[2 * k], ay = V[2 * k + 1];
+        const double ex = V[2 * j] - ax, ey = V[2 * j + 1] - ay;
+        segd.push_back(ax);
+        segd.push_back(ay);
+        segd.push_back(ex);
+        segd.push_back(ey);
+        const double l2 = ex * ex + ey * ey;
+        segn.push_back(make_float4((float)ax, (float)ay, (float)ex, (float)ey));
+        segn.push_back(make_float4((float)(ex / l2), (float)(ey / l2), 0.f, 0.f));
+      }
+    }
+    for (int k = 0; k < 8; ++k) rn[k] = (float)rd[k];
+    // source
+    double* sd = rd + kSrcOff;
+    float* sn = rn + kSrcOff;
+    switch (p.src_kind) {
+      case WOS_SRC_CONST:
+        sd[0] = p.src[0];
+        break;
+      case WOS_SRC_RBF2:
+        for (int k = 0; k < 6; ++k) sd[k] = p.src[k];
+        break;
+      case WOS_SRC_SINE: {
+        const int Ki = (int)p.src[0];
+        const double* a = p.src + 1;
+        if (dim == 2) {
+          for (int k = 0; k < Ki; ++k)
+            for (int l = 0; l < Ki; ++l) {
+              sd[k * K + l] = a[k * Ki + l];   // replay: order K
+              sn[k * Kn + l] = (float)a[k * Ki + l];  // native: order Kn
+            }
+        } else {
+          for (int k = 0; k < Ki; ++k)
+            for (int l = 0; l < Ki; ++l)
+              for (int m = 0; m < Ki; ++m) {
+                sd[(k * K + l) * K + m] = a[(k * Ki + l) * Ki + m];
+                sn[(k * Kn + l) * Kn + m] = (float)a[(k * Ki + l) * Ki + m];
+              }
+        }
+        break;
+      }
+      case WOS_SRC_GAUSS:
+        for (int k = 0; k < 2 + dim; ++k) sd[k] = p.src[k];
+        break;
+    }
+    if (p.src_kind != WOS_SRC_SINE)
+      for (int k = 0; k < ns; ++k) sn[k] = (float)sd[k];
+    if (p.src_kind == WOS_SRC_GAUSS) sn[1] = (float)(1.4426950408889634 / (2.0 * p.src[1] * p.src[1]));
+    // boundary (orders padded to the set maximum)
+    double* bd = rd + s->bnd_off;
+    switch (p.bnd_kind) {
+      case WOS_BND_FOURIER: {
+        const int Mi = (int)p.bnd[0];
+        bd[0] = M;
+        bd[1] = p.bnd[1];
+        for (int m = 1; m <= Mi; ++m) {
+          bd[1 + m] = p.bnd[1 + m];
+          bd[1 + M + m] = p.bnd[1 + Mi + m];
+        }
+        break;
+      }
+      case WOS_BND_SQUARE_ARCSINE: {
+        const int Mi = (int)p.bnd[3];
+        bd[0] = p.bnd[0];
+        bd[1] = p.bnd[1];
+        bd[2] = p.bnd[2];
+        bd[3] = M;
+        for (int m = 1; m <= Mi; ++m) bd[3 + m] = p.bnd[3 + m];
+        break;
+      }
+      default:
+        for (int k = 0; k < p.n_bnd; ++k) bd[k] = p.bnd[k];
+    }
+    for (int k = 0; k < nb; ++k) rn[s->bnd_off + k] = (float)bd[k];
+  }
+  std::vector<float> tf(td.size());
+  for (size_t k = 0; k < td.size(); ++k) tf[k] = (float)td[k];
+  std::vector<float> segf(segd.size());
+  for (size_t k = 0; k < segd.size(); ++k) segf[k] = (float)segd[k];
+
+  s->bytes_d = pad16(td.size() * sizeof(double));
+  s->bytes_f = pad16(tn.size() * sizeof(float));
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_table_d, s->bytes_d);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_table_f, s->bytes_f);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_table_n, s->bytes_f);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_hdr, sizeof(InstHdr) * n);
+  if (e == cudaSuccess) e = cudaMemset(s->d_table_d, 0, s->bytes_d);
+  if (e == cudaSuccess) e = cudaMemset(s->d_table_f, 0, s->bytes_f);
+  if (e == cudaSuccess) e = cudaMemset(s->d_table_n, 0, s->bytes_f);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_table_d, td.data(), td.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_table_f, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_table_n, tn.data(), tn.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_hdr, hd.data(), sizeof(InstHdr) * n, cudaMemcpyHostToDevice);
+  if (!segd.empty()) {
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_d, segd.size() * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_f, segf.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_n, segn.size() * sizeof(float4));
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_segs_d, segd.data(), segd.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_segs_f, segf.data(), segf.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->d_segs_n, segn.data(), segn.size() * sizeof(float4), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    wos_problem_set_destroy(s);
+    return fail(WOS_ERR_CUDA, "problem set upload: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return WOS_OK;
+}
+
+extern "C" void wos_problem_set_destroy(wos_problem_set* s) {
+  if (!s) return;
+  cudaSetDevice(s->ctx->device);
+  cudaFree(s->d_table_d);
+  cudaFree(s->d_table_f);
+  cudaFree(s->d_table_n);
+  cudaFree(s->d_hdr);
+  cudaFree(s->d_segs_d);
+  cudaFree(s->d_segs_f);
+  cudaFree(s->d_segs_n);
+  delete s;
+}
+
+// ------------------------------------------------------------------------
+// interior check (geometry.*.contains; oracle_contains in oracle/wos_oracle.c)
+// ------------------------------------------------------------------------
+__global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
+                                    const int32_t* __restrict__ inst, const double* __restrict__ table,
+                                    int stride, const InstHdr* __restrict__ hdr,
+                                    const double* __restrict__ segs, int dim, int dom_kind,
+                                    unsigned long long* first) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = inst ? inst[p] : 0;
+    const double* row = table + (size_t)i * stride;
+    const double* x = pts + (size_t)p * dim;
+    bool inside = true;
+    if (dom_kind == WOS_DOM_BALL) {
+      double s = 0.0;
+      for (int k = 0; k < dim; ++k) s += (x[k] - row[k]) * (x[k] - row[k]);
+      inside = sqrt(s) < row[3];
+    } else if (dom_kind == WOS_DOM_BOX) {
+      for (int k = 0; k < dim; ++k) inside = inside && (x[k] > row[k]) && (x[k] < row[4 + k]);
+    } else {
+      const InstHdr h = hdr[i];
+      const double* S = segs + 4 * (size_t)h.seg_off;
+      bool in = false;
+      for (int k = 0; k < h.n_seg; ++k) {
+        const double ax = S[4 * k], ay = S[4 * k + 1];
+        const double bx = ax + S[4 * k + 2], by = ay + S[4 * k + 3];
+        if ((ay > x[1]) != (by > x[1])) {
+          const double xc = ax + (x[1] - ay) * (bx - ax) / (by - ay);
+          if (x[0] < xc) in = !in;
+        }
+      }
+      inside = in;
+    }
+    if (!inside) atomicMin(first, (unsigned long long)p);
+  }
+}
+
+static int launch_interior(wos_context* c, const wos_problem_set* s, int64_t n, const double* pts,
+                           const int32_t* inst, cudaStream_t st) {
+  if (n <= 0) return WOS_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->num_sms * 8);
+  wos_interior_kernel<<<blocks, 256, 0, st>>>(n, pts, inst, s->d_table_d, s->stride, s->d_hdr,
+                                              s->d_segs_d, s->dim, s->dom_kind, c->d_exterior);
+  CUDA_TRY(cudaGetLastError());
+  return WOS_OK;
+}
+
+static int read_exterior(wos_context* c, cudaStream_t st, int64_t* out) {
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, c->d_exterior, sizeof(v), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, sizeof(v), st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *out = (v == ~0ull) ? -1 : (int64_t)v;
+  return WOS_OK;
+}
+
+extern "C" int wos_check_interior(wos_context* c, const wos_problem_set* s, int64_t n,
+                                  const double* points, const int32_t* inst_index,
+                                  int64_t* out_first, void* stream) {
+  if (!c || !s || !out_first) return fail(WOS_ERR_INVALID, "null argument");
+  if (n < 0) return fail(WOS_ERR_INVALID, "negative point count");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int r = launch_interior(c, s, n, points, inst_index, st);
+  if (r) return r;
+  return read_exterior(c, st, out_first);
+}
+
+extern "C" int wos_context_exterior(wos_context* c, void* stream, int64_t* out) {
+  if (!c || !out) return fail(WOS_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int64_t v;
+  int r = read_exterior(c, (cudaStream_t)stream, &v);
+  if (r) return r;
+  if (v < 0) v = c->host_exterior;
+  c->host_exterior = -1;
+  *out = v;
+  return WOS_OK;
+}
+
+// ------------------------------------------------------------------------
+// walk launches
+// ------------------------------------------------------------------------
+struct KernelInfo {
+  const void* fn;
+  size_t elem;  // sizeof(Real)
+};
+
+static KernelInfo pick_kernel(const wos_problem_set* s, int mode) {
+  KernelInfo k{nullptr, 8};
+  const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
+  if (mode == WOS_MODE_REPLAY_F64) {
+    k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0);
+    k.elem = 8;
+  } else if (mode == WOS_MODE_REPLAY_F32) {
+    k.fn = get_kernel_replay_f32(s->dim, dom, s->src_kind, 0);
+    k.elem = 4;
+  } else {
+    const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
+    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk);
+    k.elem = 4;
+  }
+  return k;
+}
+
+static size_t smem_bytes(size_t stage, size_t elem) {
+  return stage + (size_t)kWarps * (kRing * elem + kRingWords * 4 + kUQ * 4);
+}
+
+static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
+                       KArgs a, cudaStream_t st) {
+  const KernelInfo k = pick_kernel(s, cfg->mode);
+  if (!k.fn)
+    return fail(WOS_ERR_UNSUPPORTED, "no kernel for dim %d domain %d source %d mode %d", s->dim,
+                s->dom_kind, s->src_kind, cfg->mode);
+  if (cfg->mode == WOS_MODE_REPLAY_F64) {
+    a.table = s->d_table_d;
+    a.segs = s->d_segs_d;
+    a.stage_bytes = (int)s->bytes_d;
+    a.sine_K = s->sine_K;
+  } else if (cfg->mode == WOS_MODE_REPLAY_F32) {
+    a.table = s->d_table_f;
+    a.segs = s->d_segs_f;
+    a.stage_bytes = (int)s->bytes_f;
+    a.sine_K = s->sine_K;
+  } else {
+    a.table = s->d_table_n;
+    a.segs = s->d_segs_n;
+    a.stage_bytes = (int)s->bytes_f;
+    a.sine_K = s->sine_K_native;
+  }
+  a.hdr = s->d_hdr;
+  a.n_inst = s->n;
+  a.stride = s->stride;
+  a.bnd_off = s->bnd_off;
+  a.bnd_kind = s->bnd_kind;
+  a.bnd_M = s->bnd_M;
+  a.refill_min = c->refill_min;
+  a.eps = cfg->eps;
+  a.max_steps = (int32_t)std::min<int64_t>(cfg->max_steps, 0x7fffffff);
+  a.antithetic = cfg->antithetic ? 1 : 0;
+  a.seed = cfg->rng_seed;
+  a.nkey0 = (uint32_t)cfg->rng_seed;
+  a.nkey1_seed = (uint32_t)(cfg->rng_seed >> 32);
+  const size_t smem = smem_bytes((size_t)a.stage_bytes, k.elem);
+  if (smem > 220 * 1024)
+    return fail(WOS_ERR_UNSUPPORTED,
+                "problem table too large for shared memory (%zu bytes); split the batch",
+                (size_t)a.stage_bytes);
+  CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kBlock, smem));
+  if (per_sm < 1) return fail(WOS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  if (c->blocks_per_sm > 0) per_sm = std::min(per_sm, c->blocks_per_sm);
+  int64_t grid = (int64_t)c->num_sms * per_sm;
+  grid = std::min<int64_t>(grid, ((int64_t)a.n_units + kWarps - 1) / kWarps);
+  grid = std::max<int64_t>(grid, 1);
+  unsigned slot = c->next_counter.fetch_add(1) % kCounterRing;
+  a.work_counter = c->d_counters + slot;
+  CUDA_TRY(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned), st));
+  void* args[] = {&a};
+  CUDA_TRY(cudaLaunchKernel(k.fn, dim3((unsigned)grid), dim3(kBlock), args, smem, st));
+  return WOS_OK;
+}
+
+static const int64_t kMaxItemsPerLaunch = (1ll << 31) - 4 * kRing;
+
+extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
+                             int64_t n, const double* points, const uint64_t* pid,
+                             const uint64_t* tid, const double* signs, double* out_values,
+                             int64_t* out_steps, uint8_t* out_hits, void* stream) {
+  if (!c || !s || !cfg) return fail(WOS_ERR_INVALID, "null argument");
+  if (n < 0) return fail(WOS_ERR_INVALID, "negative row count");
+  if (!(cfg->eps > 0.0)) return fail(WOS_ERR_INVALID, "eps_shell must be positive");
+  if (cfg->max_steps < 1) return fail(WOS_ERR_INVALID, "max_steps must be at least 1");
+  if (n == 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t off = 0; off < n; off += kMaxItemsPerLaunch) {
+    const int64_t m = std::min<int64_t>(kMaxItemsPerLaunch, n - off);
+    KArgs a;
+    memset(&a, 0, sizeof(a));
+    a.sink = SINK_ROWS;
+    a.n_points = (uint32_t)m;
+    a.L = 1;
+    a.U = kUnitTarget;
+    a.IU = kUnitTarget;
+    a.n_units = (uint32_t)((m + kUnitTarget - 1) / kUnitTarget);
+    a.chunk = 1;
+    fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
+    fast_div_init(1, &a.l_mul, &a.l_shr);
+    a.points = points + off * s->dim;
+    a.row_pid = pid + off;
+    a.row_tid = tid + off;
+    a.row_sign = signs + off;
+    a.out_values = out_values + off;
+    a.out_steps = out_steps + off;
+    a.out_hits = out_hits + off;
+    int r = launch_walk(c, s, cfg, a, st);
+    if (r) return r;
+  }
+  return WOS_OK;
+}
+
+extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
+                            int64_t P, const double* points, const int64_t* point_ids,
+                            const int32_t* inst_index, int64_t L, uint64_t traj_start,
+                            double* out_mean, double* out_m2, uint64_t* out_total_steps,
+                            void* stream) {
+  if (!c || !s || !cfg) return fail(WOS_ERR_INVALID, "null argument");
+  if (P < 0) return fail(WOS_ERR_INVALID, "negative point count");
+  if (L < 1) return fail(WOS_ERR_INVALID, "trajectory count must be at least 1");
+  if (cfg->antithetic && (L % 2)) return fail(WOS_ERR_INVALID, "antithetic estimation needs an even trajectory count");
+  if (!(cfg->eps > 0.0)) return fail(WOS_ERR_INVALID, "eps_shell must be positive");
+  if (cfg->max_steps < 1) return fail(WOS_ERR_INVALID, "max_steps must be at least 1");
+  if (L > kMaxItemsPerLaunch) return fail(WOS_ERR_UNSUPPORTED, "L too large");
+  if (P == 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int r = launch_interior(c, s, P, points, inst_index, st);
+  if (r) return r;
+  const int64_t pts_per_launch = kMaxItemsPerLaunch / L;
+  for (int64_t off = 0; off < P; off += pts_per_launch) {
+    const int64_t m = std::min<int64_t>(pts_per_launch, P - off);
+    KArgs a;
+    memset(&a, 0, sizeof(a));
+    a.sink = SINK_ESTIMATE;
+    a.n_points = (uint32_t)m;
+    a.L = (uint32_t)L;
+    a.U = (uint32_t)std::max<int64_t>(1, (kUnitTarget + L - 1) / L);
+    a.IU = a.U * a.L;
+    a.n_units = (uint32_t)((m + a.U - 1) / a.U);
+    a.chunk = (uint32_t)std::min<int64_t>(L, kChunkMax);
+    fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
+    fast_div_init(a.L, &a.l_mul, &a.l_shr);
+    a.points = points + off * s->dim;
+    a.point_ids = point_ids + off;
+    a.inst_index = inst_index ? inst_index + off : nullptr;
+    a.traj_start = traj_start;
+    a.out_mean = out_mean + off;
+    a.out_m2 = out_m2 + off;
+    a.total_steps = reinterpret_cast<unsigned long long*>(out_total_steps);
+    r = launch_walk(c, s, cfg, a, st);
+    if (r) return r;
+  }
+  return WOS_OK;
+}
+
+// ---- host-buffer variants ------------------------------------------------
+static int scratch(wos_context* c, size_t bytes, char** out) {
+  if (bytes > c->scratch_bytes) {
+    cudaFree(c->d_scratch);
+    c->d_scratch = nullptr;
+    c->scratch_bytes = 0;
+    size_t want = std::max(bytes, (size_t)1 << 20);
+    CUDA_TRY(cudaMalloc(&c->d_scratch, want));
+    c->scratch_bytes = want;
+  }
+  *out = (char*)c->d_scratch;
+  return WOS_OK;
+}
+
+static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+extern "C" int wos_walk_rows_host(wos_context* c, const wos_problem_set* s,
+                                  const wos_walk_config* cfg, int64_t n, const double* points,
+                                  const uint64_t* pid, const uint64_t* tid, const double* signs,
+                                  double* out_values, int64_t* out_steps, uint8_t* out_hits) {
+  if (!c || !s || !cfg) return fail(WOS_ERR_INVALID, "null argument");
+  if (n <= 0) return n < 0 ? fail(WOS_ERR_INVALID, "negative row count") : WOS_OK;
+  std::lock_guard<std::mutex> g(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bp = al(n * s->dim * 8), b8 = al(n * 8), b1 = al(n);
+  char* base;
+  int r = scratch(c, bp + 5 * b8 + b1, &base);
+  if (r) return r;
+  double* d_pts = (double*)base;
+  uint64_t* d_pid = (uint64_t*)(base + bp);
+  uint64_t* d_tid = (uint64_t*)(base + bp + b8);
+  double* d_sgn = (double*)(base + bp + 2 * b8);
+  double* d_val = (double*)(base + bp + 3 * b8);
+  int64_t* d_stp = (int64_t*)(base + bp + 4 * b8);
+  uint8_t* d_hit = (uint8_t*)(base + bp + 5 * b8);
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(d_pts, points, n * s->dim * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_pid, pid, n * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_tid, tid, n * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_sgn, signs, n * 8, cudaMemcpyHostToDevice, st));
+  r = wos_walk_rows(c, s, cfg, n, d_pts, d_pid, d_tid, d_sgn, d_val, d_stp, d_hit, st);
+  if (r) return r;
+  CUDA_TRY(cudaMemcpyAsync(out_values, d_val, n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(out_steps, d_stp, n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(out_hits, d_hit, n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return WOS_OK;
+}
+
+extern "C" int wos_check_interior_host(wos_context* c, const wos_problem_set* s, int64_t n,
+                                       const double* points, const int32_t* inst_index,
+                                       int64_t* out_first) {
+  if (!c || !s || !out_first) return fail(WOS_ERR_INVALID, "null argument");
+  if (n <= 0) {
+    *out_first = -1;
+    return n < 0 ? fail(WOS_ERR_INVALID, "negative point count") : WOS_OK;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bp = al(n * s->dim * 8);
+  char* base;
+  int r = scratch(c, bp + al(n * 4), &base);
+  if (r) return r;
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(base, points, n * s->dim * 8, cudaMemcpyHostToDevice, st));
+  int32_t* d_inst = nullptr;
+  if (inst_index) {
+    d_inst = (int32_t*)(base + bp);
+    CUDA_TRY(cudaMemcpyAsync(d_inst, inst_index, n * 4, cudaMemcpyHostToDevice, st));
+  }
+  r = launch_interior(c, s, n, (const double*)base, d_inst, st);
+  if (r) return r;
+  return read_exterior(c, st, out_first);
+}
+
+extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
+                                 const wos_walk_config* cfg, int64_t P, const double* points,
+                                 const int64_t* point_ids, const int32_t* inst_index, int64_t L,
+                                 uint64_t traj_start, double* out_mean, double* out_m2,
+                                 uint64_t* out_total_steps) {
+  if (!c || !s || !cfg) return fail(WOS_ERR_INVALID, "null argument");
+  if (P <= 0) {
+    if (out_total_steps) *out_total_steps = 0;
+    return P < 0 ? fail(WOS_ERR_INVALID, "negative point count") : WOS_OK;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bp = al(P * s->dim * 8), b8 = al(P * 8), b4 = al(P * 4);
+  char* base;
+  int r = scratch(c, bp + 3 * b8 + b4, &base);
+  if (r) return r;
+  double* d_pts = (double*)base;
+  int64_t* d_ids = (int64_t*)(base + bp);
+  double* d_mean = (double*)(base + bp + b8);
+  double* d_m2 = (double*)(base + bp + 2 * b8);
+  int32_t* d_inst = inst_index ? (int32_t*)(base + bp + 3 * b8) : nullptr;
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(d_pts, points, P * s->dim * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_ids, point_ids, P * 8, cudaMemcpyHostToDevice, st));
+  if (d_inst) CUDA_TRY(cudaMemcpyAsync(d_inst, inst_index, P * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(unsigned long long), st));
+  r = wos_estimate(c, s, cfg, P, d_pts, d_ids, d_inst, L, traj_start, d_mean, d_m2,
+                   reinterpret_cast<uint64_t*>(c->d_steps), st);
+  if (r) return r;
+  unsigned long long steps = 0, ext = 0;
+  CUDA_TRY(cudaMemcpyAsync(out_mean, d_mean, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(out_m2, d_m2, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&steps, c->d_steps, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&ext, c->d_exterior, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, 8, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (out_total_steps) *out_total_steps = steps;
+  if (ext != ~0ull) {
+    c->host_exterior = (int64_t)ext;
+    return fail(WOS_ERR_EXTERIOR, "exterior query: start point %lld", (long long)ext);
+  }
+  return WOS_OK;
+}
+
+// ------------------------------------------------------------------------
+// RNG known-answer kernels
+// ------------------------------------------------------------------------
+__global__ void philox64_kernel(int64_t n, const uint64_t* ctr, uint64_t k0, uint64_t k1, uint64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    philox4x64(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], k0, k1, w);
+    for (int j = 0; j < 4; ++j) out[4 * i + j] = w[j];
+  }
+}
+__global__ void philox32_kernel(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox4x32(make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]), k0, k1);
+    out[4 * i] = w.x;
+    out[4 * i + 1] = w.y;
+    out[4 * i + 2] = w.z;
+    out[4 * i + 3] = w.w;
+  }
+}
+
+extern "C" int wos_philox4x64(wos_context* c, int64_t n, const uint64_t* ctr, uint64_t k0, uint64_t k1,
+                              uint64_t* out, void* stream) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (n <= 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  philox64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ctr, k0, k1, out);
+  CUDA_TRY(cudaGetLastError());
+  return WOS_OK;
+}
+
+extern "C" int wos_philox4x32(wos_context* c, int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1,
+                              uint32_t* out, void* stream) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (n <= 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  philox32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ctr, k0, k1, out);
+  CUDA_TRY(cudaGetLastError());
+  return WOS_OK;
+}
+
+// ------------------------------------------------------------------------
+// roofline probes: MUFU and FFMA throughput
+// ------------------------------------------------------------------------
+constexpr int kProbeChains = 8;
+
+__global__ void __launch_bounds__(256) probe_mufu_kernel(int iters, float seed, float* sink) {
+  float v[kProbeChains];
+#pragma unroll
+  for (int j = 0; j < kProbeChains; ++j) v[j] = seed + 0.01f * (threadIdx.x + j);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < kProbeChains; ++j) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(v[j]));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kProbeChains; ++j) s += v[j];
+  if (s == 1234.5f) sink[0] = s;
+}
+
+__global__ void __launch_bounds__(256) probe_ffma_kernel(int iters, float seed, float* sink) {
+  float v[kProbeChains];
+#pragma unroll
+  for (int j = 0; j < kProbeChains; ++j) v[j] = seed + 0.01f * (threadIdx.x + j);
+  const float a = 0.999f, b = 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < kProbeChains; ++j) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(v[j]) : "f"(a), "f"(b));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kProbeChains; ++j) s += v[j];
+  if (s == 1234.5f) sink[0] = s;
+}
+
+extern "C" int wos_probe_peaks(wos_context* c, double* sfu, double* fp32, double* clk, int32_t* nsm) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  float* d_sink;
+  CUDA_TRY(cudaMalloc(&d_sink, 16));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  cudaStream_t st = c->stream;
+  const int blocks = c->num_sms * 8, threads = 256;
+  double best_sfu = 0, best_fma = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    const int it_mufu = 4096, it_fma = 16384;
+    CUDA_TRY(cudaEventRecord(e0, st));
+    probe_mufu_kernel<<<blocks, threads, 0, st>>>(it_mufu, 1.5f, d_sink);
+    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0) best_sfu = std::max(best_sfu, (double)blocks * threads * it_mufu * kProbeChains / (ms * 1e-3));
+    CUDA_TRY(cudaEventRecord(e0, st));
+    probe_ffma_kernel<<<blocks, threads, 0, st>>>(it_fma, 1.5f, d_sink);
+    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0) best_fma = std::max(best_fma, 2.0 * blocks * threads * (double)it_fma * kProbeChains / (ms * 1e-3));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_sink);
+  if (sfu) *sfu = best_sfu;
+  if (fp32) *fp32 = best_fma;
+  if (clk) *clk = best_fma / ((double)c->num_sms * 256.0);
+  if (nsm) *nsm = c->num_sms;
+  return WOS_OK;
+}

@@ -1,0 +1,39 @@
+// Kernel instantiations for MODE_REPLAY_F32 (see wos_walk.cuh).
+#include "wos_kernels.h"
+#include "wos_walk.cuh"
+
+namespace wos {
+
+#define WOS_K(DIM, DOM, SRC, SK)                                             \
+  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                    \
+    return reinterpret_cast<const void*>(                                    \
+        &wos_walk_kernel<Spec<MODE_REPLAY_F32, DIM, DOM, SRC, SK>, 2>);
+
+const void* get_kernel_replay_f32(int dim, int dom, int src, int sk) {
+  // 2D
+  WOS_K(2, DOM_BALL, SRC_NONE, 0)
+  WOS_K(2, DOM_BALL, SRC_CONST, 0)
+  WOS_K(2, DOM_BALL, SRC_RBF2, 0)
+  WOS_K(2, DOM_BALL, SRC_SINE, 0)
+  WOS_K(2, DOM_BALL, SRC_GAUSS, 0)
+  WOS_K(2, DOM_BOX, SRC_NONE, 0)
+  WOS_K(2, DOM_BOX, SRC_CONST, 0)
+  WOS_K(2, DOM_BOX, SRC_SINE, 0)
+  WOS_K(2, DOM_BOX, SRC_GAUSS, 0)
+  WOS_K(2, DOM_POLY, SRC_NONE, 0)
+  WOS_K(2, DOM_POLY, SRC_CONST, 0)
+  WOS_K(2, DOM_POLY, SRC_SINE, 0)
+  WOS_K(2, DOM_POLY, SRC_GAUSS, 0)
+  // 3D
+  WOS_K(3, DOM_BALL, SRC_NONE, 0)
+  WOS_K(3, DOM_BALL, SRC_CONST, 0)
+  WOS_K(3, DOM_BALL, SRC_SINE, 0)
+  WOS_K(3, DOM_BALL, SRC_GAUSS, 0)
+  WOS_K(3, DOM_BOX, SRC_NONE, 0)
+  WOS_K(3, DOM_BOX, SRC_CONST, 0)
+  WOS_K(3, DOM_BOX, SRC_SINE, 0)
+  WOS_K(3, DOM_BOX, SRC_GAUSS, 0)
+  return nullptr;
+}
+
+}  // namespace wos

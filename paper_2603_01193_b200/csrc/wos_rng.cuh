@@ -1,0 +1,61 @@
+// Counter-based generators for the WoS walker.
+//
+// Philox4x64-10 reproduces the reference's rng.philox4x64 (rng.py:57-82) and
+// _kernels.philox_block (_kernels.py:60-82) bit for bit: same multipliers, same
+// round (x0,x1,x2,x3) <- (hi(M1 x2)^x1^k0, lo(M1 x2), hi(M0 x0)^x3^k1, lo(M0 x0)),
+// key bumped after each round. Used by the REPLAY modes.
+//
+// Philox4x32-10 (Random123 constants) drives the NATIVE_F32 mode: 32-bit
+// multiplies map to one IMAD.WIDE.U32 each, a 3-input XOR to one LOP3.
+#pragma once
+#include <stdint.h>
+
+namespace wos {
+
+__device__ __forceinline__ void philox4x64(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                                           uint64_t k0, uint64_t k1, uint64_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    uint64_t hi0 = __umul64hi(M0, c0), lo0 = M0 * c0;
+    uint64_t hi1 = __umul64hi(M1, c2), lo1 = M1 * c2;
+    uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// rng.to_uniform (rng.py:100-102): top 53 bits -> [0, 1)
+__device__ __forceinline__ double u01_53(uint64_t w) {
+  return (double)(w >> 11) * 1.1102230246251565e-16;
+}
+
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint64_t p0 = (uint64_t)M0 * c.x;  // IMAD.WIDE.U32
+    uint64_t p1 = (uint64_t)M1 * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// NATIVE uniform: (w >> 9) * 2^-23 in [0, 1), exact in fp32 (one LOP3 + one FADD).
+__device__ __forceinline__ float u01_23(uint32_t w) {
+  return __uint_as_float(0x3f800000u | (w >> 9)) - 1.0f;
+}
+
+}  // namespace wos

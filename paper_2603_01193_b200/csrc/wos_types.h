@@ -1,0 +1,101 @@
+// Shared host/device types of the WoS walker (launch arguments, instance headers).
+#pragma once
+#include <stdint.h>
+
+namespace wos {
+
+enum : int { DOM_BALL = 0, DOM_POLAR = 1, DOM_BOX = 2, DOM_POLY = 3 };
+enum : int { SRC_NONE = 0, SRC_CONST = 1, SRC_RBF2 = 2, SRC_SINE = 3, SRC_GAUSS = 4 };
+enum : int {
+  BND_CONST = 0,
+  BND_FOURIER5 = 1,
+  BND_LINEAR = 2,
+  BND_FOURIER = 3,
+  BND_SQUARE_ARCSINE = 4,
+  BND_QUADRATIC = 5
+};
+enum : int { MODE_REPLAY_F64 = 0, MODE_REPLAY_F32 = 1, MODE_NATIVE_F32 = 2 };
+enum : int { SINK_ROWS = 0, SINK_ESTIMATE = 1 };
+
+constexpr int kBlock = 256;       // threads per CTA (8 warps)
+constexpr int kWarps = kBlock / 32;
+constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
+constexpr int kRingWords = kRing / 32;
+constexpr int kUQ = 16;           // per-warp queue of grabbed work units
+constexpr int kChunkMax = kRing / 2;  // longest run of one point's walks reduced at once
+constexpr int kUnitTarget = 128;  // minimum walks per grabbed work unit
+constexpr int kDomOff = 0;        // table row: [0, 8) domain params
+constexpr int kSrcOff = 8;        //            [8, 8 + ns) source params, then boundary params
+
+// Per-instance header (32 bytes), one per problem of a set.
+struct InstHdr {
+  uint64_t ikey;    // Problem.instance_key (REPLAY Philox4x64 key word 1)
+  uint32_t nkey1;   // NATIVE key word 1 = (seed >> 32) ^ this (lo32(ikey) ^ hi32(ikey) * 0x9E3779B9)
+  int32_t seg_off;  // polygon: first segment
+  int32_t n_seg;    // polygon: segment count
+  int32_t pad[3];
+};
+
+// n / d for n < 2^31 with host-precomputed (mul, shr) (Granlund-Montgomery round-up)
+__host__ __device__ inline uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t shr) {
+#ifdef __CUDA_ARCH__
+  return (__umulhi(n, mul) + n) >> shr;
+#else
+  return (uint32_t)((((uint64_t)n * mul) >> 32) + n) >> shr;
+#endif
+}
+inline void fast_div_init(uint32_t d, uint32_t* mul, uint32_t* shr) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  *shr = l;
+  *mul = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+}
+
+struct KArgs {
+  // ---- problem set (device) ----
+  const void* table;    // Real rows [n_inst][stride]
+  const InstHdr* hdr;   // [n_inst]
+  const void* segs;     // polygon segments (mode-specific layout)
+  int32_t n_inst;
+  int32_t stride;       // Real elements per table row
+  int32_t bnd_off;      // boundary params offset in a row
+  int32_t stage_bytes;  // bytes of the table staged into shared memory (0 = read global)
+  int32_t sine_K;       // sine order (uniform over the set; padded)
+  int32_t bnd_kind;
+  int32_t bnd_M;        // Fourier / arc-length order (uniform over the set; padded)
+  int32_t refill_min;   // refill idle lanes once this many are idle
+  // ---- walk config ----
+  double eps;
+  int32_t max_steps;
+  int32_t antithetic;
+  uint64_t seed;        // REPLAY Philox4x64 key word 0
+  uint32_t nkey0;       // NATIVE Philox4x32 key word 0 = lo32(seed)
+  uint32_t nkey1_seed;  // hi32(seed), xored with InstHdr::nkey1
+  int32_t sink;         // SINK_ROWS or SINK_ESTIMATE
+  // ---- work decomposition ----
+  uint32_t n_points;    // estimate: P; rows: n
+  uint32_t L;           // estimate: walks per point; rows: 1
+  uint32_t U;           // points per work unit
+  uint32_t IU;          // items (walks) per work unit = U * L
+  uint32_t n_units;
+  uint32_t chunk;       // reduction chunk = min(L, kChunkMax)
+  uint32_t iu_mul, iu_shr;  // magic numbers: n / IU = (umulhi(n, mul) + n) >> shr, n < 2^31
+  uint32_t l_mul, l_shr;    // same for n / L
+  const double* points;        // [n, dim]
+  const int64_t* point_ids;    // estimate
+  const int32_t* inst_index;   // estimate, may be null
+  uint64_t traj_start;
+  const uint64_t* row_pid;     // rows
+  const uint64_t* row_tid;
+  const double* row_sign;
+  // ---- outputs ----
+  double* out_values;
+  int64_t* out_steps;
+  uint8_t* out_hits;
+  double* out_mean;
+  double* out_m2;
+  unsigned long long* total_steps;
+  unsigned int* work_counter;
+};
+
+}  // namespace wos

@@ -1,0 +1,803 @@
+// Persistent Walk-on-Spheres kernel for sm_100a.
+//
+// One template covers every (mode, dimension, domain, source) combination; the
+// boundary term is a runtime switch because it runs once per walk.
+//
+// Execution model:
+//   * persistent grid (SMs x resident CTAs), 8 warps per CTA;
+//   * every warp owns a stream of walks ("items", point-major) that it pulls
+//     from a global work counter in units of >= 128 walks;
+//   * each lane carries one walk in registers (position, Green accumulator,
+//     step, RNG counter words); when lanes finish (eps-shell hit or max_steps)
+//     they are refilled with the next items of the warp's stream (lane refill),
+//     so no lane idles while work remains;
+//   * ESTIMATE sink: walk values go to a per-warp shared-memory ring indexed by
+//     the item's stream position; a chunk of one point's walks (<= 512) is
+//     reduced as soon as all of them are done, in fixed index order with fp64
+//     warp-shuffle trees (two-pass mean / m2, PointEstimate.from_values,
+//     estimator.py:106-110). The result therefore does not depend on which lane
+//     ran which walk, on the launch shape, or on the number of GPUs;
+//   * ROWS sink: per-walk (value, steps, hit) written straight to global memory
+//     (walker.walk_poisson_values, walker.py:181-229).
+//
+// Numerics per mode:
+//   REPLAY_F64 / REPLAY_F32 follow walker._poisson_generic (walker.py:257-314)
+//   operation by operation, on Philox4x64 draws identical to the reference's.
+//   NATIVE_F32 samples the source term from the ball Green's function
+//   (radius d*sqrt(U1 U2) in 2D, d*Beta(2,2) as the median of three uniforms in
+//   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
+//   and Philox4x32-10 with counter (2*step [+1], pid, tid, hi-words).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "wos_rng.cuh"
+#include "wos_types.h"
+
+namespace wos {
+
+#define WOS_FULL 0xffffffffu
+
+// ------------------------------------------------------------------------
+// math helpers
+// ------------------------------------------------------------------------
+__device__ __forceinline__ float fast_sqrt(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float fast_ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// (w >> 9) | 1.0f  ->  [1, 2); u = f - 1 exactly
+__device__ __forceinline__ float f12(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)); }
+
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 6.283185307179586;
+constexpr double kInvTwoPi = 1.0 / 6.283185307179586;
+constexpr double kInvFourPi = 1.0 / (4.0 * 3.141592653589793);
+constexpr float kTwoPiF = 6.283185307179586f;
+constexpr float kPiF = 3.141592653589793f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void psincos(double a, double* s, double* c) { sincos(a, s, c); }
+__device__ __forceinline__ void psincos(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ double psqrt(double a) { return sqrt(a); }
+__device__ __forceinline__ float psqrt(float a) { return sqrtf(a); }
+__device__ __forceinline__ double plog(double a) { return log(a); }
+__device__ __forceinline__ float plog(float a) { return logf(a); }
+__device__ __forceinline__ double pcbrt(double a) { return cbrt(a); }
+__device__ __forceinline__ float pcbrt(float a) { return cbrtf(a); }
+__device__ __forceinline__ double pexp(double a) { return exp(a); }
+__device__ __forceinline__ float pexp(float a) { return expf(a); }
+__device__ __forceinline__ double pmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float pmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double pmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float pmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double pabs(double a) { return fabs(a); }
+__device__ __forceinline__ float pabs(float a) { return fabsf(a); }
+
+template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_>
+struct Spec {
+  static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_;
+  static constexpr bool NATIVE = (MODE_ == MODE_NATIVE_F32);
+  using Real = typename std::conditional<MODE_ == MODE_REPLAY_F64, double, float>::type;
+};
+
+// ------------------------------------------------------------------------
+// the walker
+// ------------------------------------------------------------------------
+template <class S>
+struct Walker {
+  using Real = typename S::Real;
+  static constexpr int DIM = S::DIM;
+  static constexpr int ND = (S::DOM == DOM_BALL) ? 4 : ((S::DOM == DOM_BOX) ? 8 : 1);
+
+  struct Lane {
+    Real x[DIM];
+    Real acc;
+    Real sgn;
+    Real dom[ND];
+    const Real* row;  // this walk's instance row in the staged table (shared memory)
+    int step;
+    uint32_t seq;
+    uint64_t pid, tid, ikey;   // REPLAY counters / key
+    uint32_t c1, c2, c3, k1;   // NATIVE counters / key
+    int32_t seg_off, n_seg;
+  };
+
+  // ---------------- domains ----------------
+  // distance to the boundary (positive inside)
+  __device__ static __forceinline__ Real dist(const Lane& l, const KArgs& a) {
+    if constexpr (S::DOM == DOM_BALL) {
+      // geometry.py:196-206 / _kernels.py:329-339
+      Real s = Real(0);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        Real u = l.x[i] - l.dom[i];
+        if constexpr (S::NATIVE) s = fmaf(u, u, s);
+        else s = s + u * u;
+      }
+      if constexpr (S::NATIVE) return l.dom[3] - fast_sqrt(s);
+      else return pabs(l.dom[3] - psqrt(s));
+    } else if constexpr (S::DOM == DOM_BOX) {
+      Real d = l.x[0] - l.dom[0];
+      d = pmin(d, l.dom[4] - l.x[0]);
+#pragma unroll
+      for (int i = 1; i < DIM; ++i) {
+        d = pmin(d, l.x[i] - l.dom[i]);
+        d = pmin(d, l.dom[4 + i] - l.x[i]);
+      }
+      return d;
+    } else {
+      return poly_dist(l, a, nullptr);
+    }
+  }
+
+  // polygon: min distance over segments; optionally the closest point (first nearest segment)
+  __device__ static __forceinline__ Real poly_dist(const Lane& l, const KArgs& a, Real* q) {
+    if constexpr (S::NATIVE) {
+      const float4* seg = reinterpret_cast<const float4*>(a.segs) + 2 * (size_t)l.seg_off;
+      const float px = l.x[0], py = l.x[1];
+      float best = 3.0e38f, bqx = 0.f, bqy = 0.f;
+      const int n = l.n_seg;
+#pragma unroll 4
+      for (int i = 0; i < n; ++i) {
+        const float4 A = __ldg(seg + 2 * i);      // ax, ay, ex, ey
+        const float4 B = __ldg(seg + 2 * i + 1);  // ex/|e|^2, ey/|e|^2
+        const float wx = px - A.x, wy = py - A.y;
+        const float t = __saturatef(fmaf(wx, B.x, wy * B.y));
+        const float dx = fmaf(-t, A.z, wx), dy = fmaf(-t, A.w, wy);
+        const float d2 = fmaf(dx, dx, dy * dy);
+        if (q != nullptr) {
+          if (d2 < best) {
+            best = d2;
+            bqx = fmaf(t, A.z, A.x);
+            bqy = fmaf(t, A.w, A.y);
+          }
+        } else {
+          best = fminf(best, d2);
+        }
+      }
+      if (q != nullptr) {
+        q[0] = bqx;
+        q[1] = bqy;
+      }
+      return fast_sqrt(best);
+    } else {
+      // oracle/wos_oracle.c query(): t = clamp(w.e / e.e, 0, 1), c = a + t e
+      const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
+      const Real px = l.x[0], py = l.x[1];
+      Real best = Real(1e300 > 3e38 && sizeof(Real) == 8 ? 1e300 : 3e38), bqx = 0, bqy = 0;
+      const int n = l.n_seg;
+      for (int i = 0; i < n; ++i) {
+        const Real ax = seg[4 * i], ay = seg[4 * i + 1], ex = seg[4 * i + 2], ey = seg[4 * i + 3];
+        const Real wx = px - ax, wy = py - ay;
+        Real t = (wx * ex + wy * ey) / (ex * ex + ey * ey);
+        t = t < Real(0) ? Real(0) : (t > Real(1) ? Real(1) : t);
+        const Real cx = ax + t * ex, cy = ay + t * ey;
+        const Real dx = px - cx, dy = py - cy;
+        const Real d2 = dx * dx + dy * dy;
+        if (d2 < best) {
+          best = d2;
+          bqx = cx;
+          bqy = cy;
+        }
+      }
+      if (q != nullptr) {
+        q[0] = bqx;
+        q[1] = bqy;
+      }
+      return psqrt(best);
+    }
+  }
+
+  // closest boundary point at termination
+  __device__ static __forceinline__ void project(const Lane& l, const KArgs& a, Real* q) {
+    if constexpr (S::DOM == DOM_BALL) {
+      Real s = Real(0), u[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        u[i] = l.x[i] - l.dom[i];
+        s = s + u[i] * u[i];
+      }
+      const Real rho = psqrt(s), R = l.dom[3];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        const Real dir = (rho == Real(0)) ? (i == 0 ? Real(1) : Real(0)) : u[i] / rho;
+        q[i] = l.dom[i] + R * dir;
+      }
+    } else if constexpr (S::DOM == DOM_BOX) {
+      // first nearest face (axis order, lower before upper) — strict <
+      Real best = l.x[0] - l.dom[0], face = l.dom[0];
+      int axis = 0;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        const Real dl = l.x[i] - l.dom[i], du = l.dom[4 + i] - l.x[i];
+        if (i > 0 && dl < best) {
+          best = dl;
+          axis = i;
+          face = l.dom[i];
+        }
+        if (du < best) {
+          best = du;
+          axis = i;
+          face = l.dom[4 + i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) q[i] = (i == axis) ? face : l.x[i];
+    } else {
+      poly_dist(l, a, q);
+    }
+  }
+
+  // ---------------- problem terms ----------------
+  template <int K>
+  __device__ static __forceinline__ void sine_row(Real y, Real* s) {
+    // s[k] = sin((k+1) pi y)
+    if constexpr (S::NATIVE) {
+      float s1, c1;
+      __sincosf(kPiF * y, &s1, &c1);
+      const float tc = c1 + c1;
+      s[0] = s1;
+      if constexpr (K > 1) s[1] = tc * s1;
+#pragma unroll
+      for (int k = 2; k < K; ++k) s[k] = fmaf(tc, s[k - 1], -s[k - 2]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) s[k] = sin((Real)(k + 1) * (Real)kPi * y);
+    }
+  }
+
+  template <int K>
+  __device__ static __forceinline__ Real sine_eval(const Real* __restrict__ a, const Real* y) {
+    Real sx[K], sy[K];
+    sine_row<K>(y[0], sx);
+    sine_row<K>(y[1], sy);
+    if constexpr (DIM == 2) {
+      Real f = Real(0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        Real t = Real(0);
+#pragma unroll
+        for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sy[l];
+        f = f + sx[k] * t;
+      }
+      return f;
+    } else {
+      Real sz[K];
+      sine_row<K>(y[2], sz);
+      Real f = Real(0);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        Real u = Real(0);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          Real t = Real(0);
+#pragma unroll
+          for (int k = 0; k < K; ++k) t = t + a[(i * K + j) * K + k] * sz[k];
+          u = u + sy[j] * t;
+        }
+        f = f + sx[i] * u;
+      }
+      return f;
+    }
+  }
+
+  // runtime-K sine series (K <= 16), used when no specialisation matches
+  __device__ static Real sine_eval_rt(const Real* __restrict__ a, const Real* y, int K) {
+    Real f = Real(0);
+    if constexpr (DIM == 2) {
+      for (int k = 0; k < K; ++k) {
+        const Real sk = sin((Real)(k + 1) * (Real)kPi * y[0]);
+        Real t = Real(0);
+        for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sin((Real)(l + 1) * (Real)kPi * y[1]);
+        f = f + sk * t;
+      }
+    } else {
+      for (int i = 0; i < K; ++i) {
+        const Real si = sin((Real)(i + 1) * (Real)kPi * y[0]);
+        for (int j = 0; j < K; ++j) {
+          const Real sj = sin((Real)(j + 1) * (Real)kPi * y[1]);
+          Real t = Real(0);
+          for (int k = 0; k < K; ++k)
+            t = t + a[(i * K + j) * K + k] * sin((Real)(k + 1) * (Real)kPi * y[2]);
+          f = f + si * sj * t;
+        }
+      }
+    }
+    return f;
+  }
+
+  __device__ static __forceinline__ Real source(const Lane& l, const KArgs& a, const Real* y) {
+    const Real* P = l.row + kSrcOff;
+    if constexpr (S::SRC == SRC_CONST) {
+      return P[0];
+    } else if constexpr (S::SRC == SRC_RBF2) {
+      // _kernels.py:248-259
+      const Real d1x = y[0] - P[2], d1y = y[1] - P[3], d2x = y[0] - P[4], d2y = y[1] - P[5];
+      if constexpr (S::NATIVE)
+        return P[0] * fast_ex2(-(d1x * d1x + d1y * d1y) * kLog2e) +
+               P[1] * fast_ex2(-(d2x * d2x + d2y * d2y) * kLog2e);
+      else
+        return P[0] * pexp(-(d1x * d1x + d1y * d1y)) + P[1] * pexp(-(d2x * d2x + d2y * d2y));
+    } else if constexpr (S::SRC == SRC_SINE) {
+      if constexpr (S::SK > 0) return sine_eval<S::SK>(P, y);
+      else return sine_eval_rt(P, y, a.sine_K);
+    } else if constexpr (S::SRC == SRC_GAUSS) {
+      Real r2 = Real(0);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        const Real u = y[i] - P[2 + i];
+        r2 = r2 + u * u;
+      }
+      // NATIVE table holds log2(e) / (2 sigma^2) at P[1]; REPLAY holds sigma
+      if constexpr (S::NATIVE) return P[0] * fast_ex2(-r2 * P[1]);
+      else return P[0] * pexp(-r2 / (Real(2) * P[1] * P[1]));
+    } else {
+      return Real(0);
+    }
+  }
+
+  __device__ static Real boundary(const Lane& l, const KArgs& a, const Real* q) {
+    const Real* B = l.row + a.bnd_off;
+    switch (a.bnd_kind) {
+      case BND_CONST:
+        return B[0];
+      case BND_LINEAR:
+        if constexpr (DIM == 2) return B[0] * q[0] + B[1] * q[1] + B[2];
+        else return B[0] * q[0] + B[1] * q[1] + B[2] * q[2] + B[3];
+      case BND_FOURIER5: {
+        if constexpr (DIM == 2) {
+          const Real r = psqrt(q[0] * q[0] + q[1] * q[1]);
+          const Real c = (r == Real(0)) ? Real(1) : q[0] / r;
+          const Real s = (r == Real(0)) ? Real(0) : q[1] / r;
+          return B[0] + B[1] * c + B[2] * s + B[3] * (c * c - s * s) + B[4] * (Real(2) * c * s);
+        }
+        return Real(0);
+      }
+      case BND_FOURIER: {
+        if constexpr (DIM == 2) {
+          const int M = a.bnd_M;
+          const Real t = (Real)atan2((double)q[1], (double)q[0]);
+          Real g = B[1];
+          if constexpr (S::NATIVE) {
+            // Chebyshev-style rotation recurrence from (cos t, sin t)
+            float c1, s1;
+            sincosf(t, &s1, &c1);
+            float cm = c1, sm = s1;
+            for (int m = 1; m <= M; ++m) {
+              g = fmaf(B[1 + m], cm, fmaf(B[1 + M + m], sm, g));
+              const float cn = cm * c1 - sm * s1;
+              sm = sm * c1 + cm * s1;
+              cm = cn;
+            }
+          } else {
+            for (int m = 1; m <= M; ++m) {
+              Real sm, cm;
+              psincos((Real)m * t, &sm, &cm);
+              g = g + B[1 + m] * cm + B[1 + M + m] * sm;
+            }
+          }
+          return g;
+        }
+        return Real(0);
+      }
+      case BND_SQUARE_ARCSINE: {
+        if constexpr (DIM == 2) {
+          const Real x0 = B[0], y0 = B[1], side = B[2];
+          const int M = a.bnd_M;
+          const Real u = (q[0] - x0) / side, v = (q[1] - y0) / side;
+          const Real db = pabs(v), dr = pabs(Real(1) - u), dt = pabs(Real(1) - v), dl = pabs(u);
+          Real s;
+          if (db <= dr && db <= dt && db <= dl) s = u;
+          else if (dr <= dt && dr <= dl) s = Real(1) + v;
+          else if (dt <= dl) s = Real(2) + (Real(1) - u);
+          else s = Real(3) + (Real(1) - v);
+          Real g = Real(0);
+          for (int m = 1; m <= M; ++m) g = g + B[3 + m] * sin((Real)kTwoPi * (Real)m * s / Real(4));
+          return g;
+        }
+        return Real(0);
+      }
+      case BND_QUADRATIC:
+        if constexpr (DIM == 2)
+          return B[0] * q[0] * q[0] + B[1] * q[1] * q[1] + B[2] * q[0] * q[1] + B[3] * q[0] +
+                 B[4] * q[1] + B[5];
+        return Real(0);
+      default:
+        return Real(0);
+    }
+  }
+
+  // ---------------- one jump ----------------
+  // REPLAY: walker.py:284-313 operation by operation
+  __device__ static __forceinline__ double nonzero_u(double u, uint64_t draw, const Lane& l,
+                                                     const KArgs& a) {
+    uint64_t tag = 1;
+    while (u == 0.0) {  // walker.py:232-242, probability 2^-53 per draw
+      uint64_t w[4];
+      philox4x64(draw, l.pid, l.tid, tag, a.seed, l.ikey, w);
+      u = u01_53(w[0]);
+      tag += 1;
+    }
+    return u;
+  }
+
+  __device__ static __forceinline__ void advance_replay(Lane& l, Real d, const KArgs& a) {
+    const uint64_t draw = 2ull * (uint64_t)l.step;
+    uint64_t w[4];
+    philox4x64(draw, l.pid, l.tid, 0ull, a.seed, l.ikey, w);
+    Real dir[DIM];
+    const Real sg = l.sgn;
+    if constexpr (DIM == 2) {
+      const Real theta = (Real)kTwoPi * (Real)u01_53(w[0]);
+      psincos(theta, &dir[1], &dir[0]);
+      if constexpr (S::SRC != SRC_NONE) {
+        const Real u_rad = (Real)nonzero_u(u01_53(w[2]), draw, l, a);
+        const Real rad = d * psqrt(u_rad);
+        const Real phi = (Real)kTwoPi * (Real)u01_53(w[1]);
+        Real sp, cp;
+        psincos(phi, &sp, &cp);
+        const Real g[2] = {l.x[0] + sg * rad * cp, l.x[1] + sg * rad * sp};
+        const Real green = (Real)kInvTwoPi * plog(d / rad);
+        l.acc -= (Real)kPi * d * d * source(l, a, g) * green;
+      }
+    } else {
+      const Real z = Real(2) * (Real)u01_53(w[0]) - Real(1);
+      const Real s = psqrt(pmax(Real(0), Real(1) - z * z));
+      const Real phi = (Real)kTwoPi * (Real)u01_53(w[1]);
+      Real sp, cp;
+      psincos(phi, &sp, &cp);
+      dir[0] = s * cp;
+      dir[1] = s * sp;
+      dir[2] = z;
+      if constexpr (S::SRC != SRC_NONE) {
+        uint64_t wb[4];
+        philox4x64(draw + 1, l.pid, l.tid, 0ull, a.seed, l.ikey, wb);
+        const Real u_rad = (Real)nonzero_u(u01_53(wb[0]), draw + 1, l, a);
+        const Real rad = d * pcbrt(u_rad);
+        const Real vz = Real(2) * (Real)u01_53(w[2]) - Real(1);
+        const Real vs = psqrt(pmax(Real(0), Real(1) - vz * vz));
+        const Real vphi = (Real)kTwoPi * (Real)u01_53(w[3]);
+        Real vsp, vcp;
+        psincos(vphi, &vsp, &vcp);
+        const Real g[3] = {l.x[0] + sg * rad * (vs * vcp), l.x[1] + sg * rad * (vs * vsp),
+                           l.x[2] + sg * rad * vz};
+        const Real green = (Real)kInvFourPi * (Real(1) / rad - Real(1) / d);
+        const Real vol = (Real)(4.0 / 3.0) * (Real)kPi * (d * d * d);
+        l.acc -= vol * source(l, a, g) * green;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) l.x[i] += sg * d * dir[i];
+  }
+
+  // NATIVE: Green's-function importance sampling, fp32 fast math
+  __device__ static __forceinline__ void advance_native(Lane& l, float d, const KArgs& a) {
+    const uint4 A = philox4x32(make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3), a.nkey0, l.k1);
+    const float sd = l.sgn * d;
+    if constexpr (DIM == 2) {
+      float sth, cth;
+      __sincosf(fmaf(f12(A.x), kTwoPiF, -kTwoPiF), &sth, &cth);
+      if constexpr (S::SRC != SRC_NONE) {
+        float sph, cph;
+        __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
+        const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
+        const float sr = l.sgn * r;
+        const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
+        l.acc = fmaf(-0.25f * d * d, source(l, a, g), l.acc);
+      }
+      l.x[0] = fmaf(sd, cth, l.x[0]);
+      l.x[1] = fmaf(sd, sth, l.x[1]);
+    } else {
+      const float z = fmaf(2.0f, f12(A.x), -3.0f);
+      const float sxy = fast_sqrt(fmaxf(0.0f, fmaf(-z, z, 1.0f)));
+      float sph, cph;
+      __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
+      if constexpr (S::SRC != SRC_NONE) {
+        const uint4 B =
+            philox4x32(make_uint4(2u * (uint32_t)l.step + 1u, l.c1, l.c2, l.c3), a.nkey0, l.k1);
+        const float vz = fmaf(2.0f, f12(A.z), -3.0f);
+        const float vs = fast_sqrt(fmaxf(0.0f, fmaf(-vz, vz, 1.0f)));
+        float vsp, vcp;
+        __sincosf(fmaf(f12(A.w), kTwoPiF, -kTwoPiF), &vsp, &vcp);
+        const float b0 = f12(B.x), b1 = f12(B.y), b2 = f12(B.z);
+        const float t = fmaxf(fminf(b0, b1), fminf(fmaxf(b0, b1), b2)) - 1.0f;  // Beta(2,2)
+        const float sr = l.sgn * (d * t);
+        const float g[3] = {fmaf(sr, vs * vcp, l.x[0]), fmaf(sr, vs * vsp, l.x[1]),
+                            fmaf(sr, vz, l.x[2])};
+        l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
+      }
+      l.x[0] = fmaf(sd, sxy * cph, l.x[0]);
+      l.x[1] = fmaf(sd, sxy * sph, l.x[1]);
+      l.x[2] = fmaf(sd, z, l.x[2]);
+    }
+  }
+
+  // ---------------- walk start ----------------
+  __device__ static __forceinline__ void start(Lane& l, const Real* table, const InstHdr* hdr,
+                                               const KArgs& a, const double* x0, int inst,
+                                               uint64_t pid, uint64_t tid, double sgn) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) l.x[i] = (Real)x0[i];
+    l.acc = Real(0);
+    l.sgn = (Real)sgn;
+    l.step = 0;
+    l.row = table + (size_t)inst * a.stride;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) l.dom[i] = l.row[kDomOff + i];
+    const InstHdr h = hdr[inst];
+    if constexpr (S::NATIVE) {
+      l.c1 = (uint32_t)pid;
+      l.c2 = (uint32_t)tid;
+      l.c3 = (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu);
+      l.k1 = a.nkey1_seed ^ h.nkey1;
+    } else {
+      l.pid = pid;
+      l.tid = tid;
+      l.ikey = h.ikey;
+    }
+    if constexpr (S::DOM == DOM_POLY) {
+      l.seg_off = h.seg_off;
+      l.n_seg = h.n_seg;
+    }
+  }
+};
+
+// ------------------------------------------------------------------------
+// warp-level helpers
+// ------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(WOS_FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ------------------------------------------------------------------------
+// the persistent kernel
+// ------------------------------------------------------------------------
+template <class S>
+__device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
+  using W = Walker<S>;
+  using Real = typename S::Real;
+  constexpr int DIM = S::DIM;
+  extern __shared__ __align__(16) unsigned char smem[];
+
+  // ---- stage the instance table into shared memory ----
+  Real* table = reinterpret_cast<Real*>(smem);
+  {
+    const int n4 = a.stage_bytes / 16;
+    const int4* src = reinterpret_cast<const int4*>(a.table);
+    int4* dst = reinterpret_cast<int4*>(smem);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem + a.stage_bytes +
+                         (size_t)warp * (kRing * sizeof(Real) + kRingWords * 4 + kUQ * 4);
+  Real* ring = reinterpret_cast<Real*>(wbase);
+  uint32_t* done = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
+  uint32_t* unitq = done + kRingWords;
+  for (int i = lane; i < kRingWords; i += 32) done[i] = 0u;
+  __syncthreads();
+
+  const bool est = a.sink == SINK_ESTIMATE;
+  const uint32_t IU = a.IU, L = a.L, U = a.U, C = a.chunk;
+  const Real eps = (Real)a.eps;
+
+  // warp-uniform stream state
+  uint32_t s_issue = 0, s_retire = 0, s_avail = 0, n_grabbed = 0;
+  bool exhausted = false;
+  bool dirty = false;           // a walk finished since the retire loop last stalled
+  uint32_t c_len = 0;           // cached geometry of the chunk at s_retire (0 = stale)
+  uint32_t c_j0 = 0;
+  uint64_t c_p = 0;
+  double run_n = 0.0, run_mean = 0.0, run_m2 = 0.0;  // Chan accumulator for L > chunk
+
+  typename W::Lane l;
+  bool active = false;
+  unsigned long long lane_steps = 0ull;
+
+  while (true) {
+    // ================= refill idle lanes =================
+    bool null_issued = false;
+    const unsigned idle = __ballot_sync(WOS_FULL, !active);
+    const int n_idle = __popc(idle);
+    if (n_idle >= a.refill_min || n_idle == 32) {
+      const uint32_t s_low = est ? s_retire : s_issue;
+      while (!exhausted && (s_avail - s_issue) < (uint32_t)n_idle &&
+             (n_grabbed - s_low / IU) < (uint32_t)kUQ) {
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(a.work_counter, 1u);
+        u = __shfl_sync(WOS_FULL, u, 0);
+        if (u >= a.n_units) {
+          exhausted = true;
+        } else {
+          if (lane == 0) unitq[n_grabbed % kUQ] = u;
+          ++n_grabbed;
+          s_avail += IU;
+        }
+      }
+      __syncwarp();
+      uint32_t n = min((uint32_t)n_idle, s_avail - s_issue);
+      if (est) n = min(n, s_retire + (uint32_t)kRing - s_issue);
+      const uint32_t rank = __popc(idle & lanemask_lt());
+      if (!active && rank < n) {
+        const uint32_t seq = s_issue + rank;
+        const uint32_t k = fast_div(seq, a.iu_mul, a.iu_shr);
+        const uint32_t r = seq - k * IU;
+        const uint32_t unit = unitq[k % kUQ];
+        if (est) {
+          const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
+          const uint32_t j = r - pl * L;
+          const uint64_t p = (uint64_t)unit * U + pl;
+          if (p < a.n_points) {
+            const int inst = a.inst_index ? a.inst_index[p] : 0;
+            const uint64_t tid = a.antithetic ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+            const double sg = (a.antithetic && (j & 1u)) ? -1.0 : 1.0;
+            W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
+                     (uint64_t)a.point_ids[p], tid, sg);
+            l.seq = seq;
+            active = true;
+          } else {
+            atomicOr(&done[(seq % kRing) >> 5], 1u << (seq & 31u));  // null item
+            null_issued = true;
+          }
+        } else {
+          const uint64_t row = (uint64_t)unit * IU + r;
+          if (row < a.n_points) {
+            W::start(l, table, a.hdr, a, a.points + (size_t)row * DIM, 0, a.row_pid[row],
+                     a.row_tid[row], a.row_sign[row]);
+            l.seq = (uint32_t)row;
+            active = true;
+          }
+        }
+      }
+      s_issue += n;
+    }
+
+    const bool any_active = __any_sync(WOS_FULL, active);
+    if (!any_active && exhausted && s_issue == s_avail && (!est || s_retire == s_issue)) break;
+
+    // ================= one step of every active walk =================
+    bool finished = false;
+    if (active) {
+      const Real d = W::dist(l, a);
+      if (d < eps || l.step >= a.max_steps) {
+        // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
+        Real q[DIM];
+        W::project(l, a, q);
+        const Real v = l.acc + W::boundary(l, a, q);
+        lane_steps += (unsigned long long)l.step;
+        if (est) {
+          ring[l.seq % kRing] = v;
+          atomicOr(&done[(l.seq % kRing) >> 5], 1u << (l.seq & 31u));
+        } else {
+          a.out_values[l.seq] = (double)v;
+          a.out_steps[l.seq] = (int64_t)l.step;
+          a.out_hits[l.seq] = (uint8_t)(d < eps);
+        }
+        active = false;
+        finished = true;
+      } else {
+        if constexpr (S::NATIVE) W::advance_native(l, d, a);
+        else W::advance_replay(l, d, a);
+        l.step += 1;
+      }
+    }
+
+    // ================= retire completed chunks (estimate sink) =================
+    if (est) {
+      dirty = dirty || __any_sync(WOS_FULL, finished || null_issued);
+      while (dirty && s_retire < s_issue) {
+        if (c_len == 0) {  // geometry of the chunk starting at s_retire
+          const uint32_t k = fast_div(s_retire, a.iu_mul, a.iu_shr);
+          const uint32_t r = s_retire - k * IU;
+          const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
+          c_j0 = r - pl * L;
+          c_len = min(C, L - c_j0);
+          c_p = (uint64_t)unitq[k % kUQ] * U + pl;
+        }
+        const uint32_t len = c_len;
+        if (s_retire + len > s_issue) {
+          dirty = false;
+          break;
+        }
+        // all done bits of [s_retire, s_retire + len) set?
+        const uint32_t w0 = s_retire >> 5, w1 = (s_retire + len - 1) >> 5;
+        const uint32_t wi = w0 + lane;
+        uint32_t mask = 0u;
+        if (wi <= w1) {
+          const uint32_t lo = (wi == w0) ? (s_retire & 31u) : 0u;
+          const uint32_t hi = (wi == w1) ? ((s_retire + len - 1) & 31u) : 31u;
+          mask = (hi == 31u ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+        }
+        const bool ok = (done[wi % kRingWords] & mask) == mask;
+        if (!__all_sync(WOS_FULL, ok)) {
+          dirty = false;
+          break;
+        }
+        const uint64_t p = c_p;
+        const uint32_t j0 = c_j0;
+        if (p < a.n_points) {
+          // two-pass moments over the chunk's samples (pair means if antithetic),
+          // fixed index order: independent of which lane ran which walk
+          const uint32_t ns = a.antithetic ? len / 2 : len;
+          double sum = 0.0;
+          for (uint32_t i = lane; i < ns; i += 32) {
+            double v;
+            if (a.antithetic)
+              v = ((double)ring[(s_retire + 2 * i) % kRing] +
+                   (double)ring[(s_retire + 2 * i + 1) % kRing]) / 2.0;
+            else
+              v = (double)ring[(s_retire + i) % kRing];
+            sum += v;
+          }
+          sum = warp_sum(sum);
+          const double mean = sum / (double)ns;
+          double m2 = 0.0;
+          for (uint32_t i = lane; i < ns; i += 32) {
+            double v;
+            if (a.antithetic)
+              v = ((double)ring[(s_retire + 2 * i) % kRing] +
+                   (double)ring[(s_retire + 2 * i + 1) % kRing]) / 2.0;
+            else
+              v = (double)ring[(s_retire + i) % kRing];
+            m2 += (v - mean) * (v - mean);
+          }
+          m2 = warp_sum(m2);
+          if (len == L) {
+            if (lane == 0) {
+              a.out_mean[p] = mean;
+              a.out_m2[p] = m2;
+            }
+          } else {
+            // Chan merge (estimator.chan_merge, estimator.py:41-53), chunks in order
+            const double n1 = run_n, n2 = (double)ns, nn = n1 + n2;
+            const double delta = mean - run_mean;
+            run_mean = run_mean + delta * (n2 / nn);
+            run_m2 = run_m2 + m2 + delta * delta * (n1 * n2 / nn);
+            run_n = nn;
+            if (j0 + len == L) {
+              if (lane == 0) {
+                a.out_mean[p] = run_mean;
+                a.out_m2[p] = run_m2;
+              }
+              run_n = run_mean = run_m2 = 0.0;
+            }
+          }
+        }
+        __syncwarp();
+        if (mask) done[wi % kRingWords] &= ~mask;
+        __syncwarp();
+        s_retire += len;
+        c_len = 0;
+      }
+    }
+  }
+
+  // ---- walk-step total (u64, deterministic integer sum) ----
+  if (a.total_steps != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lane_steps += __shfl_xor_sync(WOS_FULL, lane_steps, o);
+    if (lane == 0) atomicAdd(a.total_steps, lane_steps);
+  }
+}
+
+template <class S, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) wos_walk_kernel(const __grid_constant__ KArgs a) {
+  wos_kernel_body<S>(a);
+}
+
+}  // namespace wos

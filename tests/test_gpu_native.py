@@ -1,0 +1,176 @@
+"""NATIVE_F32 (production) estimator on the GPU.
+
+1. Walk-by-walk against the oracle's fp64 restatement of the native estimator
+   (same Philox4x32 stream): identical step counts for almost every walk.
+2. North-star check 2: per-point means agree with the reference-form oracle
+   within 4 combined standard errors (distributional: rms z and max |z|).
+3. North-star check 3: convergence to the analytic solutions (cfg0, cfg1, cfg4)
+   at the 1/sqrt(N) rate.
+4. Determinism: bitwise identical under re-runs, point order, batch layout and
+   launch shape (the reference's worker-count invariance, test_estimator.py:147-154).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _subset(w, n, seed=0):
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(w.n_points, size=n, replace=False))
+    return w.subset(idx)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_native_rows_match_native_oracle(gpu, cfg):
+    from paper_2603_01193_b200 import configs, walk_poisson_values
+
+    w = configs.build(cfg)
+    inst = 0
+    sel = np.flatnonzero(w.inst_index == inst)[:64]
+    T = 16
+    pts = np.repeat(w.points[sel], T, axis=0)
+    pid = np.repeat(w.point_ids[sel], T)
+    tid = np.tile(np.arange(T), sel.size)
+    sgn = np.ones(pts.shape[0])
+    v, s, h = walk_poisson_values(w.problems[inst], pts, pid, tid, sgn, w.cfg)
+    vo, so, ho = O.walk_rows(w.problems[inst], pts, pid, tid, sgn, seed=w.cfg.rng_seed,
+                             eps=w.cfg.eps_shell, max_steps=w.cfg.max_steps, native=True)
+    same = np.mean(s == so)
+    assert same >= 0.99, f"identical steps {same:.4%}"
+    m = s == so
+    rms = np.sqrt(np.mean(vo**2)) + 1e-30
+    err = np.abs(v[m] - vo[m]) / np.maximum(np.abs(vo[m]), rms)
+    assert np.quantile(err, 0.99) < 1e-3, f"p99 rel err {np.quantile(err, 0.99):.2e}"
+
+
+def _z(m1, se1, m2, se2):
+    # floor: points starting inside the eps-shell have zero variance in both arms,
+    # so only fp32 rounding of g separates them
+    floor = 1e-6 * np.maximum(1.0, np.abs(m2))
+    return (m1 - m2) / np.sqrt(se1**2 + se2**2 + floor**2)
+
+
+@pytest.mark.parametrize("cfg,npts,L", [(0, 48, 4096), (1, 32, 4096), (3, 32, 1024), (4, 24, 4096)])
+def test_native_statistically_matches_reference_form(gpu, cfg, npts, L):
+    from paper_2603_01193_b200 import configs, estimate_arrays
+
+    w = _subset(configs.build(cfg), npts, seed=cfg)
+    mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, inst_index=w.inst_index,
+                                  point_ids=w.point_ids)
+    se = np.sqrt(m2 / (n - 1) / n)
+    om, om2, _ = O.estimate(w.problems, w.points, L, seed=w.cfg.rng_seed + 1, eps=w.cfg.eps_shell,
+                            max_steps=w.cfg.max_steps, point_ids=w.point_ids, inst_index=w.inst_index)
+    ose = np.sqrt(om2 / (L - 1) / L)
+    z = _z(mean, se, om, ose)
+    assert np.max(np.abs(z)) < 4.5, f"max |z| {np.max(np.abs(z)):.2f}"
+    rmsz = float(np.sqrt(np.mean(z**2)))
+    assert 0.55 < rmsz < 1.5, f"rms z {rmsz:.2f}"
+
+
+def test_native_cfg2_pooled_statistics(gpu):
+    """cfg2 runs L = 4 (noisy labels): per-point SEs are Student-t(3); pool per instance."""
+    from paper_2603_01193_b200 import configs, estimate_arrays
+
+    w = configs.build(2)
+    sel = np.flatnonzero(w.inst_index < 4)
+    w = w.subset(sel[::16])
+    L = 512
+    mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, inst_index=w.inst_index,
+                                  point_ids=w.point_ids)
+    om, om2, _ = O.estimate(w.problems, w.points, L, seed=7, eps=w.cfg.eps_shell,
+                            max_steps=w.cfg.max_steps, point_ids=w.point_ids, inst_index=w.inst_index)
+    z = _z(mean, np.sqrt(m2 / (L - 1) / L), om, np.sqrt(om2 / (L - 1) / L))
+    assert np.max(np.abs(z)) < 4.5
+    assert 0.6 < float(np.sqrt(np.mean(z**2))) < 1.4
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 4])
+def test_native_converges_to_analytic(gpu, cfg):
+    from paper_2603_01193_b200 import configs, estimate_arrays
+
+    w = _subset(configs.build(cfg), 64, seed=10 + cfg)
+    exact = w.analytic(w.points)
+    errs = {}
+    for L in (256, 16384):
+        mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, point_ids=w.point_ids,
+                                      traj_start=10**6)
+        se = np.sqrt(m2 / (n - 1) / n)
+        z = (mean - exact) / se
+        assert np.max(np.abs(z)) < 4.5, f"L={L} max |z| {np.max(np.abs(z)):.2f}"
+        assert 0.6 < float(np.sqrt(np.mean(z**2))) < 1.4
+        errs[L] = float(np.sqrt(np.mean((mean - exact) ** 2)))
+    ratio = errs[256] / errs[16384]
+    assert 5.0 < ratio < 12.0, f"rms error ratio {ratio:.2f} (1/sqrt(N) predicts 8)"
+
+
+def test_native_se_ratio(gpu):
+    """test_walker.py:146-150: SE from 100 walks vs 10^4 walks ratio in [8, 12]."""
+    from paper_2603_01193_b200 import BallDomain, Problem, WalkConfig, walk_poisson_values
+
+    prob = Problem(BallDomain([0.0, 0.0], 1.0), boundary_spec=(0, (0.0,)), source_spec=(1, (1.0,)))
+    n = 10_000
+    v, _, _ = walk_poisson_values(prob, np.zeros((n, 2)), np.zeros(n), np.arange(n), np.ones(n),
+                                  WalkConfig(rng_seed=13))
+    se_small = v[:100].std(ddof=1) / 10.0
+    se_big = v.std(ddof=1) / 100.0
+    assert 8.0 <= se_small / se_big <= 12.0
+    assert abs(v.mean() + 0.25) < 4 * se_big
+
+
+def test_native_determinism_and_layout_invariance(gpu):
+    from paper_2603_01193_b200 import configs, engine, estimate_arrays
+
+    w = _subset(configs.build(4), 300, seed=3)
+    a = estimate_arrays(w.problems, w.points, 256, w.cfg, point_ids=w.point_ids)
+    b = estimate_arrays(w.problems, w.points, 256, w.cfg, point_ids=w.point_ids)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    perm = np.random.default_rng(1).permutation(w.n_points)
+    c = estimate_arrays(w.problems, w.points[perm], 256, w.cfg, point_ids=w.point_ids[perm])
+    assert np.array_equal(c[0], a[0][perm]) and np.array_equal(c[1], a[1][perm])
+    d = estimate_arrays(w.problems, w.points[:7], 256, w.cfg, point_ids=w.point_ids[:7])
+    assert np.array_equal(d[0], a[0][:7])
+    ctx = engine.get_context(0)
+    try:
+        ctx.set_tuning(refill_min=17, blocks_per_sm=1)
+        e = estimate_arrays(w.problems, w.points, 256, w.cfg, point_ids=w.point_ids)
+    finally:
+        ctx.set_tuning()
+    assert np.array_equal(e[0], a[0]) and np.array_equal(e[1], a[1])
+
+
+def test_native_antithetic_pair_cancels_linear_data(gpu):
+    """test_walker.py:219-229 in the native mode."""
+    from paper_2603_01193_b200 import (BallDomain, Problem, TrajectoryStream, WalkConfig,
+                                       walk_poisson_antithetic)
+
+    inst = Problem(BallDomain([0.0, 0.0], 1.0), boundary_spec=(2, (1.0, 0.0, 0.0)))
+    for t in range(20):
+        a, b = walk_poisson_antithetic(inst, [0.0, 0.0], WalkConfig(rng_seed=29), TrajectoryStream(0, t))
+        assert a.value + b.value == 0.0
+        assert a.steps_taken == b.steps_taken
+
+
+@pytest.mark.parametrize("mode", ["replay", "native"])
+def test_long_ensembles_use_chunked_reduction(gpu, mode):
+    """L > 512 merges per-chunk moments (Chan) in fixed order; compare with the oracle."""
+    from paper_2603_01193_b200 import configs, estimate_arrays
+
+    w = _subset(configs.build(0, mode=mode), 6, seed=4)
+    L = 1500
+    mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, point_ids=w.point_ids, traj_start=3)
+    om, om2, _ = O.estimate(w.problems, w.points, L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
+                            max_steps=w.cfg.max_steps, point_ids=w.point_ids, traj_start=3,
+                            native=(mode == "native"))
+    if mode == "replay":
+        np.testing.assert_allclose(mean, om, rtol=1e-9, atol=1e-14)
+        np.testing.assert_allclose(m2, om2, rtol=1e-8)
+    else:
+        np.testing.assert_allclose(mean, om, rtol=2e-3, atol=2e-6)
+        np.testing.assert_allclose(m2, om2, rtol=2e-2)
+    assert np.all(n == L)

@@ -1,0 +1,135 @@
+"""Pin the CPU oracle (oracle/wos_oracle.c) to the reference's own outputs.
+
+Golden fixtures were produced by running the reference package itself
+(tests/golden/make_golden.py): Philox words from rng.philox4x64, uniform draws
+captured from live reference walks, per-walk (values, steps, hits) from
+walker.walk_poisson_values on every BASELINE config, estimator.estimate
+moments, and the reference's numba kernels on spec-coded disk/ball problems.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_records, load_golden
+from oracle import oracle as O
+
+CFGS = [0, 1, 2, 3, 4]
+
+
+def test_philox4x64_random123_kat():
+    for ctr, key, want in O.PHILOX4X64_KAT:
+        assert O.philox4x64_int(ctr, key) == list(want)
+        assert [int(w) for w in O.philox4x64([ctr], *key)[0]] == list(want)
+
+
+def test_philox4x32_random123_kat():
+    for ctr, key, want in O.PHILOX4X32_KAT:
+        assert O.philox4x32_int(ctr, key) == list(want)
+        assert [int(w) for w in O.philox4x32([ctr], *key)[0]] == list(want)
+
+
+def test_philox4x64_matches_reference_words():
+    z = load_golden("golden_rng.npz")
+    for c, k, w in zip(z["ctr"], z["key"], z["words"]):
+        assert O.philox4x64_int(c, k) == [int(v) for v in w]
+        got = O.philox4x64([c], int(k[0]), int(k[1]))[0]
+        assert np.array_equal(got, w)
+
+
+def test_philox4x64_numpy_cross_check():
+    # numpy's Philox block at counter c equals the reference's at c + 1 (test_rng.py:29-39)
+    z = load_golden("golden_rng.npz")
+    k0, k1 = (int(v) for v in z["np_key"])
+    for blk in range(4):
+        assert O.philox4x64_int((blk + 1, 0, 0, 0), (k0, k1)) == [int(v) for v in z["np_raw"][blk]]
+
+
+def test_captured_reference_draws():
+    z = load_golden("golden_capture.npz")
+    for k0, k1 in {(int(a), int(b)) for a, b in z["key"]}:
+        m = (z["key"][:, 0] == k0) & (z["key"][:, 1] == k1)
+        got = O.philox4x64(z["ctr"][m], k0, k1)
+        assert np.array_equal(got, z["words"][m])
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_oracle_rows_match_reference(cfg):
+    z = load_golden(f"golden_cfg{cfg}.npz")
+    recs = golden_records(z)
+    seed, eps, ms = int(z["seed"][0]), float(z["eps"][0]), int(z["max_steps"][0])
+    for inst in np.unique(z["inst"]):
+        m = z["inst"] == inst
+        v, s, h = O.walk_rows(recs[inst], z["points"][m], z["pid"][m], z["tid"][m], z["sign"][m],
+                              seed=seed, eps=eps, max_steps=ms)
+        assert np.array_equal(s, z["steps"][m])
+        assert np.array_equal(h, z["hits"][m])
+        np.testing.assert_allclose(v, z["values"][m], rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_oracle_truncated_walks(cfg):
+    z = load_golden(f"golden_cfg{cfg}.npz")
+    rec = golden_records(z)[int(z["t_inst"][0])]
+    v, s, h = O.walk_rows(rec, z["t_points"], z["t_pid"], z["t_tid"], z["t_sign"],
+                          seed=int(z["seed"][0]), eps=float(z["eps"][0]), max_steps=3)
+    assert np.array_equal(s, z["t_steps"])
+    assert np.array_equal(h, z["t_hits"])
+    assert (z["t_hits"] == 0).any()  # the fixture exercises the max_steps exit
+    np.testing.assert_allclose(v, z["t_values"], rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 4])
+@pytest.mark.parametrize("anti", [False, True])
+def test_oracle_estimate_matches_reference(cfg, anti):
+    from paper_2603_01193_b200 import configs
+
+    w = configs.build(cfg)
+    z = load_golden("golden_estimate.npz")
+    tag = f"cfg{cfg}_{'anti' if anti else 'plain'}"
+    sel = z[tag + "_sel"]
+    L = int(z[tag + "_L"][0])
+    mean, m2, _ = O.estimate(w.problems, w.points[sel], L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
+                             max_steps=w.cfg.max_steps, point_ids=w.point_ids[sel], traj_start=5,
+                             antithetic=anti)
+    np.testing.assert_allclose(mean, z[tag + "_mean"], rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(m2, z[tag + "_m2"], rtol=1e-7, atol=1e-14)
+
+
+def _refkernel_record(z, name):
+    from paper_2603_01193_b200 import specs
+
+    dim = int(z[name + "_dim"][0])
+    src = z[name + "_src"]
+    bnd = z[name + "_bnd"]
+    dom = (0.0,) * dim + (1.0,)
+    sk = specs.SRC_NONE if src[0] < 0 else int(src[0])
+    sp = () if src[0] < 0 else tuple(src[1:])
+    return (dim, specs.DOM_BALL, dom, sk, sp, int(bnd[0]), tuple(bnd[1:]), 3)
+
+
+def test_oracle_matches_reference_numba_kernels():
+    z = load_golden("golden_refkernels.npz")
+    for name in z["names"]:
+        name = str(name)
+        rec = _refkernel_record(z, name)
+        v, s, h = O.walk_rows(rec, z[name + "_points"], z[name + "_pid"], z[name + "_tid"],
+                              z[name + "_sign"], seed=11, eps=float(z[name + "_eps"][0]), max_steps=1000)
+        assert np.array_equal(s, z[name + "_steps"]), name
+        np.testing.assert_allclose(v, z[name + "_values"], rtol=1e-10, atol=1e-13, err_msg=name)
+
+
+def test_golden_records_match_config_builders():
+    """The pinned synthetic configs still produce the problems the fixtures were made from."""
+    from paper_2603_01193_b200 import configs
+    from paper_2603_01193_b200.engine import problem_record
+
+    for cfg in CFGS:
+        z = load_golden(f"golden_cfg{cfg}.npz")
+        recs = golden_records(z)
+        w = configs.build(cfg)
+        for i, r in enumerate(recs):
+            mine = problem_record(w.problems[i])
+            assert mine[:2] == r[:2] and mine[3] == r[3] and mine[5] == r[5] and mine[7] == r[7]
+            np.testing.assert_array_equal(mine[2], r[2])
+            np.testing.assert_array_equal(mine[4], r[4])
+            np.testing.assert_array_equal(mine[6], r[6])
