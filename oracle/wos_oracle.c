@@ -360,15 +360,11 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       *hit = (uint8_t)shell;
       return;
     }
-    /* block A = Philox4x32(2*step, ...), block B = Philox4x32(2*step+1, ...) (3D source only) */
-    uint32_t u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    /* one Philox4x32 block per jump at counter (2*step, pid, tid, hi-words) */
+    uint32_t u[4];
     {
       uint32_t ca[4] = {(uint32_t)(2 * step), c1, c2, c3};
       philox4x32(ca, k0, k1, u);
-      if (dim == 3 && has_src) {
-        uint32_t cb[4] = {(uint32_t)(2 * step + 1), c1, c2, c3};
-        philox4x32(cb, k0, k1, u + 4);
-      }
     }
     double dir[3];
     if (dim == 2) {
@@ -381,22 +377,38 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
         double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
         acc -= (d * d * 0.25) * source(pb, g);
       }
-    } else {
+    } else if (!has_src) {
       double z = 2.0 * u23(u[0]) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
       double phi = TWO_PI * u23(u[1]);
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;
-      if (has_src) {
-        double vz = 2.0 * u23(u[2]) - 1.0;
-        double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
-        double vphi = TWO_PI * u23(u[3]);
-        double r = d * med3(u23(u[4]), u23(u[5]), u23(u[6]));
-        double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
-                       x[2] + sgn * r * vz};
-        acc -= (d * d * (1.0 / 6.0)) * source(pb, g);
-      }
+    } else {
+      /* seven uniforms from the block's 128 bits (wos_walk.cuh native_uniforms7):
+         v[0..3] = top 23 bits of each word; v[4..6] = 12-bit fields (9 low bits of
+         u[0..2] and 3 bits of u[3]), midpoint-rounded (b + 1/2) 2^-12 */
+      double v[7];
+      for (int k = 0; k < 4; ++k) v[k] = u23(u[k]);
+      uint32_t b4 = ((u[0] & 0x1FFu) << 3) | (u[3] & 0x7u);
+      uint32_t b5 = ((u[1] & 0x1FFu) << 3) | ((u[3] >> 3) & 0x7u);
+      uint32_t b6 = ((u[2] & 0x1FFu) << 3) | ((u[3] >> 6) & 0x7u);
+      v[4] = ((double)b4 + 0.5) * (1.0 / 4096.0);
+      v[5] = ((double)b5 + 0.5) * (1.0 / 4096.0);
+      v[6] = ((double)b6 + 0.5) * (1.0 / 4096.0);
+      double z = 2.0 * v[0] - 1.0;
+      double s = sqrt(fmax(0.0, 1.0 - z * z));
+      double phi = TWO_PI * v[1];
+      dir[0] = s * cos(phi);
+      dir[1] = s * sin(phi);
+      dir[2] = z;
+      double vz = 2.0 * v[2] - 1.0;
+      double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
+      double vphi = TWO_PI * v[3];
+      double r = d * med3(v[4], v[5], v[6]);
+      double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
+                     x[2] + sgn * r * vz};
+      acc -= (d * d * (1.0 / 6.0)) * source(pb, g);
     }
     for (int i = 0; i < dim; ++i) x[i] += sgn * d * dir[i];
   }

@@ -56,7 +56,7 @@ struct wos_context {
   int64_t host_exterior = -1;
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
-  int refill_min = 2;
+  int refill_min = 4;
   int blocks_per_sm = 0;
   std::mutex mu;  // serialises the *_host entry points' scratch
 };
@@ -76,6 +76,8 @@ struct wos_problem_set {
   double* d_segs_d = nullptr;             // [nseg][ax, ay, ex, ey]
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
   float4* d_segs_n = nullptr;             // NATIVE: [nseg][2] float4
+  std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
+  uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
 
 extern "C" int wos_abi_version(void) { return WOS_ABI_VERSION; }
@@ -324,6 +326,11 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       }
     }
     for (int k = 0; k < 8; ++k) rn[k] = (float)rd[k];
+    if (p.dom_kind == WOS_DOM_BOX)  // NATIVE box distance: centre and half extent
+      for (int k = 0; k < dim; ++k) {
+        rn[8 + k] = (float)(0.5 * (p.dom[k] + p.dom[dim + k]));
+        rn[12 + k] = (float)(0.5 * (p.dom[dim + k] - p.dom[k]));
+      }
     // source
     double* sd = rd + kSrcOff;
     float* sn = rn + kSrcOff;
@@ -387,6 +394,8 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     }
     for (int k = 0; k < nb; ++k) rn[s->bnd_off + k] = (float)bd[k];
   }
+  s->h_row_n.assign(tn.begin(), tn.begin() + stride);
+  s->h_nkey1 = hd[0].nkey1;
   std::vector<float> tf(td.size());
   for (size_t k = 0; k < td.size(); ++k) tf[k] = (float)td[k];
   std::vector<float> segf(segd.size());
@@ -523,10 +532,11 @@ extern "C" int wos_context_exterior(wos_context* c, void* stream, int64_t* out) 
 struct KernelInfo {
   const void* fn;
   size_t elem;  // sizeof(Real)
+  bool one;     // single-instance NATIVE launch (parameters in the constant bank)
 };
 
 static KernelInfo pick_kernel(const wos_problem_set* s, int mode) {
-  KernelInfo k{nullptr, 8};
+  KernelInfo k{nullptr, 8, false};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
     k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0);
@@ -536,14 +546,15 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode) {
     k.elem = 4;
   } else {
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
-    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk);
+    k.one = (s->n == 1 && s->stride <= kCP);
+    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one);
     k.elem = 4;
   }
   return k;
 }
 
 static size_t smem_bytes(size_t stage, size_t elem) {
-  return stage + (size_t)kWarps * (kRing * elem + kRingWords * 4 + kUQ * 4);
+  return stage + (size_t)kWarps * (kRing * elem + kSlots * 4 + kUQ * 4);
 }
 
 static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
@@ -567,6 +578,17 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     a.segs = s->d_segs_n;
     a.stage_bytes = (int)s->bytes_f;
     a.sine_K = s->sine_K_native;
+    if (k.one) {
+      // instance row and Philox4x32 round keys ride in the kernel parameters
+      a.stage_bytes = 0;
+      memcpy(a.cp, s->h_row_n.data(), sizeof(float) * s->stride);
+      const uint32_t k0 = (uint32_t)cfg->rng_seed;
+      const uint32_t k1 = (uint32_t)(cfg->rng_seed >> 32) ^ s->h_nkey1;
+      for (int r = 0; r < 10; ++r) {
+        a.rk0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        a.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+      }
+    }
   }
   a.hdr = s->d_hdr;
   a.n_inst = s->n;
@@ -625,7 +647,7 @@ extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos
     a.U = kUnitTarget;
     a.IU = kUnitTarget;
     a.n_units = (uint32_t)((m + kUnitTarget - 1) / kUnitTarget);
-    a.chunk = 1;
+    a.n_chunks = 1;
     fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
     fast_div_init(1, &a.l_mul, &a.l_shr);
     a.points = points + off * s->dim;
@@ -669,7 +691,7 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
     a.U = (uint32_t)std::max<int64_t>(1, (kUnitTarget + L - 1) / L);
     a.IU = a.U * a.L;
     a.n_units = (uint32_t)((m + a.U - 1) / a.U);
-    a.chunk = (uint32_t)std::min<int64_t>(L, kChunkMax);
+    a.n_chunks = (uint32_t)((L + kChunkMax - 1) / kChunkMax);
     fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
     fast_div_init(a.L, &a.l_mul, &a.l_shr);
     a.points = points + off * s->dim;

@@ -4,12 +4,14 @@
 
 namespace wos {
 
-#define WOS_K(DIM, DOM, SRC, SK)                                             \
-  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                    \
-    return reinterpret_cast<const void*>(                                    \
-        &wos_walk_kernel<Spec<MODE_NATIVE_F32, DIM, DOM, SRC, SK>, 3>);
+#define WOS_K(DIM, DOM, SRC, SK)                                                   \
+  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                          \
+    return one ? reinterpret_cast<const void*>(                                    \
+                     &wos_walk_kernel<Spec<MODE_NATIVE_F32, DIM, DOM, SRC, SK, true>, 3>) \
+               : reinterpret_cast<const void*>(                                    \
+                     &wos_walk_kernel<Spec<MODE_NATIVE_F32, DIM, DOM, SRC, SK, false>, 3>);
 
-const void* get_kernel_native(int dim, int dom, int src, int sk) {
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one) {
   // 2D
   WOS_K(2, DOM_BALL, SRC_NONE, 0)
   WOS_K(2, DOM_BALL, SRC_CONST, 0)

@@ -53,6 +53,21 @@ __device__ __forceinline__ uint4 philox4x32(uint4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Same with a precomputed round-key schedule (rk0[r] = k0 + r W0, rk1[r] = k1 + r W1).
+// With the schedule in the kernel parameters the XORs take c[] operands directly.
+__device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const uint32_t* rk0, const uint32_t* rk1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint64_t p0 = (uint64_t)M0 * c.x;
+    uint64_t p1 = (uint64_t)M1 * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c = make_uint4(hi1 ^ c.y ^ rk0[r], lo1, hi0 ^ c.w ^ rk1[r], lo0);
+  }
+  return c;
+}
+
 // NATIVE uniform: (w >> 9) * 2^-23 in [0, 1), exact in fp32 (one LOP3 + one FADD).
 __device__ __forceinline__ float u01_23(uint32_t w) {
   return __uint_as_float(0x3f800000u | (w >> 9)) - 1.0f;

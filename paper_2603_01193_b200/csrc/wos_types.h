@@ -20,12 +20,15 @@ enum : int { SINK_ROWS = 0, SINK_ESTIMATE = 1 };
 constexpr int kBlock = 256;       // threads per CTA (8 warps)
 constexpr int kWarps = kBlock / 32;
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
-constexpr int kRingWords = kRing / 32;
+constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
-constexpr int kChunkMax = kRing / 2;  // longest run of one point's walks reduced at once
+constexpr int kChunkMax = 512;    // L > kChunkMax: a point retires in chunks of kChunkMax walks
+constexpr int kChunkShift = 9;    // log2(kChunkMax)
 constexpr int kUnitTarget = 128;  // minimum walks per grabbed work unit
+constexpr int kCP = 256;          // floats of single-instance parameters held in the kernel params
 constexpr int kDomOff = 0;        // table row: [0, 8) domain params
-constexpr int kSrcOff = 8;        //            [8, 8 + ns) source params, then boundary params
+constexpr int kSrcOff = 16;       //            [16, 16 + ns) source params, then boundary params
+// NATIVE box rows also hold the centre at [8, 11) and the half extent at [12, 15)
 
 // Per-instance header (32 bytes), one per problem of a set.
 struct InstHdr {
@@ -78,7 +81,7 @@ struct KArgs {
   uint32_t U;           // points per work unit
   uint32_t IU;          // items (walks) per work unit = U * L
   uint32_t n_units;
-  uint32_t chunk;       // reduction chunk = min(L, kChunkMax)
+  uint32_t n_chunks;    // L > kChunkMax: chunks per point (ceil(L / kChunkMax)); else 1
   uint32_t iu_mul, iu_shr;  // magic numbers: n / IU = (umulhi(n, mul) + n) >> shr, n < 2^31
   uint32_t l_mul, l_shr;    // same for n / L
   const double* points;        // [n, dim]
@@ -96,6 +99,11 @@ struct KArgs {
   double* out_m2;
   unsigned long long* total_steps;
   unsigned int* work_counter;
+  // ---- single-instance NATIVE launches: the instance row and the Philox round
+  // keys live in the kernel-parameter constant bank (FFMA / LOP3 c[] operands) ----
+  uint32_t rk0[10];
+  uint32_t rk1[10];
+  alignas(16) float cp[kCP];
 };
 
 }  // namespace wos

