@@ -37,7 +37,7 @@ WOS_ERR_EXTERIOR = 4
 WOS_ERR_NOMEM = 5
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libwos_b200.so")
+lib_path = os.environ.get("WOS_B200_LIB") or os.path.join(_HERE, "libwos_b200.so")
 
 
 class WosError(RuntimeError):

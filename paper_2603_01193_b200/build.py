@@ -30,10 +30,12 @@ COMMON = ARCH + [
 UNITS = {
     "wos_capi.cu": [],
     "wos_kernels_native.cu": [],
+    "wos_kernels_native_est.cu": [],
+    "wos_kernels_native_rows.cu": [],
     "wos_kernels_replay_f64.cu": ["--fmad=false"],
     "wos_kernels_replay_f32.cu": ["--fmad=false"],
 }
-HEADERS = ["wos_types.h", "wos_rng.cuh", "wos_walk.cuh", "wos_kernels.h"]
+HEADERS = ["wos_types.h", "wos_rng.cuh", "wos_walk.cuh", "wos_kernels.h", "wos_kernels_native.inc"]
 
 
 def _stale(obj, deps):
@@ -43,8 +45,8 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, extra, verbose):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+def _compile(src, extra, verbose, build_dir=None):
+    obj = os.path.join(build_dir or BUILD, src.replace(".cu", ".o"))
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(HERE, "..", "include", "wos_b200.h")
     ]
@@ -59,26 +61,35 @@ def _compile(src, extra, verbose):
     return obj, r.stderr if verbose else None
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines=(),
+          out: str | None = None) -> str:
+    """Compile every unit and link the shared library.
+
+    ``defines``/``out`` build an experimental variant (e.g. WOS_NATIVE_MINB=3) into a
+    separate directory and library; load it with WOS_B200_LIB=<path>.
+    """
+    build_dir = BUILD if not out else os.path.join(HERE, "_build_" + os.path.basename(out).split(".")[0])
+    lib = LIB if not out else os.path.join(HERE, out)
+    os.makedirs(build_dir, exist_ok=True)
     if force:
-        for f in os.listdir(BUILD):
-            os.remove(os.path.join(BUILD, f))
+        for f in os.listdir(build_dir):
+            os.remove(os.path.join(build_dir, f))
+    extra_d = [f"-D{d}" for d in defines]
     jobs = jobs or min(len(UNITS), os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        futs = [ex.submit(_compile, s, e, verbose) for s, e in UNITS.items()]
+        futs = [ex.submit(_compile, s, e + extra_d, verbose, build_dir) for s, e in UNITS.items()]
         objs = []
         for f in futs:
             obj, log = f.result()
             objs.append(obj)
             if log:
                 print(log, file=sys.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
@@ -86,5 +97,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    print(build(a.force, a.jobs, a.verbose))
+    print(build(a.force, a.jobs, a.verbose, a.defines, a.out))

@@ -53,6 +53,7 @@ struct wos_context {
   std::atomic<unsigned> next_counter{0};
   unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
   unsigned long long* d_steps = nullptr;     // total-steps scratch of the *_host variants
+  unsigned int* d_watchdog = nullptr;        // kernel iteration-limit flag
   int64_t host_exterior = -1;
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -101,6 +102,8 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, sizeof(unsigned) * kCounterRing);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_exterior, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_watchdog, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->d_watchdog, 0, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->d_exterior, 0xff, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     delete c;
@@ -116,6 +119,7 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_counters);
   cudaFree(c->d_exterior);
   cudaFree(c->d_steps);
+  cudaFree(c->d_watchdog);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -493,13 +497,24 @@ static int launch_interior(wos_context* c, const wos_problem_set* s, int64_t n, 
   return WOS_OK;
 }
 
+static int check_watchdog(wos_context* c, cudaStream_t st) {
+  unsigned int w = 0;
+  CUDA_TRY(cudaMemcpyAsync(&w, c->d_watchdog, sizeof(w), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (w) {
+    cudaMemsetAsync(c->d_watchdog, 0, sizeof(w), st);
+    return fail(WOS_ERR_CUDA, "walk kernel watchdog tripped (iteration limit): results invalid");
+  }
+  return WOS_OK;
+}
+
 static int read_exterior(wos_context* c, cudaStream_t st, int64_t* out) {
   unsigned long long v = 0;
   CUDA_TRY(cudaMemcpyAsync(&v, c->d_exterior, sizeof(v), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, sizeof(v), st));
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = (v == ~0ull) ? -1 : (int64_t)v;
-  return WOS_OK;
+  return check_watchdog(c, st);
 }
 
 extern "C" int wos_check_interior(wos_context* c, const wos_problem_set* s, int64_t n,
@@ -535,19 +550,19 @@ struct KernelInfo {
   bool one;     // single-instance NATIVE launch (parameters in the constant bank)
 };
 
-static KernelInfo pick_kernel(const wos_problem_set* s, int mode) {
+static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
   KernelInfo k{nullptr, 8, false};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
-    k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0);
+    k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0, rows);
     k.elem = 8;
   } else if (mode == WOS_MODE_REPLAY_F32) {
-    k.fn = get_kernel_replay_f32(s->dim, dom, s->src_kind, 0);
+    k.fn = get_kernel_replay_f32(s->dim, dom, s->src_kind, 0, rows);
     k.elem = 4;
   } else {
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
     k.one = (s->n == 1 && s->stride <= kCP);
-    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one);
+    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows);
     k.elem = 4;
   }
   return k;
@@ -559,7 +574,7 @@ static size_t smem_bytes(size_t stage, size_t elem) {
 
 static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
                        KArgs a, cudaStream_t st) {
-  const KernelInfo k = pick_kernel(s, cfg->mode);
+  const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS);
   if (!k.fn)
     return fail(WOS_ERR_UNSUPPORTED, "no kernel for dim %d domain %d source %d mode %d", s->dim,
                 s->dom_kind, s->src_kind, cfg->mode);
@@ -618,6 +633,8 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   grid = std::max<int64_t>(grid, 1);
   unsigned slot = c->next_counter.fetch_add(1) % kCounterRing;
   a.work_counter = c->d_counters + slot;
+  a.watchdog = c->d_watchdog;
+  a.iter_limit = (uint32_t)std::min<int64_t>(0xffffffffll, std::max<int64_t>(1ll << 27, 4 * (int64_t)a.max_steps));
   CUDA_TRY(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned), st));
   void* args[] = {&a};
   CUDA_TRY(cudaLaunchKernel(k.fn, dim3((unsigned)grid), dim3(kBlock), args, smem, st));
@@ -753,7 +770,7 @@ extern "C" int wos_walk_rows_host(wos_context* c, const wos_problem_set* s,
   CUDA_TRY(cudaMemcpyAsync(out_steps, d_stp, n * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(out_hits, d_hit, n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  return WOS_OK;
+  return check_watchdog(c, st);
 }
 
 extern "C" int wos_check_interior_host(wos_context* c, const wos_problem_set* s, int64_t n,
@@ -819,6 +836,8 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, 8, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (out_total_steps) *out_total_steps = steps;
+  r = check_watchdog(c, st);
+  if (r) return r;
   if (ext != ~0ull) {
     c->host_exterior = (int64_t)ext;
     return fail(WOS_ERR_EXTERIOR, "exterior query: start point %lld", (long long)ext);

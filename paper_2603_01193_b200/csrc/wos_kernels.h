@@ -3,8 +3,9 @@
 
 namespace wos {
 // Returns the __global__ entry for (dim, domain, source, sine order) or nullptr.
-const void* get_kernel_replay_f64(int dim, int dom, int src, int sk);
-const void* get_kernel_replay_f32(int dim, int dom, int src, int sk);
+// rows = walk_poisson_values sink (per-walk outputs) instead of the per-point estimate
+const void* get_kernel_replay_f64(int dim, int dom, int src, int sk, bool rows);
+const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows);
 // one = single-instance launch (instance row + Philox keys in the kernel parameters)
-const void* get_kernel_native(int dim, int dom, int src, int sk, bool one);
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows);
 }  // namespace wos

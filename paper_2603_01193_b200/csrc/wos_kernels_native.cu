@@ -1,45 +1,11 @@
-// Kernel instantiations for MODE_NATIVE_F32 (see wos_walk.cuh).
+// NATIVE_F32 kernel lookup (instantiations live in wos_kernels_native_{est,rows}.cu).
 #include "wos_kernels.h"
-#include "wos_walk.cuh"
 
 namespace wos {
+const void* get_kernel_native_est(int dim, int dom, int src, int sk, bool one);
+const void* get_kernel_native_rows(int dim, int dom, int src, int sk, bool one);
 
-#define WOS_K(DIM, DOM, SRC, SK)                                                   \
-  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                          \
-    return one ? reinterpret_cast<const void*>(                                    \
-                     &wos_walk_kernel<Spec<MODE_NATIVE_F32, DIM, DOM, SRC, SK, true>, 3>) \
-               : reinterpret_cast<const void*>(                                    \
-                     &wos_walk_kernel<Spec<MODE_NATIVE_F32, DIM, DOM, SRC, SK, false>, 3>);
-
-const void* get_kernel_native(int dim, int dom, int src, int sk, bool one) {
-  // 2D
-  WOS_K(2, DOM_BALL, SRC_NONE, 0)
-  WOS_K(2, DOM_BALL, SRC_CONST, 0)
-  WOS_K(2, DOM_BALL, SRC_RBF2, 0)
-  WOS_K(2, DOM_BALL, SRC_SINE, 0)
-  WOS_K(2, DOM_BALL, SRC_GAUSS, 0)
-  WOS_K(2, DOM_BOX, SRC_NONE, 0)
-  WOS_K(2, DOM_BOX, SRC_CONST, 0)
-  WOS_K(2, DOM_BOX, SRC_SINE, 0)
-  WOS_K(2, DOM_BOX, SRC_GAUSS, 0)
-  WOS_K(2, DOM_POLY, SRC_NONE, 0)
-  WOS_K(2, DOM_POLY, SRC_CONST, 0)
-  WOS_K(2, DOM_POLY, SRC_SINE, 0)
-  WOS_K(2, DOM_POLY, SRC_GAUSS, 0)
-  // 3D
-  WOS_K(3, DOM_BALL, SRC_NONE, 0)
-  WOS_K(3, DOM_BALL, SRC_CONST, 0)
-  WOS_K(3, DOM_BALL, SRC_SINE, 0)
-  WOS_K(3, DOM_BALL, SRC_GAUSS, 0)
-  WOS_K(3, DOM_BOX, SRC_NONE, 0)
-  WOS_K(3, DOM_BOX, SRC_CONST, 0)
-  WOS_K(3, DOM_BOX, SRC_SINE, 0)
-  WOS_K(3, DOM_BOX, SRC_GAUSS, 0)
-  // specialised sine orders (coefficients zero-padded up to K)
-  WOS_K(2, DOM_BOX, SRC_SINE, 4)
-  WOS_K(2, DOM_BOX, SRC_SINE, 8)
-  WOS_K(3, DOM_BOX, SRC_SINE, 3)
-  return nullptr;
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows) {
+  return rows ? get_kernel_native_rows(dim, dom, src, sk, one) : get_kernel_native_est(dim, dom, src, sk, one);
 }
-
 }  // namespace wos

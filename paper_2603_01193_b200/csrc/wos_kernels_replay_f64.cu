@@ -4,12 +4,14 @@
 
 namespace wos {
 
-#define WOS_K(DIM, DOM, SRC, SK)                                             \
-  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                    \
-    return reinterpret_cast<const void*>(                                    \
-        &wos_walk_kernel<Spec<MODE_REPLAY_F64, DIM, DOM, SRC, SK>, 1>);
+#define WOS_K(DIM, DOM, SRC, SK)                                                         \
+  if (dim == DIM && dom == DOM && src == SRC && sk == SK)                                \
+    return rows ? reinterpret_cast<const void*>(                                         \
+                      &wos_walk_kernel<Spec<MODE_REPLAY_F64, DIM, DOM, SRC, SK, false, SINK_ROWS>, 1>) \
+                : reinterpret_cast<const void*>(                                         \
+                      &wos_walk_kernel<Spec<MODE_REPLAY_F64, DIM, DOM, SRC, SK, false, SINK_ESTIMATE>, 1>);
 
-const void* get_kernel_replay_f64(int dim, int dom, int src, int sk) {
+const void* get_kernel_replay_f64(int dim, int dom, int src, int sk, bool rows) {
   // 2D
   WOS_K(2, DOM_BALL, SRC_NONE, 0)
   WOS_K(2, DOM_BALL, SRC_CONST, 0)

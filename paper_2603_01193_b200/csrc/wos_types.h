@@ -99,6 +99,8 @@ struct KArgs {
   double* out_m2;
   unsigned long long* total_steps;
   unsigned int* work_counter;
+  unsigned int* watchdog;      // set to 1 if a warp hit the iteration limit
+  uint32_t iter_limit;         // max(2^27, 4 * max_steps) loop iterations per warp
   // ---- single-instance NATIVE launches: the instance row and the Philox round
   // keys live in the kernel-parameter constant bank (FFMA / LOP3 c[] operands) ----
   uint32_t rk0[10];

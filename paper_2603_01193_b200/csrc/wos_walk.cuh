@@ -107,9 +107,9 @@ __device__ __forceinline__ void native_uniforms7(uint4 W, float f[7]) {
   f[6] = f12_m12((W.z << 14) | ((W.w << 5) & 0x3800u));
 }
 
-template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false>
+template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false, int SINK_ = SINK_ESTIMATE>
 struct Spec {
-  static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_;
+  static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_, SINK = SINK_;
   static constexpr bool NATIVE = (MODE_ == MODE_NATIVE_F32);
   static constexpr bool ONE = ONE_;
   using Real = typename std::conditional<MODE_ == MODE_REPLAY_F64, double, float>::type;
@@ -691,7 +691,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   if (lane < kSlots) cnt[lane] = 0u;
   __syncthreads();
 
-  const bool est = a.sink == SINK_ESTIMATE;
+  constexpr bool est = S::SINK == SINK_ESTIMATE;
   const bool anti = a.antithetic != 0;
   const uint32_t IU = a.IU, L = a.L, U = a.U;
   const bool chunked = a.n_chunks > 1;  // L > kChunkMax (then U == 1, IU == L)
@@ -712,11 +712,18 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   unsigned idle = WOS_FULL;    // warp-uniform: lanes without a walk
   unsigned long long lane_steps = 0ull;
 
+  uint32_t refills = 0;
   while (true) {
     bool ready = false;  // this lane completed a retire block
     // ================= refill idle lanes =================
     const int n_idle = __popc(idle);
     if (n_idle >= a.refill_min || n_idle == 32) {
+      // watchdog: bail out and flag instead of spinning forever if the stream
+      // bookkeeping ever stalled (a stall leaves every lane idle, so it lands here)
+      if (++refills > a.iter_limit) {
+        if (lane == 0) atomicExch(a.watchdog, 1u);
+        break;
+      }
       const uint32_t live_units = n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr));
       bool grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && live_units < (uint32_t)kUQ;
       while (grab) {
@@ -744,7 +751,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const uint32_t k = fast_div(seq, a.iu_mul, a.iu_shr);
         const uint32_t r = seq - k * IU;
         const uint32_t unit = unitq[k % kUQ];
-        if (est) {
+        if constexpr (est) {
           const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
           const uint32_t j = r - pl * L;
           const uint64_t p = (uint64_t)unit * U + pl;
@@ -787,7 +794,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
         const Real v = W::finish_value(l, a);
         lane_steps += (unsigned long long)l.step;
-        if (est) {
+        if constexpr (est) {
           ring[l.seq % kRing] = v;
           ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == need;
         } else {
@@ -805,7 +812,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     idle = __ballot_sync(WOS_FULL, !active);
 
     // ================= retire completed blocks, in stream order =================
-    if (est && __any_sync(WOS_FULL, ready)) {
+    if (est && __any_sync(WOS_FULL, ready)) {  // est is constexpr
       __syncwarp();
       while (true) {
         const uint32_t size = chunked ? min((uint32_t)kChunkMax, L - (r_chunk << kChunkShift)) : IU;
