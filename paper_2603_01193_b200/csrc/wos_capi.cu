@@ -237,6 +237,33 @@ static int sine_native_order(int dim, int K, int* sk) {
 
 static size_t pad16(size_t b) { return (b + 15) & ~(size_t)15; }
 
+// Monomial form of a sine series for the NATIVE K <= 4 kernels (wos_walk.cuh sine_eval):
+// sin(k pi y) = s U_{k-1}(c), U Chebyshev polynomials of the second kind, so
+// sum a_{i..} prod_d sin((i_d + 1) pi y_d) = prod_d s_d * sum b_{p..} prod_d c_d^{p_d}
+// with b = a contracted with T[i][p] (monomial coefficients of U_i) along every axis.
+static void sine_monomial(const double* a, int K, int dim, double* b) {
+  double T[4][4] = {{1, 0, 0, 0}, {0, 2, 0, 0}, {-1, 0, 4, 0}, {0, -4, 0, 8}};
+  if (dim == 2) {
+    for (int p = 0; p < K; ++p)
+      for (int q = 0; q < K; ++q) {
+        double v = 0.0;
+        for (int i = 0; i < K; ++i)
+          for (int j = 0; j < K; ++j) v += a[i * K + j] * T[i][p] * T[j][q];
+        b[p * K + q] = v;
+      }
+  } else {
+    for (int p = 0; p < K; ++p)
+      for (int q = 0; q < K; ++q)
+        for (int r = 0; r < K; ++r) {
+          double v = 0.0;
+          for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j)
+              for (int k = 0; k < K; ++k) v += a[(i * K + j) * K + k] * T[i][p] * T[j][q] * T[k][r];
+          b[(p * K + q) * K + r] = v;
+        }
+  }
+}
+
 extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs, int32_t n,
                                       wos_problem_set** out) {
   if (!ctx || !probs || !out) return fail(WOS_ERR_INVALID, "null argument");
@@ -348,19 +375,27 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       case WOS_SRC_SINE: {
         const int Ki = (int)p.src[0];
         const double* a = p.src + 1;
+        std::vector<double> an((size_t)(dim == 2 ? Kn * Kn : Kn * Kn * Kn), 0.0);
         if (dim == 2) {
           for (int k = 0; k < Ki; ++k)
             for (int l = 0; l < Ki; ++l) {
               sd[k * K + l] = a[k * Ki + l];   // replay: order K
-              sn[k * Kn + l] = (float)a[k * Ki + l];  // native: order Kn
+              an[k * Kn + l] = a[k * Ki + l];  // native: order Kn (zero-padded)
             }
         } else {
           for (int k = 0; k < Ki; ++k)
             for (int l = 0; l < Ki; ++l)
               for (int m = 0; m < Ki; ++m) {
                 sd[(k * K + l) * K + m] = a[(k * Ki + l) * Ki + m];
-                sn[(k * Kn + l) * Kn + m] = (float)a[(k * Ki + l) * Ki + m];
+                an[(k * Kn + l) * Kn + m] = a[(k * Ki + l) * Ki + m];
               }
+        }
+        if (sk == 3 || sk == 4) {  // monomial-Horner kernels
+          std::vector<double> bm(an.size());
+          sine_monomial(an.data(), Kn, dim, bm.data());
+          for (size_t k = 0; k < bm.size(); ++k) sn[k] = (float)bm[k];
+        } else {
+          for (size_t k = 0; k < an.size(); ++k) sn[k] = (float)an[k];
         }
         break;
       }

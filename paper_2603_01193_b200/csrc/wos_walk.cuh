@@ -299,38 +299,75 @@ struct Walker {
     }
   }
 
+  // NATIVE, K <= 4: sin(k pi y) = s U_{k-1}(c) with s = sin(pi y), c = cos(pi y), so the
+  // series is s_x s_y (s_z) Q(c_x, c_y (, c_z)) with Q a polynomial whose monomial
+  // coefficients the host precomputes (wos_capi.cu sine_monomial); nested Horner.
+  static constexpr bool kMonomial = S::NATIVE && (S::SK == 3 || S::SK == 4);
+
   template <int K>
   __device__ static __forceinline__ Real sine_eval(const Real* __restrict__ a, const Real* y) {
-    Real sx[K], sy[K];
-    sine_row<K>(y[0], sx);
-    sine_row<K>(y[1], sy);
-    if constexpr (DIM == 2) {
-      Real f = Real(0);
+    if constexpr (kMonomial) {
+      float s[DIM], c[DIM];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        Real t = Real(0);
+      for (int i = 0; i < DIM; ++i) __sincosf(kPiF * y[i], &s[i], &c[i]);
+      if constexpr (DIM == 2) {
+        float q = 0.f;
 #pragma unroll
-        for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sy[l];
-        f = f + sx[k] * t;
+        for (int p = K - 1; p >= 0; --p) {
+          float h = a[p * K + (K - 1)];
+#pragma unroll
+          for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[1], a[p * K + r]);
+          q = (p == K - 1) ? h : fmaf(q, c[0], h);
+        }
+        return (s[0] * s[1]) * q;
+      } else {
+        float q = 0.f;
+#pragma unroll
+        for (int p = K - 1; p >= 0; --p) {
+          float m = 0.f;
+#pragma unroll
+          for (int qd = K - 1; qd >= 0; --qd) {
+            float h = a[(p * K + qd) * K + (K - 1)];
+#pragma unroll
+            for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[2], a[(p * K + qd) * K + r]);
+            m = (qd == K - 1) ? h : fmaf(m, c[1], h);
+          }
+          q = (p == K - 1) ? m : fmaf(q, c[0], m);
+        }
+        return (s[0] * s[1] * s[2]) * q;
       }
-      return f;
     } else {
-      Real sz[K];
-      sine_row<K>(y[2], sz);
-      Real f = Real(0);
+      Real sx[K], sy[K];
+      sine_row<K>(y[0], sx);
+      sine_row<K>(y[1], sy);
+      if constexpr (DIM == 2) {
+        Real f = Real(0);
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        Real u = Real(0);
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
+        for (int k = 0; k < K; ++k) {
           Real t = Real(0);
 #pragma unroll
-          for (int k = 0; k < K; ++k) t = t + a[(i * K + j) * K + k] * sz[k];
-          u = u + sy[j] * t;
+          for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sy[l];
+          f = f + sx[k] * t;
         }
-        f = f + sx[i] * u;
+        return f;
+      } else {
+        Real sz[K];
+        sine_row<K>(y[2], sz);
+        Real f = Real(0);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          Real u = Real(0);
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            Real t = Real(0);
+#pragma unroll
+            for (int k = 0; k < K; ++k) t = t + a[(i * K + j) * K + k] * sz[k];
+            u = u + sy[j] * t;
+          }
+          f = f + sx[i] * u;
+        }
+        return f;
       }
-      return f;
     }
   }
 
