@@ -648,6 +648,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.bnd_M = s->bnd_M;
   a.refill_min = c->refill_min;
   a.eps = cfg->eps;
+  a.eps_f = (float)cfg->eps;
   a.max_steps = (int32_t)std::min<int64_t>(cfg->max_steps, 0x7fffffff);
   a.antithetic = cfg->antithetic ? 1 : 0;
   a.seed = cfg->rng_seed;

@@ -69,6 +69,7 @@ struct KArgs {
   int32_t refill_min;   // refill idle lanes once this many are idle
   // ---- walk config ----
   double eps;
+  float eps_f;          // eps rounded to fp32 (NATIVE / REPLAY_F32 compare in fp32)
   int32_t max_steps;
   int32_t antithetic;
   uint64_t seed;        // REPLAY Philox4x64 key word 0

@@ -623,8 +623,9 @@ struct Walker {
   }
 
   // ---------------- walk start ----------------
+  template <class X>
   __device__ static __forceinline__ void start(Lane& l, const Real* table, const InstHdr* hdr,
-                                               const KArgs& a, const double* x0, int inst,
+                                               const KArgs& a, const X* x0, int inst,
                                                uint64_t pid, uint64_t tid, double sgn) {
 #pragma unroll
     for (int i = 0; i < DIM; ++i) l.x[i] = (Real)x0[i];
@@ -732,7 +733,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   const bool anti = a.antithetic != 0;
   const uint32_t IU = a.IU, L = a.L, U = a.U;
   const bool chunked = a.n_chunks > 1;  // L > kChunkMax (then U == 1, IU == L)
-  const Real eps = (Real)a.eps;
+  const Real eps = sizeof(Real) == 8 ? (Real)a.eps : (Real)a.eps_f;
 
   // warp-uniform stream state
   uint32_t s_issue = 0, s_avail = 0, n_grabbed = 0;
@@ -749,12 +750,72 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   unsigned idle = WOS_FULL;    // warp-uniform: lanes without a walk
   unsigned long long lane_steps = 0ull;
 
+  // fast refill path (ESTIMATE, one point per unit): warp-uniform cache of the point
+  const bool fast = est && U == 1;
+  uint32_t cu_k = 0xffffffffu;  // local index of the cached unit (none yet)
+  uint32_t cu_end = 0;          // stream position where the cached unit ends
+  Real cu_x[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) cu_x[i] = Real(0);
+  uint64_t cu_pid = 0;
+  int cu_inst = 0;
+
   uint32_t refills = 0;
   while (true) {
     bool ready = false;  // this lane completed a retire block
-    // ================= refill idle lanes =================
     const int n_idle = __popc(idle);
-    if (n_idle >= a.refill_min || n_idle == 32) {
+    if (fast && (n_idle >= a.refill_min || n_idle == 32)) {
+      // ============ refill, one point per unit (L >= 128): cached point ============
+      if (++refills > a.iter_limit) {
+        if (lane == 0) atomicExch(a.watchdog, 1u);
+        break;
+      }
+      if (s_issue == cu_end) {  // current point fully issued: move to the next unit
+        if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
+          uint32_t u = 0;
+          if (lane == 0) u = atomicAdd(a.work_counter, 1u);
+          u = __shfl_sync(WOS_FULL, u, 0);
+          if (u >= a.n_units) {
+            exhausted = true;
+          } else {
+            if (lane == 0) unitq[n_grabbed % kUQ] = u;
+            ++n_grabbed;
+            s_avail += IU;
+          }
+        }
+        if (n_grabbed != cu_k + 1u) {  // the next unit is grabbed: cache its point
+          cu_k += 1u;
+          cu_end += L;
+          const uint32_t p = unitq[cu_k % kUQ];  // U == 1: unit id == point index
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
+          cu_pid = (uint64_t)a.point_ids[p];
+          cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+        }
+      }
+      const uint32_t n = min(min((uint32_t)n_idle, cu_end - s_issue), r_seq + (uint32_t)kRing - s_issue);
+      if (n == 0 && n_idle == 32 && exhausted && s_issue == s_avail && r_seq == s_issue) break;
+      const uint32_t rank = __popc(idle & lanemask_lt());
+      if (!active && rank < n) {
+        const uint32_t seq = s_issue + rank;
+        const uint32_t j = seq - (cu_end - L);
+        const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+        const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+        W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
+        if (chunked) {
+          const uint32_t c = j >> kChunkShift;
+          blk = cu_k * a.n_chunks + c;
+          need = min((uint32_t)kChunkMax, L - (c << kChunkShift));
+        } else {
+          blk = cu_k;
+          need = IU;
+        }
+        l.seq = seq;
+        active = true;
+      }
+      s_issue += n;
+    } else if (!fast && (n_idle >= a.refill_min || n_idle == 32)) {
+      // ================= refill idle lanes (general) =================
       // watchdog: bail out and flag instead of spinning forever if the stream
       // bookkeeping ever stalled (a stall leaves every lane idle, so it lands here)
       if (++refills > a.iter_limit) {
