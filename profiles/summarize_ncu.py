@@ -1,0 +1,55 @@
+"""Summarise an ncu --set full report (first kernel) into a short text file.
+
+    python profiles/summarize_ncu.py gpurun_out/prof_r1.ncu-rep > profiles/r1_cfg4_ncu_full.txt
+"""
+
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("smsp__inst_issued.sum", "issued instructions"),
+    ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "avg active threads / warp inst"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers / thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe % of peak"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe % of peak"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % of peak"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe % of peak"),
+    ("dram__bytes_read.sum", "DRAM bytes read"),
+    ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+]
+
+
+def main(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+    print(f"kernel: {d.get('Kernel Name', ('?', ''))[0]}")
+    for k, label in KEYS:
+        if k in d:
+            v, u = d[k]
+            print(f"{label:38s} {v} {u}".rstrip())
+    stalls = []
+    for h, (v, u) in d.items():
+        if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio") \
+                and "not_issued" not in h:
+            try:
+                stalls.append((float(v), h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    print("warp stall reasons (warps per issue):")
+    for v, name in sorted(stalls, reverse=True)[:8]:
+        print(f"  {name:28s} {v:.3f}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
