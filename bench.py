@@ -42,6 +42,15 @@ WORK = {
 }
 
 
+def _ncu_traffic(workload):
+    """DRAM bytes (read + write) per launch of the walk kernel from the committed ncu capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[workload]
+        return d["dram_bytes_read"] + d["dram_bytes_write"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -372,7 +381,7 @@ def main():
                 "peak": sfu_peak if bound == "sfu" else fp32_peak,
                 "unit": "SFU op/s" if bound == "sfu" else "FP32 flop/s",
                 "frac": fr_sfu if bound == "sfu" else fr_fp32,
-                "traffic": None,
+                "traffic": _ncu_traffic(w.name),
                 "sfu": {"achieved": sfu_ach, "peak_measured": sfu_peak, "frac": fr_sfu,
                         "per_step": S_step, "per_walk": S_walk},
                 "fp32": {"achieved": fp32_ach, "peak_measured": fp32_peak, "frac": fr_fp32,
