@@ -95,6 +95,13 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (prop.major < 10)
     return fail(WOS_ERR_UNSUPPORTED, "device %d is sm_%d%d; libwos_b200 is built for sm_100a",
                 device, prop.major, prop.minor);
+  // stream-ordered scratch (chunk partials) comes from the default pool: keep freed
+  // memory cached so a per-call cudaMallocAsync never re-maps pages on the hot path
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   wos_context* c = new wos_context();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
@@ -677,6 +684,28 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   return WOS_OK;
 }
 
+// Chan-merge each point's chunk moments in chunk order (L > kChunk)
+__global__ void wos_merge_chunks_kernel(uint32_t n_points, uint32_t L, uint32_t n_chunks, int anti,
+                                        const double* __restrict__ partials, double* __restrict__ out_mean,
+                                        double* __restrict__ out_m2) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n_points; p += gridDim.x * blockDim.x) {
+    double n1 = 0.0, mean = 0.0, m2 = 0.0;
+    for (uint32_t c = 0; c < n_chunks; ++c) {
+      const uint32_t valid = min((uint32_t)kChunk, L - c * kChunk);
+      const double n2 = (double)(anti ? valid / 2 : valid);
+      const double mc = partials[2 * ((size_t)p * n_chunks + c)];
+      const double qc = partials[2 * ((size_t)p * n_chunks + c) + 1];
+      const double nn = n1 + n2;
+      const double delta = mc - mean;
+      mean = mean + delta * (n2 / nn);
+      m2 = m2 + qc + delta * delta * (n1 * n2 / nn);
+      n1 = nn;
+    }
+    out_mean[p] = mean;
+    out_m2[p] = m2;
+  }
+}
+
 static const int64_t kMaxItemsPerLaunch = (1ll << 31) - 4 * kRing;
 
 extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
@@ -700,9 +729,10 @@ extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos
     a.U = kUnitTarget;
     a.IU = kUnitTarget;
     a.n_units = (uint32_t)((m + kUnitTarget - 1) / kUnitTarget);
-    a.n_chunks = 1;
+    a.n_chunks = 0;
     fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
     fast_div_init(1, &a.l_mul, &a.l_shr);
+    fast_div_init(1, &a.nc_mul, &a.nc_shr);
     a.points = points + off * s->dim;
     a.row_pid = pid + off;
     a.row_tid = tid + off;
@@ -733,7 +763,16 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
   cudaStream_t st = (cudaStream_t)stream;
   int r = launch_interior(c, s, P, points, inst_index, st);
   if (r) return r;
-  const int64_t pts_per_launch = kMaxItemsPerLaunch / L;
+  // L > kChunk: units are kChunk-walk chunks of one point, merged by wos_merge_chunks_kernel
+  const bool split = L > kChunk;
+  const int64_t n_chunks = split ? (L + kChunk - 1) / kChunk : 0;
+  const int64_t items_per_point = split ? n_chunks * kChunk : L;
+  const int64_t pts_per_launch = std::max<int64_t>(1, kMaxItemsPerLaunch / items_per_point);
+  double* partials = nullptr;
+  if (split) {
+    const int64_t m_max = std::min<int64_t>(pts_per_launch, P);
+    CUDA_TRY(cudaMallocAsync((void**)&partials, (size_t)m_max * n_chunks * 2 * sizeof(double), st));
+  }
   for (int64_t off = 0; off < P; off += pts_per_launch) {
     const int64_t m = std::min<int64_t>(pts_per_launch, P - off);
     KArgs a;
@@ -741,12 +780,21 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
     a.sink = SINK_ESTIMATE;
     a.n_points = (uint32_t)m;
     a.L = (uint32_t)L;
-    a.U = (uint32_t)std::max<int64_t>(1, (kUnitTarget + L - 1) / L);
-    a.IU = a.U * a.L;
-    a.n_units = (uint32_t)((m + a.U - 1) / a.U);
-    a.n_chunks = (uint32_t)((L + kChunkMax - 1) / kChunkMax);
+    if (split) {
+      a.U = 1;
+      a.IU = kChunk;
+      a.n_chunks = (uint32_t)n_chunks;
+      a.n_units = (uint32_t)(m * n_chunks);
+      a.partials = partials;
+    } else {
+      a.U = (uint32_t)std::max<int64_t>(1, (kUnitTarget + L - 1) / L);
+      a.IU = a.U * a.L;
+      a.n_units = (uint32_t)((m + a.U - 1) / a.U);
+      a.n_chunks = 0;
+    }
     fast_div_init(a.IU, &a.iu_mul, &a.iu_shr);
     fast_div_init(a.L, &a.l_mul, &a.l_shr);
+    fast_div_init(std::max<uint32_t>(1u, a.n_chunks), &a.nc_mul, &a.nc_shr);
     a.points = points + off * s->dim;
     a.point_ids = point_ids + off;
     a.inst_index = inst_index ? inst_index + off : nullptr;
@@ -755,8 +803,19 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
     a.out_m2 = out_m2 + off;
     a.total_steps = reinterpret_cast<unsigned long long*>(out_total_steps);
     r = launch_walk(c, s, cfg, a, st);
-    if (r) return r;
+    if (r) {
+      if (partials) cudaFreeAsync(partials, st);
+      return r;
+    }
+    if (split) {
+      const int blocks = (int)std::min<int64_t>((m + 255) / 256, (int64_t)c->num_sms * 8);
+      wos_merge_chunks_kernel<<<blocks, 256, 0, st>>>((uint32_t)m, (uint32_t)L, (uint32_t)n_chunks,
+                                                      cfg->antithetic ? 1 : 0, partials,
+                                                      out_mean + off, out_m2 + off);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
+  if (partials) CUDA_TRY(cudaFreeAsync(partials, st));
   return WOS_OK;
 }
 

@@ -22,9 +22,8 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
-constexpr int kChunkMax = 512;    // L > kChunkMax: a point retires in chunks of kChunkMax walks
-constexpr int kChunkShift = 9;    // log2(kChunkMax)
-constexpr int kUnitTarget = 128;  // minimum walks per grabbed work unit
+constexpr int kChunk = 128;       // L > kChunk: work units are kChunk-walk chunks of one point
+constexpr int kUnitTarget = 128;  // walks per grabbed work unit (at least)
 constexpr int kCP = 256;          // floats of single-instance parameters held in the kernel params
 constexpr int kDomOff = 0;        // table row: [0, 8) domain params
 constexpr int kSrcOff = 16;       //            [16, 16 + ns) source params, then boundary params
@@ -82,7 +81,9 @@ struct KArgs {
   uint32_t U;           // points per work unit
   uint32_t IU;          // items (walks) per work unit = U * L
   uint32_t n_units;
-  uint32_t n_chunks;    // L > kChunkMax: chunks per point (ceil(L / kChunkMax)); else 1
+  uint32_t n_chunks;    // L > kChunk: chunks per point (ceil(L / kChunk)); else 0
+  uint32_t nc_mul, nc_shr;  // magic numbers for n / n_chunks
+  double* partials;     // L > kChunk: per-chunk (mean, m2), [P * n_chunks][2]
   uint32_t iu_mul, iu_shr;  // magic numbers: n / IU = (umulhi(n, mul) + n) >> shr, n < 2^31
   uint32_t l_mul, l_shr;    // same for n / L
   const double* points;        // [n, dim]

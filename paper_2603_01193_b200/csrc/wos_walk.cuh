@@ -12,11 +12,13 @@
 //     they are refilled with the next items of the warp's stream (lane refill),
 //     so lanes do not idle while work remains;
 //   * ESTIMATE sink: walk values go to a per-warp shared-memory ring indexed by
-//     the item's stream position; a chunk of one point's walks (<= 512) is
-//     reduced as soon as all of them are done, in fixed index order with fp64
-//     warp-shuffle trees (two-pass mean / m2, PointEstimate.from_values,
-//     estimator.py:106-110). The result therefore does not depend on which lane
-//     ran which walk, on the launch shape, or on the number of GPUs;
+//     the item's stream position; a unit (whole points for L <= 128, else a
+//     128-walk chunk of one point) is reduced as soon as all its walks are done,
+//     in fixed index order with fp64 warp-shuffle trees (two-pass mean / m2,
+//     PointEstimate.from_values, estimator.py:106-110); chunks of long ensembles
+//     are Chan-merged in chunk order by a second small kernel. The result does not
+//     depend on which lane ran which walk, on the launch shape, or on the number
+//     of GPUs;
 //   * ROWS sink: per-walk (value, steps, hit) written straight to global memory
 //     (walker.walk_poisson_values, walker.py:181-229).
 //
@@ -446,20 +448,21 @@ struct Walker {
       case BND_FOURIER: {
         if constexpr (DIM == 2) {
           const int M = a.bnd_M;
-          const Real t = (Real)atan2((double)q[1], (double)q[0]);
           Real g = B[1];
           if constexpr (S::NATIVE) {
-            // rotation recurrence from (cos t, sin t)
-            float c1, s1;
-            sincosf(t, &s1, &c1);
+            // (cos t, sin t) = q / |q| (t = polar angle), then the rotation recurrence
+            const float r2 = fmaf(q[0], q[0], q[1] * q[1]);
+            const float inv = r2 > 0.0f ? rsqrtf(r2) : 0.0f;
+            const float c1 = r2 > 0.0f ? q[0] * inv : 1.0f, s1 = q[1] * inv;
             float cm = c1, sm = s1;
             for (int m = 1; m <= M; ++m) {
               g = fmaf(B[1 + m], cm, fmaf(B[1 + M + m], sm, g));
-              const float cn = cm * c1 - sm * s1;
-              sm = sm * c1 + cm * s1;
+              const float cn = fmaf(cm, c1, -sm * s1);
+              sm = fmaf(sm, c1, cm * s1);
               cm = cn;
             }
           } else {
+            const Real t = (Real)atan2((double)q[1], (double)q[0]);
             for (int m = 1; m <= M; ++m) {
               Real sm, cm;
               psincos((Real)m * t, &sm, &cm);
@@ -675,11 +678,17 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ------------------------------------------------------------------------
 // the persistent kernel
 // ------------------------------------------------------------------------
-// Retire blocks (ESTIMATE sink). Items of a warp's stream are grouped into
-// blocks that are reduced as a whole: for L <= kChunkMax a block is one work
-// unit (U whole points), for larger L a chunk of <= kChunkMax walks of one
-// point. Each live block has a completion counter; the lane that completes a
-// block raises `ready`, and only then does the warp run the (in-order) retire loop.
+// Work units (also the ESTIMATE sink's retire blocks), fixed by L alone so that the
+// reduction order never depends on the launch or on the number of GPUs:
+//   L <= kChunk: U = ceil(kChunk / L) whole points (IU = U L walks); each point's L
+//                values are reduced in the warp (two-pass, estimator.py:106-110) and
+//                written to out_mean / out_m2;
+//   L >  kChunk: one chunk of kChunk walks of one point (IU = kChunk; walks past L are
+//                null items); the chunk's (mean, m2) goes to `partials` and
+//                wos_merge_chunks Chan-merges each point's chunks in chunk order
+//                (estimator.chan_merge, estimator.py:41-53).
+// Each live unit has a shared-memory completion counter; the lane completing a
+// unit raises `ready`, and only then does the warp run its in-order retire loop.
 template <class Real>
 __device__ __forceinline__ double sample_at(const Real* ring, uint32_t base, uint32_t i, bool anti) {
   if (anti)
@@ -710,6 +719,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   using W = Walker<S>;
   using Real = typename S::Real;
   constexpr int DIM = S::DIM;
+  constexpr bool est = S::SINK == SINK_ESTIMATE;
   extern __shared__ __align__(16) unsigned char smem[];
 
   // ---- stage the instance table into shared memory (multi-instance launches) ----
@@ -729,48 +739,100 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   if (lane < kSlots) cnt[lane] = 0u;
   __syncthreads();
 
-  constexpr bool est = S::SINK == SINK_ESTIMATE;
   const bool anti = a.antithetic != 0;
   const uint32_t IU = a.IU, L = a.L, U = a.U;
-  const bool chunked = a.n_chunks > 1;  // L > kChunkMax (then U == 1, IU == L)
+  const bool split = a.n_chunks > 0;  // L > kChunk: units are chunks of one point
   const Real eps = sizeof(Real) == 8 ? (Real)a.eps : (Real)a.eps_f;
 
   // warp-uniform stream state
   uint32_t s_issue = 0, s_avail = 0, n_grabbed = 0;
-  uint32_t r_seq = 0;    // first item of the next block to retire
-  uint32_t r_blk = 0;    // its block number in this warp's stream
-  uint32_t r_unit = 0;   // retired units
-  uint32_t r_chunk = 0;  // chunked: next chunk of the current point
+  uint32_t r_seq = 0;    // first item of the next unit to retire
+  uint32_t r_unit = 0;   // its index in this warp's stream
   bool exhausted = false;
-  double run_n = 0.0, run_mean = 0.0, run_m2 = 0.0;  // Chan accumulator (chunked)
 
-  typename W::Lane l;
-  bool active = false;
-  uint32_t blk = 0, need = 0;  // this lane's retire block and its size
-  unsigned idle = WOS_FULL;    // warp-uniform: lanes without a walk
-  unsigned long long lane_steps = 0ull;
-
-  // fast refill path (ESTIMATE, one point per unit): warp-uniform cache of the point
-  const bool fast = est && U == 1;
-  uint32_t cu_k = 0xffffffffu;  // local index of the cached unit (none yet)
+  // fast refill path (ESTIMATE, one point per unit): warp-uniform cache of the unit's point
+  const bool fast = est && (split || U == 1);
+  uint32_t cu_k = 0xffffffffu;  // stream index of the cached unit (none yet)
   uint32_t cu_end = 0;          // stream position where the cached unit ends
+  uint32_t cu_j0 = 0, cu_jend = 0;  // walk range [j0, jend) of the cached unit
   Real cu_x[DIM];
 #pragma unroll
   for (int i = 0; i < DIM; ++i) cu_x[i] = Real(0);
   uint64_t cu_pid = 0;
   int cu_inst = 0;
 
+  typename W::Lane l;
+  bool active = false;
+  uint32_t blk = 0;          // this lane's unit (stream index)
+  unsigned idle = WOS_FULL;  // warp-uniform: lanes without a walk
+  unsigned long long lane_steps = 0ull;
   uint32_t refills = 0;
+
+  // in-order retirement of completed units (ESTIMATE sink)
+  auto retire = [&]() {
+    while (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) {
+      const uint32_t unit = unitq[r_unit % kUQ];
+      if (split) {
+        const uint32_t p = fast_div(unit, a.nc_mul, a.nc_shr);
+        const uint32_t c = unit - p * a.n_chunks;
+        const uint32_t valid = min((uint32_t)kChunk, L - c * kChunk);
+        double mu, q;
+        warp_moments(ring, r_seq, anti ? valid / 2 : valid, anti, lane, &mu, &q);
+        if (lane == 0) {
+          a.partials[2 * (size_t)unit] = mu;
+          a.partials[2 * (size_t)unit + 1] = q;
+        }
+      } else if (L <= 32) {
+        // small L: lane per point, sequential fixed-order two-pass, coalesced stores
+        const uint32_t ns = anti ? L / 2 : L;
+        for (uint32_t pl = lane; pl < U; pl += 32) {
+          const uint64_t p = (uint64_t)unit * U + pl;
+          if (p < a.n_points) {
+            const uint32_t base = r_seq + pl * L;
+            double sum = 0.0;
+            for (uint32_t i = 0; i < ns; ++i) sum += sample_at(ring, base, i, anti);
+            const double mu = sum / (double)ns;
+            double q = 0.0;
+            for (uint32_t i = 0; i < ns; ++i) {
+              const double v = sample_at(ring, base, i, anti);
+              q += (v - mu) * (v - mu);
+            }
+            a.out_mean[p] = mu;
+            a.out_m2[p] = q;
+          }
+        }
+      } else {
+        for (uint32_t pl = 0; pl < U; ++pl) {
+          const uint64_t p = (uint64_t)unit * U + pl;
+          if (p >= a.n_points) break;
+          double mu, q;
+          warp_moments(ring, r_seq + pl * L, anti ? L / 2 : L, anti, lane, &mu, &q);
+          if (lane == 0) {
+            a.out_mean[p] = mu;
+            a.out_m2[p] = q;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) cnt[r_unit % kSlots] = 0u;
+      __syncwarp();
+      r_seq += IU;
+      ++r_unit;
+    }
+  };
+
   while (true) {
-    bool ready = false;  // this lane completed a retire block
+    bool ready = false;  // this lane completed a unit
     const int n_idle = __popc(idle);
     if (fast && (n_idle >= a.refill_min || n_idle == 32)) {
-      // ============ refill, one point per unit (L >= 128): cached point ============
+      // ============ refill, one point per unit: cached point in registers ============
+      // watchdog: bail out and flag instead of spinning forever if the stream
+      // bookkeeping ever stalled (a stall leaves every lane idle, so it lands here)
       if (++refills > a.iter_limit) {
         if (lane == 0) atomicExch(a.watchdog, 1u);
         break;
       }
-      if (s_issue == cu_end) {  // current point fully issued: move to the next unit
+      if (s_issue == cu_end) {  // current unit fully issued: move to the next one
         if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
           uint32_t u = 0;
           if (lane == 0) u = atomicAdd(a.work_counter, 1u);
@@ -785,8 +847,16 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         }
         if (n_grabbed != cu_k + 1u) {  // the next unit is grabbed: cache its point
           cu_k += 1u;
-          cu_end += L;
-          const uint32_t p = unitq[cu_k % kUQ];  // U == 1: unit id == point index
+          cu_end += IU;
+          const uint32_t unit = unitq[cu_k % kUQ];
+          uint32_t p = unit;
+          cu_j0 = 0;
+          cu_jend = L;
+          if (split) {
+            p = fast_div(unit, a.nc_mul, a.nc_shr);
+            cu_j0 = (unit - p * a.n_chunks) * kChunk;
+            cu_jend = min(L, cu_j0 + kChunk);
+          }
 #pragma unroll
           for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
           cu_pid = (uint64_t)a.point_ids[p];
@@ -798,26 +868,21 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       const uint32_t rank = __popc(idle & lanemask_lt());
       if (!active && rank < n) {
         const uint32_t seq = s_issue + rank;
-        const uint32_t j = seq - (cu_end - L);
-        const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
-        const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
-        W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
-        if (chunked) {
-          const uint32_t c = j >> kChunkShift;
-          blk = cu_k * a.n_chunks + c;
-          need = min((uint32_t)kChunkMax, L - (c << kChunkShift));
-        } else {
-          blk = cu_k;
-          need = IU;
+        const uint32_t j = cu_j0 + (seq - (cu_end - IU));
+        blk = cu_k;
+        if (j < cu_jend) {
+          const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+          const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+          W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
+          l.seq = seq;
+          active = true;
+        } else {  // null item padding the point's last chunk: complete at once
+          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
         }
-        l.seq = seq;
-        active = true;
       }
       s_issue += n;
     } else if (!fast && (n_idle >= a.refill_min || n_idle == 32)) {
       // ================= refill idle lanes (general) =================
-      // watchdog: bail out and flag instead of spinning forever if the stream
-      // bookkeeping ever stalled (a stall leaves every lane idle, so it lands here)
       if (++refills > a.iter_limit) {
         if (lane == 0) atomicExch(a.watchdog, 1u);
         break;
@@ -835,8 +900,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           ++n_grabbed;
           s_avail += IU;
         }
-        grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && (live_units + 1) < (uint32_t)kUQ &&
-               (n_grabbed - (est ? r_unit : 0u)) < (uint32_t)kUQ;
+        grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle &&
+               (n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr))) < (uint32_t)kUQ;
       }
       __syncwarp();
       uint32_t n = min((uint32_t)n_idle, s_avail - s_issue);
@@ -853,14 +918,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
           const uint32_t j = r - pl * L;
           const uint64_t p = (uint64_t)unit * U + pl;
-          if (chunked) {
-            const uint32_t c = j >> kChunkShift;
-            blk = k * a.n_chunks + c;
-            need = min((uint32_t)kChunkMax, L - (c << kChunkShift));
-          } else {
-            blk = k;
-            need = IU;
-          }
+          blk = k;
           if (p < a.n_points) {
             const int inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
             const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
@@ -870,7 +928,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             l.seq = seq;
             active = true;
           } else {  // null item padding the last unit: complete at once
-            ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == need;
+            ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
           }
         } else {
           const uint64_t row = (uint64_t)unit * IU + r;
@@ -894,7 +952,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         lane_steps += (unsigned long long)l.step;
         if constexpr (est) {
           ring[l.seq % kRing] = v;
-          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == need;
+          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
         } else {
           a.out_values[l.seq] = (double)v;
           a.out_steps[l.seq] = (int64_t)l.step;
@@ -909,75 +967,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
     idle = __ballot_sync(WOS_FULL, !active);
 
-    // ================= retire completed blocks, in stream order =================
-    if (est && __any_sync(WOS_FULL, ready)) {  // est is constexpr
-      __syncwarp();
-      while (true) {
-        const uint32_t size = chunked ? min((uint32_t)kChunkMax, L - (r_chunk << kChunkShift)) : IU;
-        if (r_seq + size > s_issue || cnt[r_blk % kSlots] != size) break;
-        const uint32_t unit = unitq[r_unit % kUQ];
-        if (!chunked) {
-          if (L <= 32) {
-            // small L: lane per point, sequential fixed-order two-pass, coalesced stores
-            const uint32_t ns = anti ? L / 2 : L;
-            for (uint32_t pl = lane; pl < U; pl += 32) {
-              const uint64_t p = (uint64_t)unit * U + pl;
-              if (p < a.n_points) {
-                const uint32_t base = r_seq + pl * L;
-                double sum = 0.0;
-                for (uint32_t i = 0; i < ns; ++i) sum += sample_at(ring, base, i, anti);
-                const double mu = sum / (double)ns;
-                double q = 0.0;
-                for (uint32_t i = 0; i < ns; ++i) {
-                  const double v = sample_at(ring, base, i, anti);
-                  q += (v - mu) * (v - mu);
-                }
-                a.out_mean[p] = mu;
-                a.out_m2[p] = q;
-              }
-            }
-          } else {
-            for (uint32_t pl = 0; pl < U; ++pl) {
-              const uint64_t p = (uint64_t)unit * U + pl;
-              if (p >= a.n_points) break;
-              double mu, q;
-              warp_moments(ring, r_seq + pl * L, anti ? L / 2 : L, anti, lane, &mu, &q);
-              if (lane == 0) {
-                a.out_mean[p] = mu;
-                a.out_m2[p] = q;
-              }
-            }
-          }
-          ++r_unit;
-        } else {
-          // one chunk of a long ensemble: moments of the chunk, Chan-merged in order
-          // (estimator.chan_merge, estimator.py:41-53)
-          const uint64_t p = (uint64_t)unit;  // U == 1
-          if (p < a.n_points) {
-            double mu, q;
-            const uint32_t ns = anti ? size / 2 : size;
-            warp_moments(ring, r_seq, ns, anti, lane, &mu, &q);
-            const double n1 = run_n, n2 = (double)ns, nn = n1 + n2;
-            const double delta = mu - run_mean;
-            run_mean = run_mean + delta * (n2 / nn);
-            run_m2 = run_m2 + q + delta * delta * (n1 * n2 / nn);
-            run_n = nn;
-          }
-          if (++r_chunk == a.n_chunks) {
-            if (p < a.n_points && lane == 0) {
-              a.out_mean[p] = run_mean;
-              a.out_m2[p] = run_m2;
-            }
-            run_n = run_mean = run_m2 = 0.0;
-            r_chunk = 0;
-            ++r_unit;
-          }
-        }
+    // ================= retire completed units, in stream order =================
+    if constexpr (est) {
+      if (__any_sync(WOS_FULL, ready)) {
         __syncwarp();
-        if (lane == 0) cnt[r_blk % kSlots] = 0u;
-        __syncwarp();
-        r_seq += size;
-        ++r_blk;
+        retire();
       }
     }
   }
