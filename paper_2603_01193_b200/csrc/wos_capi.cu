@@ -76,7 +76,8 @@ struct wos_problem_set {
   InstHdr* d_hdr = nullptr;
   double* d_segs_d = nullptr;             // [nseg][ax, ay, ex, ey]
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
-  float4* d_segs_n = nullptr;             // NATIVE: [nseg][2] float4
+  float4* d_segs_n = nullptr;             // NATIVE: per polygon n + 1 records {v_k, e_k/|e_k|^2}
+  size_t bytes_segs_n = 0;
   std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
@@ -349,6 +350,7 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       const int nv = (int)p.dom[0];
       const double* V = p.dom + 1;
       hd[i].seg_off = (int)(segd.size() / 4);
+      hd[i].rec_off = (int)segn.size();
       hd[i].n_seg = nv;
       for (int k = 0; k < nv; ++k) {
         const int j = (k + 1 == nv) ? 0 : k + 1;
@@ -359,9 +361,10 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
         segd.push_back(ex);
         segd.push_back(ey);
         const double l2 = ex * ex + ey * ey;
-        segn.push_back(make_float4((float)ax, (float)ay, (float)ex, (float)ey));
-        segn.push_back(make_float4((float)(ex / l2), (float)(ey / l2), 0.f, 0.f));
+        // NATIVE record: vertex k and e_k / |e_k|^2; the next record holds vertex k+1
+        segn.push_back(make_float4((float)ax, (float)ay, (float)(ex / l2), (float)(ey / l2)));
       }
+      segn.push_back(make_float4((float)V[0], (float)V[1], 0.f, 0.f));  // closing vertex
     }
     for (int k = 0; k < 8; ++k) rn[k] = (float)rd[k];
     if (p.dom_kind == WOS_DOM_BOX)  // NATIVE box distance: centre and half extent
@@ -464,6 +467,7 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   if (!segd.empty()) {
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_d, segd.size() * 8);
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_f, segf.size() * 4);
+    s->bytes_segs_n = segn.size() * sizeof(float4);
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_n, segn.size() * sizeof(float4));
     if (e == cudaSuccess) e = cudaMemcpy(s->d_segs_d, segd.data(), segd.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(s->d_segs_f, segf.data(), segf.size() * 4, cudaMemcpyHostToDevice);
@@ -610,6 +614,8 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
   return k;
 }
 
+static const size_t kSegStageMax = 96 * 1024;  // polygon records staged per CTA at most
+
 static size_t smem_bytes(size_t stage, size_t elem) {
   return stage + (size_t)kWarps * (kRing * elem + kSlots * 4 + kUQ * 4);
 }
@@ -635,6 +641,8 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     a.segs = s->d_segs_n;
     a.stage_bytes = (int)s->bytes_f;
     a.sine_K = s->sine_K_native;
+    // polygon records go to shared memory when they fit (else read through L1)
+    if (s->bytes_segs_n > 0 && s->bytes_segs_n <= kSegStageMax) a.seg_stage_bytes = (int)s->bytes_segs_n;
     if (k.one) {
       // instance row and Philox4x32 round keys ride in the kernel parameters
       a.stage_bytes = 0;
@@ -661,7 +669,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.seed = cfg->rng_seed;
   a.nkey0 = (uint32_t)cfg->rng_seed;
   a.nkey1_seed = (uint32_t)(cfg->rng_seed >> 32);
-  const size_t smem = smem_bytes((size_t)a.stage_bytes, k.elem);
+  const size_t smem = smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes, k.elem);
   if (smem > 220 * 1024)
     return fail(WOS_ERR_UNSUPPORTED,
                 "problem table too large for shared memory (%zu bytes); split the batch",

@@ -35,7 +35,8 @@ struct InstHdr {
   uint32_t nkey1;   // NATIVE key word 1 = (seed >> 32) ^ this (lo32(ikey) ^ hi32(ikey) * 0x9E3779B9)
   int32_t seg_off;  // polygon: first segment
   int32_t n_seg;    // polygon: segment count
-  int32_t pad[3];
+  int32_t rec_off;  // polygon, NATIVE: first record of the n_seg + 1 vertex records
+  int32_t pad[2];
 };
 
 // n / d for n < 2^31 with host-precomputed (mul, shr) (Granlund-Montgomery round-up)
@@ -62,6 +63,7 @@ struct KArgs {
   int32_t stride;       // Real elements per table row
   int32_t bnd_off;      // boundary params offset in a row
   int32_t stage_bytes;  // bytes of the table staged into shared memory (0 = read global)
+  int32_t seg_stage_bytes;  // NATIVE polygon records staged after the table (0 = read global)
   int32_t sine_K;       // sine order (uniform over the set; padded)
   int32_t bnd_kind;
   int32_t bnd_M;        // Fourier / arc-length order (uniform over the set; padded)

@@ -136,7 +136,8 @@ struct Walker {
     uint32_t seq;
     uint64_t pid, tid, ikey;   // REPLAY counters / key
     uint32_t c1, c2, c3, k1;   // NATIVE counters / key
-    int32_t seg_off, n_seg;
+    int32_t seg_off, n_seg, rec_off;
+    int32_t seg_i;  // polygon: nearest segment found by the last distance query
   };
 
   // instance parameters: constant bank (ONE) or the staged shared-memory row
@@ -151,7 +152,7 @@ struct Walker {
 
   // ---------------- domains ----------------
   // distance to the boundary (positive inside)
-  __device__ static __forceinline__ Real dist(const Lane& l, const KArgs& a) {
+  __device__ static __forceinline__ Real dist(Lane& l, const KArgs& a, const float4* srec) {
     if constexpr (S::DOM == DOM_BALL) {
       // geometry.py:196-206 / _kernels.py:329-339
       Real s = Real(0);
@@ -181,45 +182,50 @@ struct Walker {
         return d;
       }
     } else {
-      return poly_dist(l, a, nullptr);
+      return poly_dist(l, a, srec);
     }
   }
 
-  // polygon: min distance over segments; optionally the closest point (first nearest segment)
-  __device__ static __forceinline__ Real poly_dist(const Lane& l, const KArgs& a, Real* q) {
-    if constexpr (S::NATIVE) {
-      const float4* seg = reinterpret_cast<const float4*>(a.segs) + 2 * (size_t)l.seg_off;
-      const float px = l.x[0], py = l.x[1];
-      float best = 3.0e38f, bqx = 0.f, bqy = 0.f;
-      const int n = l.n_seg;
+  // polygon: min distance over segments; records the first nearest segment in l.seg_i
+  // (the closest point is rebuilt from that one segment only at termination)
+  // NATIVE scan over vertex records {v_k, e_k/|e_k|^2} (record k+1 supplies v_{k+1})
+  template <class P>
+  __device__ static __forceinline__ float poly_scan(const P rec, int n, float px, float py, int* bi_out) {
+    float best = 3.0e38f;
+    int bi = 0;
+    float4 R = rec[0];
 #pragma unroll 4
-      for (int i = 0; i < n; ++i) {
-        const float4 A = __ldg(seg + 2 * i);      // ax, ay, ex, ey
-        const float4 B = __ldg(seg + 2 * i + 1);  // ex/|e|^2, ey/|e|^2
-        const float wx = px - A.x, wy = py - A.y;
-        const float t = __saturatef(fmaf(wx, B.x, wy * B.y));
-        const float dx = fmaf(-t, A.z, wx), dy = fmaf(-t, A.w, wy);
-        const float d2 = fmaf(dx, dx, dy * dy);
-        if (q != nullptr) {
-          if (d2 < best) {
-            best = d2;
-            bqx = fmaf(t, A.z, A.x);
-            bqy = fmaf(t, A.w, A.y);
-          }
-        } else {
-          best = fminf(best, d2);
-        }
-      }
-      if (q != nullptr) {
-        q[0] = bqx;
-        q[1] = bqy;
-      }
+    for (int i = 0; i < n; ++i) {
+      const float4 Rn = rec[i + 1];
+      const float ex = Rn.x - R.x, ey = Rn.y - R.y;
+      const float wx = px - R.x, wy = py - R.y;
+      const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
+      const float dx = fmaf(-t, ex, wx), dy = fmaf(-t, ey, wy);
+      const float d2 = fmaf(dx, dx, dy * dy);
+      bi = d2 < best ? i : bi;
+      best = fminf(best, d2);
+      R = Rn;
+    }
+    *bi_out = bi;
+    return best;
+  }
+
+  __device__ static __forceinline__ Real poly_dist(Lane& l, const KArgs& a, const float4* srec) {
+    if constexpr (S::NATIVE) {
+      int bi;
+      float best;
+      if (srec != nullptr)  // staged in shared memory
+        best = poly_scan(srec + l.rec_off, l.n_seg, l.x[0], l.x[1], &bi);
+      else
+        best = poly_scan(reinterpret_cast<const float4*>(a.segs) + l.rec_off, l.n_seg, l.x[0], l.x[1], &bi);
+      l.seg_i = bi;
       return fast_sqrt(best);
     } else {
       // oracle/wos_oracle.c query(): t = clamp(w.e / e.e, 0, 1), c = a + t e
       const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
       const Real px = l.x[0], py = l.x[1];
-      Real best = sizeof(Real) == 8 ? Real(1e300) : Real(3e38), bqx = 0, bqy = 0;
+      Real best = sizeof(Real) == 8 ? Real(1e300) : Real(3e38);
+      int bi = 0;
       const int n = l.n_seg;
       for (int i = 0; i < n; ++i) {
         const Real ax = seg[4 * i], ay = seg[4 * i + 1], ex = seg[4 * i + 2], ey = seg[4 * i + 3];
@@ -231,15 +237,33 @@ struct Walker {
         const Real d2 = dx * dx + dy * dy;
         if (d2 < best) {
           best = d2;
-          bqx = cx;
-          bqy = cy;
+          bi = i;
         }
       }
-      if (q != nullptr) {
-        q[0] = bqx;
-        q[1] = bqy;
-      }
+      l.seg_i = bi;
       return psqrt(best);
+    }
+  }
+
+  // closest point on the segment recorded by the last distance query
+  __device__ static __forceinline__ void poly_project(const Lane& l, const KArgs& a, Real* q) {
+    const int i = l.seg_i;
+    if constexpr (S::NATIVE) {
+      const float4* rec = reinterpret_cast<const float4*>(a.segs) + l.rec_off;
+      const float4 R = __ldg(rec + i), Rn = __ldg(rec + i + 1);
+      const float ex = Rn.x - R.x, ey = Rn.y - R.y;
+      const float wx = l.x[0] - R.x, wy = l.x[1] - R.y;
+      const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
+      q[0] = fmaf(t, ex, R.x);
+      q[1] = fmaf(t, ey, R.y);
+    } else {
+      const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
+      const Real ax = seg[4 * i], ay = seg[4 * i + 1], ex = seg[4 * i + 2], ey = seg[4 * i + 3];
+      const Real wx = l.x[0] - ax, wy = l.x[1] - ay;
+      Real t = (wx * ex + wy * ey) / (ex * ex + ey * ey);
+      t = t < Real(0) ? Real(0) : (t > Real(1) ? Real(1) : t);
+      q[0] = ax + t * ex;
+      q[1] = ay + t * ey;
     }
   }
 
@@ -279,7 +303,7 @@ struct Walker {
 #pragma unroll
       for (int i = 0; i < DIM; ++i) q[i] = (i == axis) ? face : l.x[i];
     } else {
-      poly_dist(l, a, q);
+      poly_project(l, a, q);
     }
   }
 
@@ -651,11 +675,13 @@ struct Walker {
       if constexpr (S::DOM == DOM_POLY) {
         l.seg_off = h.seg_off;
         l.n_seg = h.n_seg;
+        l.rec_off = h.rec_off;
       }
     } else if constexpr (S::DOM == DOM_POLY) {
       const InstHdr h = hdr[0];
       l.seg_off = h.seg_off;
       l.n_seg = h.n_seg;
+      l.rec_off = h.rec_off;
     }
   }
 };
@@ -730,8 +756,18 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     int4* dst = reinterpret_cast<int4*>(smem);
     for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
   }
+  // ---- stage NATIVE polygon records after the table ----
+  const float4* srec = nullptr;
+  if constexpr (S::NATIVE && S::DOM == DOM_POLY) {
+    if (a.seg_stage_bytes > 0) {
+      float4* dst = reinterpret_cast<float4*>(smem + a.stage_bytes);
+      const float4* src = reinterpret_cast<const float4*>(a.segs);
+      for (int i = threadIdx.x; i < a.seg_stage_bytes / 16; i += blockDim.x) dst[i] = src[i];
+      srec = dst;
+    }
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem + a.stage_bytes +
+  unsigned char* wbase = smem + a.stage_bytes + a.seg_stage_bytes +
                          (size_t)warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4);
   Real* ring = reinterpret_cast<Real*>(wbase);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
@@ -945,7 +981,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 
     // ================= one step of every active walk =================
     if (active) {
-      const Real d = W::dist(l, a);
+      const Real d = W::dist(l, a, srec);
       if (d < eps || l.step >= a.max_steps) {
         // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
         const Real v = W::finish_value(l, a);
