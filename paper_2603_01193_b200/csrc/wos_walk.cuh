@@ -713,8 +713,9 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 //                null items); the chunk's (mean, m2) goes to `partials` and
 //                wos_merge_chunks Chan-merges each point's chunks in chunk order
 //                (estimator.chan_merge, estimator.py:41-53).
-// Each live unit has a shared-memory completion counter; the lane completing a
-// unit raises `ready`, and only then does the warp run its in-order retire loop.
+// Each live unit has a shared-memory completion counter bumped by every finishing
+// walk; at each refill the warp retires the completed units at the head of its
+// stream, in order.
 template <class Real>
 __device__ __forceinline__ double sample_at(const Real* ring, uint32_t base, uint32_t i, bool anti) {
   if (anti)
@@ -806,6 +807,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 
   // in-order retirement of completed units (ESTIMATE sink)
   auto retire = [&]() {
+    __syncwarp();
     while (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) {
       const uint32_t unit = unitq[r_unit % kUQ];
       if (split) {
@@ -858,18 +860,88 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   };
 
   while (true) {
-    bool ready = false;  // this lane completed a unit
     const int n_idle = __popc(idle);
-    if (fast && (n_idle >= a.refill_min || n_idle == 32)) {
-      // ============ refill, one point per unit: cached point in registers ============
-      // watchdog: bail out and flag instead of spinning forever if the stream
-      // bookkeeping ever stalled (a stall leaves every lane idle, so it lands here)
-      if (++refills > a.iter_limit) {
-        if (lane == 0) atomicExch(a.watchdog, 1u);
-        break;
+    if (n_idle >= a.refill_min || n_idle == 32) {
+      // retire lazily: the ring holds kRing walks, so completed units only need to be
+      // reduced before new walks are issued (one shared-memory check, no vote)
+      if constexpr (est) {
+        __syncwarp();  // order the lanes' counter updates before the check
+        if (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) retire();
       }
-      if (s_issue == cu_end) {  // current unit fully issued: move to the next one
-        if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
+      if (fast) {
+        // ============ refill, one point per unit: cached point in registers ============
+        uint32_t room = cu_end - s_issue;
+        const uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
+        if (room == 0 || cap == 0) {
+          // watchdog: bail out and flag instead of spinning forever if the stream
+          // bookkeeping ever stalled (a stall can only loop through here)
+          if (++refills > a.iter_limit) {
+            if (lane == 0) atomicExch(a.watchdog, 1u);
+            break;
+          }
+          if (room == 0) {  // current unit fully issued: move to the next one
+            if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
+              uint32_t u = 0;
+              if (lane == 0) u = atomicAdd(a.work_counter, 1u);
+              u = __shfl_sync(WOS_FULL, u, 0);
+              if (u >= a.n_units) {
+                exhausted = true;
+              } else {
+                if (lane == 0) unitq[n_grabbed % kUQ] = u;
+                ++n_grabbed;
+                s_avail += IU;
+              }
+            }
+            if (n_grabbed != cu_k + 1u) {  // the next unit is grabbed: cache its point
+              cu_k += 1u;
+              cu_end += IU;
+              const uint32_t unit = unitq[cu_k % kUQ];
+              uint32_t p = unit;
+              cu_j0 = 0;
+              cu_jend = L;
+              if (split) {
+                p = fast_div(unit, a.nc_mul, a.nc_shr);
+                cu_j0 = (unit - p * a.n_chunks) * kChunk;
+                cu_jend = min(L, cu_j0 + kChunk);
+              }
+#pragma unroll
+              for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
+              cu_pid = (uint64_t)a.point_ids[p];
+              cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+              room = IU;
+            } else if (n_idle == 32 && exhausted && r_seq == s_issue) {
+              break;  // no walk left, none running, all retired
+            }
+          }
+        }
+        const uint32_t n = min(min((uint32_t)n_idle, room), cap);
+        if (!active) {
+          const uint32_t rank = __popc(idle & lanemask_lt());
+          if (rank < n) {
+            const uint32_t seq = s_issue + rank;
+            const uint32_t j = cu_j0 + (seq - (cu_end - IU));
+            blk = cu_k;
+            if (j < cu_jend) {
+              const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+              const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+              W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
+              l.seq = seq;
+              active = true;
+            } else {  // null item padding the point's last chunk: complete at once
+              atomicAdd(&cnt[blk % kSlots], 1u);
+            }
+          }
+        }
+        s_issue += n;
+      } else {
+        // ================= refill idle lanes (general) =================
+        if (++refills > a.iter_limit) {
+          if (lane == 0) atomicExch(a.watchdog, 1u);
+          break;
+        }
+        const uint32_t live_units = n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr));
+        bool grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && live_units < (uint32_t)kUQ;
+        while (grab) {
           uint32_t u = 0;
           if (lane == 0) u = atomicAdd(a.work_counter, 1u);
           u = __shfl_sync(WOS_FULL, u, 0);
@@ -880,103 +952,48 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             ++n_grabbed;
             s_avail += IU;
           }
+          grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle &&
+                 (n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr))) < (uint32_t)kUQ;
         }
-        if (n_grabbed != cu_k + 1u) {  // the next unit is grabbed: cache its point
-          cu_k += 1u;
-          cu_end += IU;
-          const uint32_t unit = unitq[cu_k % kUQ];
-          uint32_t p = unit;
-          cu_j0 = 0;
-          cu_jend = L;
-          if (split) {
-            p = fast_div(unit, a.nc_mul, a.nc_shr);
-            cu_j0 = (unit - p * a.n_chunks) * kChunk;
-            cu_jend = min(L, cu_j0 + kChunk);
-          }
-#pragma unroll
-          for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
-          cu_pid = (uint64_t)a.point_ids[p];
-          cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
-        }
-      }
-      const uint32_t n = min(min((uint32_t)n_idle, cu_end - s_issue), r_seq + (uint32_t)kRing - s_issue);
-      if (n == 0 && n_idle == 32 && exhausted && s_issue == s_avail && r_seq == s_issue) break;
-      const uint32_t rank = __popc(idle & lanemask_lt());
-      if (!active && rank < n) {
-        const uint32_t seq = s_issue + rank;
-        const uint32_t j = cu_j0 + (seq - (cu_end - IU));
-        blk = cu_k;
-        if (j < cu_jend) {
-          const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
-          const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
-          W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
-          l.seq = seq;
-          active = true;
-        } else {  // null item padding the point's last chunk: complete at once
-          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
-        }
-      }
-      s_issue += n;
-    } else if (!fast && (n_idle >= a.refill_min || n_idle == 32)) {
-      // ================= refill idle lanes (general) =================
-      if (++refills > a.iter_limit) {
-        if (lane == 0) atomicExch(a.watchdog, 1u);
-        break;
-      }
-      const uint32_t live_units = n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr));
-      bool grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle && live_units < (uint32_t)kUQ;
-      while (grab) {
-        uint32_t u = 0;
-        if (lane == 0) u = atomicAdd(a.work_counter, 1u);
-        u = __shfl_sync(WOS_FULL, u, 0);
-        if (u >= a.n_units) {
-          exhausted = true;
-        } else {
-          if (lane == 0) unitq[n_grabbed % kUQ] = u;
-          ++n_grabbed;
-          s_avail += IU;
-        }
-        grab = !exhausted && (s_avail - s_issue) < (uint32_t)n_idle &&
-               (n_grabbed - (est ? r_unit : fast_div(s_issue, a.iu_mul, a.iu_shr))) < (uint32_t)kUQ;
-      }
-      __syncwarp();
-      uint32_t n = min((uint32_t)n_idle, s_avail - s_issue);
-      if (est) n = min(n, r_seq + (uint32_t)kRing - s_issue);
-      if (n == 0 && n_idle == 32 && exhausted && s_issue == s_avail && (!est || r_seq == s_issue))
-        break;  // no walk left, none running, all retired
-      const uint32_t rank = __popc(idle & lanemask_lt());
-      if (!active && rank < n) {
-        const uint32_t seq = s_issue + rank;
-        const uint32_t k = fast_div(seq, a.iu_mul, a.iu_shr);
-        const uint32_t r = seq - k * IU;
-        const uint32_t unit = unitq[k % kUQ];
-        if constexpr (est) {
-          const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
-          const uint32_t j = r - pl * L;
-          const uint64_t p = (uint64_t)unit * U + pl;
-          blk = k;
-          if (p < a.n_points) {
-            const int inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
-            const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
-            const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
-            W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
-                     (uint64_t)a.point_ids[p], tid, sg);
-            l.seq = seq;
-            active = true;
-          } else {  // null item padding the last unit: complete at once
-            ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
-          }
-        } else {
-          const uint64_t row = (uint64_t)unit * IU + r;
-          if (row < a.n_points) {
-            W::start(l, table, a.hdr, a, a.points + (size_t)row * DIM, 0, a.row_pid[row],
-                     a.row_tid[row], a.row_sign[row]);
-            l.seq = (uint32_t)row;
-            active = true;
+        __syncwarp();
+        uint32_t n = min((uint32_t)n_idle, s_avail - s_issue);
+        if (est) n = min(n, r_seq + (uint32_t)kRing - s_issue);
+        if (n == 0 && n_idle == 32 && exhausted && s_issue == s_avail && (!est || r_seq == s_issue))
+          break;  // no walk left, none running, all retired
+        const uint32_t rank = __popc(idle & lanemask_lt());
+        if (!active && rank < n) {
+          const uint32_t seq = s_issue + rank;
+          const uint32_t k = fast_div(seq, a.iu_mul, a.iu_shr);
+          const uint32_t r = seq - k * IU;
+          const uint32_t unit = unitq[k % kUQ];
+          if constexpr (est) {
+            const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
+            const uint32_t j = r - pl * L;
+            const uint64_t p = (uint64_t)unit * U + pl;
+            blk = k;
+            if (p < a.n_points) {
+              const int inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+              const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+              const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+              W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
+                       (uint64_t)a.point_ids[p], tid, sg);
+              l.seq = seq;
+              active = true;
+            } else {  // null item padding the last unit: complete at once
+              atomicAdd(&cnt[blk % kSlots], 1u);
+            }
+          } else {
+            const uint64_t row = (uint64_t)unit * IU + r;
+            if (row < a.n_points) {
+              W::start(l, table, a.hdr, a, a.points + (size_t)row * DIM, 0, a.row_pid[row],
+                       a.row_tid[row], a.row_sign[row]);
+              l.seq = (uint32_t)row;
+              active = true;
+            }
           }
         }
+        s_issue += n;
       }
-      s_issue += n;
     }
 
     // ================= one step of every active walk =================
@@ -988,7 +1005,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         lane_steps += (unsigned long long)l.step;
         if constexpr (est) {
           ring[l.seq % kRing] = v;
-          ready = atomicAdd(&cnt[blk % kSlots], 1u) + 1u == IU;
+          atomicAdd(&cnt[blk % kSlots], 1u);
         } else {
           a.out_values[l.seq] = (double)v;
           a.out_steps[l.seq] = (int64_t)l.step;
@@ -1002,14 +1019,6 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       }
     }
     idle = __ballot_sync(WOS_FULL, !active);
-
-    // ================= retire completed units, in stream order =================
-    if constexpr (est) {
-      if (__any_sync(WOS_FULL, ready)) {
-        __syncwarp();
-        retire();
-      }
-    }
   }
 
   // ---- walk-step total (u64, deterministic integer sum) ----
