@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="independent label replicas per point per step (small configs)")
     ap.add_argument("--refill-min", type=int, default=None)
     ap.add_argument("--blocks-per-sm", type=int, default=None)
     args = ap.parse_args()
@@ -237,7 +239,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    w = configs.build(args.config, mode=args.mode)
+    w = configs.build(args.config, mode=args.mode).replicate(args.replicas)
     idx = shard_indices(w.n_points, rank, world)
     shard = w.subset(idx)
     ctx = engine.get_context(local)
@@ -341,7 +343,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = cpu_baseline(configs.build(args.config, mode="replay"))
+            cpu = cpu_baseline(configs.build(args.config, mode="replay").replicate(args.replicas))
         sfu_peak = peaks["sfu_ops_per_s"]
         fp32_peak = peaks["fp32_flops_per_s"]
         fr_sfu = sfu_ach / sfu_peak
@@ -368,6 +370,7 @@ def main():
                 "points": w.n_points,
                 "walks_per_point": w.L,
                 "instances": len(w.problems),
+                "replicas": args.replicas,
                 "eps": w.cfg.eps_shell,
                 "max_steps": w.cfg.max_steps,
                 "mode": args.mode,

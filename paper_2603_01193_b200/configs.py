@@ -70,6 +70,23 @@ class Workload:
             self.inst_index[idx], self.L, self.cfg, self.analytic, dict(self.meta),
         )
 
+    def replicate(self, R: int):
+        """R independent label replicas of every point in one batch.
+
+        Replica r of point p gets point id r * (max id + 1) + id, i.e. its own Philox
+        streams: R independent estimates of the same labels (small
+        configs are measured with replicas per launch).
+        """
+        if R <= 1:
+            return self
+        span = int(self.point_ids.max()) + 1
+        ids = np.concatenate([self.point_ids + r * span for r in range(R)])
+        return Workload(
+            self.index, self.name, self.dim, self.problems, np.tile(self.points, (R, 1)), ids,
+            np.tile(self.inst_index, R), self.L, self.cfg, self.analytic,
+            dict(self.meta, replicas=R),
+        )
+
     def with_mode(self, mode: str):
         c = self.cfg
         cfg = WalkConfig(c.eps_shell, c.max_steps, c.antithetic, c.sigma_bar, c.rng_seed, mode)

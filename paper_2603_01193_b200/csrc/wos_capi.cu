@@ -795,7 +795,9 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
       a.n_units = (uint32_t)(m * n_chunks);
       a.partials = partials;
     } else {
-      a.U = (uint32_t)std::max<int64_t>(1, (kUnitTarget + L - 1) / L);
+      // L >= 32: one point per unit (the cached-point fast refill path);
+      // smaller L: whole points up to >= kUnitTarget walks per unit
+      a.U = L >= 32 ? 1u : (uint32_t)((kUnitTarget + L - 1) / L);
       a.IU = a.U * a.L;
       a.n_units = (uint32_t)((m + a.U - 1) / a.U);
       a.n_chunks = 0;

@@ -23,7 +23,7 @@ constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
 constexpr int kChunk = 128;       // L > kChunk: work units are kChunk-walk chunks of one point
-constexpr int kUnitTarget = 128;  // walks per grabbed work unit (at least)
+constexpr int kUnitTarget = 128;  // L < 32: whole points per unit up to >= this many walks
 constexpr int kCP = 256;          // floats of single-instance parameters held in the kernel params
 constexpr int kDomOff = 0;        // table row: [0, 8) domain params
 constexpr int kSrcOff = 16;       //            [16, 16 + ns) source params, then boundary params
