@@ -620,31 +620,34 @@ struct Walker {
       l.x[1] = fmaf(sd, sth, l.x[1]);
     } else if constexpr (S::SRC == SRC_NONE) {
       const float z = fmaf(2.0f, f12(A.x), -3.0f);
-      const float sxy = fast_sqrt(fmaxf(0.0f, fmaf(-z, z, 1.0f)));
+      const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
       __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
-      l.x[0] = fmaf(sd, sxy * cph, l.x[0]);
-      l.x[1] = fmaf(sd, sxy * sph, l.x[1]);
+      const float sdxy = sd * sxy;
+      l.x[0] = fmaf(sdxy, cph, l.x[0]);
+      l.x[1] = fmaf(sdxy, sph, l.x[1]);
       l.x[2] = fmaf(sd, z, l.x[2]);
     } else {
       float u[7];
       native_uniforms7(A, u);
+      // z = 2u - 1 is exact for u = f - 1 (23-bit f in [1, 2)), so fmaf(-z, z, 1) >= 0
       const float z = fmaf(2.0f, u[0], -3.0f);
-      const float sxy = fast_sqrt(fmaxf(0.0f, fmaf(-z, z, 1.0f)));
+      const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
       __sincosf(fmaf(u[1], kTwoPiF, -kTwoPiF), &sph, &cph);
       const float vz = fmaf(2.0f, u[2], -3.0f);
-      const float vs = fast_sqrt(fmaxf(0.0f, fmaf(-vz, vz, 1.0f)));
+      const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
       float vsp, vcp;
       __sincosf(fmaf(u[3], kTwoPiF, -kTwoPiF), &vsp, &vcp);
-      // Beta(2,2) radius fraction = median of three uniforms
-      const float t = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6])) - 1.0f;
-      const float sr = l.sgn * (d * t);
-      const float g[3] = {fmaf(sr, vs * vcp, l.x[0]), fmaf(sr, vs * vsp, l.x[1]),
-                          fmaf(sr, vz, l.x[2])};
+      // Beta(2,2) radius fraction = median of three uniforms; r = d * (med - 1)
+      const float med = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6]));
+      const float sr = l.sgn * fmaf(d, med, -d);
+      const float srv = sr * vs;
+      const float g[3] = {fmaf(srv, vcp, l.x[0]), fmaf(srv, vsp, l.x[1]), fmaf(sr, vz, l.x[2])};
       l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
-      l.x[0] = fmaf(sd, sxy * cph, l.x[0]);
-      l.x[1] = fmaf(sd, sxy * sph, l.x[1]);
+      const float sdxy = sd * sxy;
+      l.x[0] = fmaf(sdxy, cph, l.x[0]);
+      l.x[1] = fmaf(sdxy, sph, l.x[1]);
       l.x[2] = fmaf(sd, z, l.x[2]);
     }
   }
