@@ -200,8 +200,8 @@ int wos_walk_rows_host(wos_context* ctx, const wos_problem_set* set,
  * trajectories with traj ids traj_start + j (antithetic: traj_start + 2*(j/2),
  * signs +1/-1, samples = pair means; estimator.py:119-141) and is reduced to
  * (mean, m2) with m2 = sum (v - mean)^2 over its n = L (or L/2) samples.
- * Device pointers: points [P, dim] fp64, point_ids [P] int64, inst_index [P] int32
- * or NULL, out_mean/out_m2 [P] fp64, out_total_steps: device uint64 accumulator
+ * Device pointers: points [P, dim] fp64, point_ids [P] int64 or NULL (ids = 0..P-1,
+ * estimator.py:165), inst_index [P] int32 or NULL, out_mean/out_m2 [P] fp64, out_total_steps: device uint64 accumulator
  * (added to, not overwritten) or NULL. Exterior start points are detected on the
  * device; query them with wos_context_exterior().                           */
 int wos_estimate(wos_context* ctx, const wos_problem_set* set, const wos_walk_config* cfg,
@@ -210,7 +210,8 @@ int wos_estimate(wos_context* ctx, const wos_problem_set* set, const wos_walk_co
                  double* out_mean, double* out_m2, uint64_t* out_total_steps,
                  void* stream);
 
-/* Same with host buffers (copies inside, synchronous). Returns WOS_ERR_EXTERIOR
+/* Same with host buffers (copies inside, synchronous; large calls are pipelined in
+ * point chunks so host<->device copies overlap the walks). Returns WOS_ERR_EXTERIOR
  * (outputs undefined) if a start point is exterior; wos_context_exterior() then
  * reports its index. out_total_steps: host, may be NULL (overwritten, not added). */
 int wos_estimate_host(wos_context* ctx, const wos_problem_set* set,

@@ -44,11 +44,16 @@ static int fail(int code, const char* fmt, ...) {
 // context and problem set
 // ------------------------------------------------------------------------
 constexpr int kCounterRing = 256;
+constexpr int kPipeChunks = 4;                 // host pipeline: point chunks per call (at most)
+constexpr int64_t kPipeMinWork = 1ll << 23;    // walks per chunk (at least)
 
 struct wos_context {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;          // private stream of the *_host entry points
+  cudaStream_t copy_stream = nullptr;     // host pipeline copies
+  cudaEvent_t ev_copy[kPipeChunks] = {};
+  cudaEvent_t ev_kernel[kPipeChunks] = {};
   unsigned int* d_counters = nullptr;     // work counters, one per launch slot
   std::atomic<unsigned> next_counter{0};
   unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
@@ -107,6 +112,11 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < kPipeChunks && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_kernel[i], cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, sizeof(unsigned) * kCounterRing);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_exterior, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
@@ -130,6 +140,11 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_watchdog);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (int i = 0; i < kPipeChunks; ++i) {
+    if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+    if (c->ev_kernel[i]) cudaEventDestroy(c->ev_kernel[i]);
+  }
   delete c;
 }
 
@@ -502,7 +517,7 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
                                     const int32_t* __restrict__ inst, const double* __restrict__ table,
                                     int stride, const InstHdr* __restrict__ hdr,
                                     const double* __restrict__ segs, int dim, int dom_kind,
-                                    unsigned long long* first) {
+                                    unsigned long long* first, int64_t idx_base) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int i = inst ? inst[p] : 0;
@@ -529,16 +544,16 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
       }
       inside = in;
     }
-    if (!inside) atomicMin(first, (unsigned long long)p);
+    if (!inside) atomicMin(first, (unsigned long long)(idx_base + p));
   }
 }
 
 static int launch_interior(wos_context* c, const wos_problem_set* s, int64_t n, const double* pts,
-                           const int32_t* inst, cudaStream_t st) {
+                           const int32_t* inst, cudaStream_t st, int64_t idx_base = 0) {
   if (n <= 0) return WOS_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->num_sms * 8);
   wos_interior_kernel<<<blocks, 256, 0, st>>>(n, pts, inst, s->d_table_d, s->stride, s->d_hdr,
-                                              s->d_segs_d, s->dim, s->dom_kind, c->d_exterior);
+                                              s->d_segs_d, s->dim, s->dom_kind, c->d_exterior, idx_base);
   CUDA_TRY(cudaGetLastError());
   return WOS_OK;
 }
@@ -754,11 +769,13 @@ extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos
   return WOS_OK;
 }
 
-extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
-                            int64_t P, const double* points, const int64_t* point_ids,
-                            const int32_t* inst_index, int64_t L, uint64_t traj_start,
-                            double* out_mean, double* out_m2, uint64_t* out_total_steps,
-                            void* stream) {
+// idx_base: index of points[0] in the caller's full point array (chunked host
+// pipeline): offsets exterior-point reports and the default point ids.
+static int estimate_impl(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
+                         int64_t P, const double* points, const int64_t* point_ids,
+                         const int32_t* inst_index, int64_t L, uint64_t traj_start,
+                         double* out_mean, double* out_m2, uint64_t* out_total_steps,
+                         cudaStream_t st, int64_t idx_base) {
   if (!c || !s || !cfg) return fail(WOS_ERR_INVALID, "null argument");
   if (P < 0) return fail(WOS_ERR_INVALID, "negative point count");
   if (L < 1) return fail(WOS_ERR_INVALID, "trajectory count must be at least 1");
@@ -768,8 +785,7 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
   if (L > kMaxItemsPerLaunch) return fail(WOS_ERR_UNSUPPORTED, "L too large");
   if (P == 0) return WOS_OK;
   CUDA_TRY(cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  int r = launch_interior(c, s, P, points, inst_index, st);
+  int r = launch_interior(c, s, P, points, inst_index, st, idx_base);
   if (r) return r;
   // L > kChunk: units are kChunk-walk chunks of one point, merged by wos_merge_chunks_kernel
   const bool split = L > kChunk;
@@ -806,7 +822,8 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
     fast_div_init(a.L, &a.l_mul, &a.l_shr);
     fast_div_init(std::max<uint32_t>(1u, a.n_chunks), &a.nc_mul, &a.nc_shr);
     a.points = points + off * s->dim;
-    a.point_ids = point_ids + off;
+    a.point_ids = point_ids ? point_ids + off : nullptr;
+    a.id_base = (uint64_t)(idx_base + off);
     a.inst_index = inst_index ? inst_index + off : nullptr;
     a.traj_start = traj_start;
     a.out_mean = out_mean + off;
@@ -827,6 +844,15 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
   }
   if (partials) CUDA_TRY(cudaFreeAsync(partials, st));
   return WOS_OK;
+}
+
+extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
+                            int64_t P, const double* points, const int64_t* point_ids,
+                            const int32_t* inst_index, int64_t L, uint64_t traj_start,
+                            double* out_mean, double* out_m2, uint64_t* out_total_steps,
+                            void* stream) {
+  return estimate_impl(c, s, cfg, P, points, point_ids, inst_index, L, traj_start, out_mean, out_m2,
+                       out_total_steps, (cudaStream_t)stream, 0);
 }
 
 // ---- host-buffer variants ------------------------------------------------
@@ -914,6 +940,9 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
     if (out_total_steps) *out_total_steps = 0;
     return P < 0 ? fail(WOS_ERR_INVALID, "negative point count") : WOS_OK;
   }
+  if (L < 1 || (cfg->antithetic && (L % 2)))  // same checks and messages as wos_estimate
+    return estimate_impl(c, s, cfg, P, nullptr, nullptr, nullptr, L, traj_start, nullptr, nullptr,
+                         nullptr, c->stream, 0);
   std::lock_guard<std::mutex> g(c->mu);
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t bp = al(P * s->dim * 8), b8 = al(P * 8), b4 = al(P * 4);
@@ -921,27 +950,49 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   int r = scratch(c, bp + 3 * b8 + b4, &base);
   if (r) return r;
   double* d_pts = (double*)base;
-  int64_t* d_ids = (int64_t*)(base + bp);
+  int64_t* d_ids = point_ids ? (int64_t*)(base + bp) : nullptr;
   double* d_mean = (double*)(base + bp + b8);
   double* d_m2 = (double*)(base + bp + 2 * b8);
   int32_t* d_inst = inst_index ? (int32_t*)(base + bp + 3 * b8) : nullptr;
-  cudaStream_t st = c->stream;
-  CUDA_TRY(cudaMemcpyAsync(d_pts, points, P * s->dim * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(d_ids, point_ids, P * 8, cudaMemcpyHostToDevice, st));
-  if (d_inst) CUDA_TRY(cudaMemcpyAsync(d_inst, inst_index, P * 4, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(unsigned long long), st));
-  r = wos_estimate(c, s, cfg, P, d_pts, d_ids, d_inst, L, traj_start, d_mean, d_m2,
-                   reinterpret_cast<uint64_t*>(c->d_steps), st);
-  if (r) return r;
+  const cudaStream_t cs = c->stream, xs = c->copy_stream;
+  CUDA_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(unsigned long long), cs));
+  // Software pipeline over point chunks: copies on `xs`, walks on `cs`, so the
+  // copies of chunk i+1 and the results of chunk i-1 overlap the walks of chunk i.
+  const int64_t work = P * L;
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kPipeChunks, work / kPipeMinWork));
+  int64_t lo[kPipeChunks + 1];
+  for (int i = 0; i <= nch; ++i) lo[i] = P * i / nch;
+  auto d2h = [&](int i) -> int {
+    const int64_t o = lo[i], m = lo[i + 1] - lo[i];
+    CUDA_TRY(cudaStreamWaitEvent(xs, c->ev_kernel[i], 0));
+    CUDA_TRY(cudaMemcpyAsync(out_mean + o, d_mean + o, m * 8, cudaMemcpyDeviceToHost, xs));
+    CUDA_TRY(cudaMemcpyAsync(out_m2 + o, d_m2 + o, m * 8, cudaMemcpyDeviceToHost, xs));
+    return WOS_OK;
+  };
+  for (int i = 0; i < nch; ++i) {
+    const int64_t o = lo[i], m = lo[i + 1] - lo[i];
+    CUDA_TRY(cudaMemcpyAsync(d_pts + o * s->dim, points + o * s->dim, m * s->dim * 8,
+                             cudaMemcpyHostToDevice, xs));
+    if (d_ids) CUDA_TRY(cudaMemcpyAsync(d_ids + o, point_ids + o, m * 8, cudaMemcpyHostToDevice, xs));
+    if (d_inst) CUDA_TRY(cudaMemcpyAsync(d_inst + o, inst_index + o, m * 4, cudaMemcpyHostToDevice, xs));
+    CUDA_TRY(cudaEventRecord(c->ev_copy[i], xs));
+    CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_copy[i], 0));
+    r = estimate_impl(c, s, cfg, m, d_pts + o * s->dim, d_ids ? d_ids + o : nullptr,
+                      d_inst ? d_inst + o : nullptr, L, traj_start, d_mean + o, d_m2 + o,
+                      reinterpret_cast<uint64_t*>(c->d_steps), cs, o);
+    if (r) return r;
+    CUDA_TRY(cudaEventRecord(c->ev_kernel[i], cs));
+    if (i > 0 && (r = d2h(i - 1))) return r;
+  }
+  if ((r = d2h(nch - 1))) return r;
   unsigned long long steps = 0, ext = 0;
-  CUDA_TRY(cudaMemcpyAsync(out_mean, d_mean, P * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(out_m2, d_m2, P * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&steps, c->d_steps, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&ext, c->d_exterior, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, 8, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaMemcpyAsync(&steps, c->d_steps, 8, cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaMemcpyAsync(&ext, c->d_exterior, 8, cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, 8, cs));
+  CUDA_TRY(cudaStreamSynchronize(cs));
+  CUDA_TRY(cudaStreamSynchronize(xs));
   if (out_total_steps) *out_total_steps = steps;
-  r = check_watchdog(c, st);
+  r = check_watchdog(c, cs);
   if (r) return r;
   if (ext != ~0ull) {
     c->host_exterior = (int64_t)ext;

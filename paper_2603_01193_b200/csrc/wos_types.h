@@ -89,7 +89,8 @@ struct KArgs {
   uint32_t iu_mul, iu_shr;  // magic numbers: n / IU = (umulhi(n, mul) + n) >> shr, n < 2^31
   uint32_t l_mul, l_shr;    // same for n / L
   const double* points;        // [n, dim]
-  const int64_t* point_ids;    // estimate
+  const int64_t* point_ids;    // estimate; null = ids are id_base + index
+  uint64_t id_base;
   const int32_t* inst_index;   // estimate, may be null
   uint64_t traj_start;
   const uint64_t* row_pid;     // rows

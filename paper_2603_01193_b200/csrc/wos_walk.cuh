@@ -909,7 +909,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               }
 #pragma unroll
               for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
-              cu_pid = (uint64_t)a.point_ids[p];
+              cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
               cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
               room = IU;
             } else if (n_idle == 32 && exhausted && r_seq == s_issue) {
@@ -979,7 +979,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
               const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
               W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
-                       (uint64_t)a.point_ids[p], tid, sg);
+                       a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p, tid, sg);
               l.seq = seq;
               active = true;
             } else {  // null item padding the last unit: complete at once

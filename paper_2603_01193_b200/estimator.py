@@ -93,7 +93,7 @@ def _estimate_one_device(device, problems, pts, pids, inst, L, cfg, eps, traj_st
     m2 = np.empty(P, dtype=np.float64)
     steps = c_uint64(0)
     status = ctx._lib.wos_estimate_host(
-        ctx.handle, pset.handle, byref(wc), P, pts.ctypes.data, pids.ctypes.data,
+        ctx.handle, pset.handle, byref(wc), P, pts.ctypes.data, None if pids is None else pids.ctypes.data,
         None if inst is None else inst.ctypes.data, int(L), int(traj_start) & ((1 << 64) - 1),
         mean.ctypes.data, m2.ctypes.data, byref(steps),
     )
@@ -126,10 +126,9 @@ def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None
     if pts.ndim == 1:
         pts = pts[None, :]
     P = pts.shape[0]
-    pids = np.ascontiguousarray(
-        np.arange(P, dtype=np.int64) if point_ids is None else np.asarray(point_ids).astype(np.int64)
-    )
-    if pids.shape != (P,):
+    # point_ids=None: ids 0..P-1 (estimator.py:165), generated on the device (no copy)
+    pids = None if point_ids is None else np.ascontiguousarray(np.asarray(point_ids).astype(np.int64))
+    if pids is not None and pids.shape != (P,):
         raise ValueError("point_ids must have one entry per point")
     inst = None
     if inst_index is not None:
@@ -155,6 +154,9 @@ def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None
     else:
         chunks = np.array_split(np.arange(P), ndev)
         results = [None] * ndev
+
+        if pids is None:
+            pids = np.arange(P, dtype=np.int64)
 
         def run(i, idx):
             results[i] = _estimate_one_device(
