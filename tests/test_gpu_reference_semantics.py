@@ -1,0 +1,244 @@
+"""The reference's own walker/estimator test semantics, run on the CUDA path.
+
+Ports the behaviours pinned by /root/reference/pkg/tests/test_walker.py and
+test_estimator.py (exact values, termination rules, determinism, antithetic
+pairs, estimate bookkeeping, errors) to this package, in both the REPLAY
+(reference estimator) and NATIVE (production) modes where they apply, plus
+edge cases: empty inputs, L = 1, very long ensembles, every domain kind.
+"""
+
+import math
+import types
+
+import numpy as np
+import pytest
+
+from paper_2603_01193_b200 import (BallDomain, BoxDomain, ExteriorQueryError, PolygonDomain,
+                                   Problem, TrajectoryStream, WalkConfig, estimate, estimate_arrays,
+                                   specs, star_polygon, walk_poisson, walk_poisson_antithetic,
+                                   walk_poisson_values)
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["replay", "native"]
+DISK = BallDomain([0.0, 0.0], 1.0)
+BALL = BallDomain([0.0, 0.0, 0.0], 1.0)
+SQUARE = BoxDomain([0.0, 0.0], [1.0, 1.0])
+POLY = star_polygon([0.05, -0.03, 0.02, 0.01], [0.0, 0.04, -0.02, 0.01], 64)
+
+DISK_POISSON = Problem(DISK, boundary_spec=specs.const_boundary(0.0), source_spec=specs.const_source(1.0))
+BALL_POISSON = Problem(BALL, boundary_spec=specs.const_boundary(0.0), source_spec=specs.const_source(1.0))
+
+
+def run_walks(inst, point, n, cfg, traj_start=0):
+    pts = np.tile(np.asarray(point, dtype=np.float64), (n, 1))
+    return walk_poisson_values(inst, pts, np.zeros(n), np.arange(traj_start, traj_start + n),
+                               np.ones(n), cfg)
+
+
+def mean_se(v):
+    return float(v.mean()), float(v.std(ddof=1) / math.sqrt(len(v)))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("dom,pt", [(DISK, [0.3, -0.2]), (SQUARE, [0.3, 0.7]), (POLY, [0.1, -0.2]),
+                                    (BALL, [0.1, 0.2, -0.3])])
+def test_constant_boundary_exact_every_trajectory(gpu, mode, dom, pt):
+    inst = Problem(dom, boundary_spec=specs.const_boundary(3.25))
+    v, s, h = run_walks(inst, pt, 500, WalkConfig(rng_seed=1, mode=mode))
+    assert np.all(v == 3.25)
+    assert np.all(h == 1)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_disk_constant_source_off_center(gpu, mode):
+    p = [0.5, -0.3]
+    want = (0.5**2 + 0.3**2 - 1.0) / 4.0
+    v, _, _ = run_walks(DISK_POISSON, p, 60_000, WalkConfig(rng_seed=8, mode=mode))
+    m, se = mean_se(v)
+    assert abs(m - want) < 3.0 * se
+
+
+def test_disk_and_ball_constant_source_at_center_replay(gpu):
+    v, _, _ = run_walks(DISK_POISSON, [0.0, 0.0], 100_000, WalkConfig(rng_seed=7, mode="replay"))
+    m, se = mean_se(v)
+    assert abs(m + 0.25) < 3.0 * se
+    v, _, _ = run_walks(BALL_POISSON, [0.0, 0.0, 0.0], 100_000, WalkConfig(rng_seed=9, mode="replay"))
+    m, se = mean_se(v)
+    assert abs(m + 1.0 / 6.0) < 3.0 * se
+
+
+def test_ball_constant_source_native(gpu):
+    # Green's-function sampling: from the centre the first jump is the whole ball -> exact
+    v, s, _ = run_walks(BALL_POISSON, [0.0, 0.0, 0.0], 1000, WalkConfig(rng_seed=9))
+    np.testing.assert_allclose(v, -1.0 / 6.0, rtol=1e-6)
+    p = [0.3, -0.2, 0.1]
+    want = (0.09 + 0.04 + 0.01 - 1.0) / 6.0
+    v, _, _ = run_walks(BALL_POISSON, p, 60_000, WalkConfig(rng_seed=9))
+    m, se = mean_se(v)
+    assert abs(m - want) < 3.0 * se
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_first_step_from_center_reaches_boundary(gpu, mode):
+    inst = Problem(DISK, boundary_spec=specs.const_boundary(0.0))
+    _, s, h = run_walks(inst, [0.0, 0.0], 200, WalkConfig(rng_seed=3, mode=mode))
+    assert np.all(s == 1)
+    assert np.all(h == 1)
+
+
+@pytest.mark.parametrize("mode,tol", [("replay", 1e-12), ("native", 1e-6)])
+def test_start_inside_shell_returns_projection_value(gpu, mode, tol):
+    inst = Problem(DISK, boundary_spec=specs.linear_boundary([1.0, 0.0, 0.0]))
+    r = walk_poisson(inst, [1.0 - 1e-5, 0.0], WalkConfig(rng_seed=4, mode=mode))
+    assert r.steps_taken == 0
+    assert r.terminated_by == "boundary"
+    assert r.value == pytest.approx(1.0, abs=tol)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_max_steps_projection(gpu, mode):
+    for dom, p in ((POLY, [0.0, 0.0]), (SQUARE, [0.5, 0.5])):
+        inst = Problem(dom, boundary_spec=specs.const_boundary(2.0))
+        v, s, h = run_walks(inst, p, 256, WalkConfig(rng_seed=5, max_steps=2, mode=mode))
+        assert np.all(s <= 2)
+        assert np.all((h == 1) | (s == 2))
+        assert (h == 0).any()
+        assert np.all(v == 2.0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_max_steps_bias_negligible(gpu, mode):
+    v1, _, _ = run_walks(DISK_POISSON, [0.2, 0.2], 20_000, WalkConfig(rng_seed=11, max_steps=1000, mode=mode))
+    v2, _, _ = run_walks(DISK_POISSON, [0.2, 0.2], 20_000, WalkConfig(rng_seed=11, max_steps=10_000, mode=mode))
+    assert abs(v1.mean() - v2.mean()) < math.hypot(mean_se(v1)[1], mean_se(v2)[1]) + 1e-12
+
+
+@pytest.mark.parametrize("dom,out", [(DISK, [2.0, 0.0]), (SQUARE, [1.5, 0.5]), (POLY, [3.0, 0.0]),
+                                     (BALL, [0.0, 0.0, 1.5])])
+def test_exterior_start_raises(gpu, dom, out):
+    inst = Problem(dom, boundary_spec=specs.const_boundary(0.0))
+    with pytest.raises(ExteriorQueryError):
+        walk_poisson(inst, out, WalkConfig())
+    inside = [0.5, 0.5] if dom is SQUARE else ([0.0, 0.0, 0.0] if dom is BALL else [0.0, 0.0])
+    with pytest.raises(ExteriorQueryError):
+        estimate(inst, [inside, out], 4, WalkConfig())
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_replay_bitwise_and_layout_invariance(gpu, mode):
+    cfg = WalkConfig(rng_seed=23, mode=mode)
+    a = walk_poisson(DISK_POISSON, [0.1, 0.2], cfg, TrajectoryStream(3, 9))
+    b = walk_poisson(DISK_POISSON, [0.1, 0.2], cfg, TrajectoryStream(3, 9))
+    assert a == b
+    pts = np.array([[0.1, 0.2], [0.3, -0.1], [0.0, 0.5], [-0.4, -0.2]])
+    pids, tids = np.array([0, 1, 2, 3]), np.array([5, 6, 7, 8])
+    full, _, _ = walk_poisson_values(DISK_POISSON, pts, pids, tids, np.ones(4), cfg)
+    for i in range(4):
+        one, _, _ = walk_poisson_values(DISK_POISSON, pts[i:i + 1], pids[i:i + 1], tids[i:i + 1], [1.0], cfg)
+        assert one[0] == full[i]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_distinct_streams_and_seeds_differ(gpu, mode):
+    cfg = WalkConfig(rng_seed=17, mode=mode)
+    a = walk_poisson(DISK_POISSON, [0.1, 0.2], cfg, TrajectoryStream(0, 0))
+    b = walk_poisson(DISK_POISSON, [0.1, 0.2], cfg, TrajectoryStream(0, 1))
+    c = walk_poisson(DISK_POISSON, [0.1, 0.2], cfg, TrajectoryStream(1, 0))
+    d = walk_poisson(DISK_POISSON, [0.1, 0.2], WalkConfig(rng_seed=18, mode=mode), TrajectoryStream(0, 0))
+    assert len({a.value, b.value, c.value, d.value}) == 4
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_instance_key_selects_the_stream(gpu, mode):
+    p0 = Problem(DISK, boundary_spec=specs.const_boundary(0.0), source_spec=specs.const_source(1.0), instance_key=0)
+    p1 = Problem(DISK, boundary_spec=specs.const_boundary(0.0), source_spec=specs.const_source(1.0), instance_key=1)
+    cfg = WalkConfig(rng_seed=2, mode=mode)
+    v0, _, _ = run_walks(p0, [0.3, 0.3], 64, cfg)
+    v1, _, _ = run_walks(p1, [0.3, 0.3], 64, cfg)
+    assert not np.array_equal(v0, v1)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_antithetic_pair_from_origin_cancels_linear_data(gpu, mode):
+    inst = Problem(DISK, boundary_spec=specs.linear_boundary([1.0, 0.0, 0.0]))
+    for t in range(30):
+        a, b = walk_poisson_antithetic(inst, [0.0, 0.0], WalkConfig(rng_seed=29, mode=mode),
+                                       TrajectoryStream(0, t))
+        assert a.value + b.value == 0.0
+        assert a.steps_taken == b.steps_taken
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_antithetic_estimate_counts_pairs(gpu, mode):
+    cfg = WalkConfig(rng_seed=10, antithetic=True, mode=mode)
+    (est,) = estimate(DISK_POISSON, [0.2, 0.0], 40, cfg)
+    assert est.n_samples == 20
+    with pytest.raises(ValueError):
+        estimate(DISK_POISSON, [0.2, 0.0], 41, cfg)
+    with pytest.raises(ValueError):
+        estimate(DISK_POISSON, [0.2, 0.0], 0, WalkConfig(mode=mode))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_single_trajectory_estimate_equals_walk(gpu, mode):
+    cfg = WalkConfig(rng_seed=5, mode=mode)
+    (est,) = estimate(DISK_POISSON, [0.2, 0.1], 1, cfg)
+    direct = walk_poisson(DISK_POISSON, [0.2, 0.1], cfg)
+    assert est.mean == direct.value
+    assert est.n_samples == 1 and math.isnan(est.variance)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_constant_boundary_zero_variance_and_holder(gpu, mode):
+    const = Problem(DISK, boundary_spec=specs.const_boundary(4.5))
+    (est,) = estimate(types.SimpleNamespace(problem=const), [0.3, -0.2], 40, WalkConfig(rng_seed=6, mode=mode))
+    assert est.mean == 4.5 and est.variance == 0.0
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("L", [30, 300])
+def test_multi_point_matches_single_point_calls(gpu, mode, L):
+    pts = np.array([[0.1, 0.2], [0.3, -0.1], [-0.5, 0.0]])
+    cfg = WalkConfig(rng_seed=8, mode=mode)
+    batch = estimate(DISK_POISSON, pts, L, cfg)
+    for i in range(3):
+        (solo,) = estimate(DISK_POISSON, pts[i], L, cfg, point_ids=[i])
+        assert solo.mean == batch[i].mean and solo.m2 == batch[i].m2
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_traj_windows_are_disjoint(gpu, mode):
+    cfg = WalkConfig(rng_seed=9, mode=mode)
+    (a,) = estimate(DISK_POISSON, [0.1, 0.1], 50, cfg, traj_start=0)
+    (b,) = estimate(DISK_POISSON, [0.1, 0.1], 50, cfg, traj_start=50)
+    assert a.mean != b.mean
+
+
+def test_multi_instance_batch_equals_per_instance_calls(gpu):
+    from paper_2603_01193_b200 import configs
+
+    w = configs.build(3)
+    sel = np.concatenate([np.flatnonzero(w.inst_index == j)[:40] for j in (2, 5, 9)])
+    sub = w.subset(sel)
+    mean, m2, _ = estimate_arrays(sub.problems, sub.points, 64, sub.cfg, inst_index=sub.inst_index,
+                                  point_ids=sub.point_ids)
+    for j in (2, 5, 9):
+        m = sub.inst_index == j
+        mj, qj, _ = estimate_arrays(sub.problems[j], sub.points[m], 64, sub.cfg, point_ids=sub.point_ids[m])
+        assert np.array_equal(mj, mean[m]) and np.array_equal(qj, m2[m])
+
+
+def test_empty_inputs(gpu):
+    assert estimate(DISK_POISSON, np.zeros((0, 2)), 8, WalkConfig()) == []
+    v, s, h = walk_poisson_values(DISK_POISSON, np.zeros((0, 2)), [], [], [], WalkConfig())
+    assert v.shape == (0,) and s.shape == (0,) and h.shape == (0,)
+
+
+def test_very_long_ensemble(gpu):
+    """L = 100 000 for one point (782 chunks, test_estimator.py:105-107 at scale)."""
+    p = [0.5, -0.3]
+    want = (0.25 + 0.09 - 1.0) / 4.0
+    (est,) = estimate(DISK_POISSON, p, 100_000, WalkConfig(rng_seed=7))
+    assert est.n_samples == 100_000
+    assert abs(est.mean - want) < 3.0 * est.std_error
