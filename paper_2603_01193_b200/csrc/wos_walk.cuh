@@ -862,6 +862,107 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
   };
 
+  // ======================================================================
+  // Eager fast path (ESTIMATE, one point per unit, polygon domains): finished walks
+  // are recorded and their lanes re-issued in the same divergent block right after
+  // the step; unit grabs, retirement and the exit test run only when the unit or
+  // the ring runs short. Re-issuing every iteration costs a divergent start per
+  // iteration, which pays off only when a jump is expensive (a 128-segment scan);
+  // cheap jumps use the batched refill of the general loop below (measured, cfg3
+  // vs cfg4: DESIGN.md section 3).
+  // ======================================================================
+  constexpr bool kEager = (S::DOM == DOM_POLY);
+  if (kEager && fast) {
+    while (true) {
+      bool fin = false;
+      if (active) {
+        const Real d = W::dist(l, a, srec);
+        if (d < eps || l.step >= a.max_steps) {
+          fin = true;
+        } else {
+          if constexpr (S::NATIVE) W::advance_native(l, d, a);
+          else W::advance_replay(l, d, a);
+          l.step += 1;
+        }
+      }
+      idle |= __ballot_sync(WOS_FULL, fin);
+      if (idle == 0u) continue;
+      if (fin) {  // record: walker.py:275-281, value = acc + g(projection)
+        const Real v = W::finish_value(l, a);
+        lane_steps += (unsigned long long)l.step;
+        ring[l.seq % kRing] = v;
+        atomicAdd(&cnt[blk % kSlots], 1u);
+        active = false;
+      }
+      const uint32_t n_idle = (uint32_t)__popc(idle);
+      uint32_t room = cu_end - s_issue;
+      uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
+      if (room < n_idle || cap < n_idle) {
+        // ---- slow path: free the ring, move to the next unit, or finish ----
+        if (++refills > a.iter_limit) {  // watchdog (a stall can only loop through here)
+          if (lane == 0) atomicExch(a.watchdog, 1u);
+          break;
+        }
+        __syncwarp();
+        retire();
+        cap = r_seq + (uint32_t)kRing - s_issue;
+        if (room == 0) {
+          if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
+            uint32_t u = 0;
+            if (lane == 0) u = atomicAdd(a.work_counter, 1u);
+            u = __shfl_sync(WOS_FULL, u, 0);
+            if (u >= a.n_units) {
+              exhausted = true;
+            } else {
+              if (lane == 0) unitq[n_grabbed % kUQ] = u;
+              ++n_grabbed;
+              s_avail += IU;
+            }
+          }
+          if (n_grabbed != cu_k + 1u) {  // the next unit is grabbed: cache its point
+            cu_k += 1u;
+            cu_end += IU;
+            const uint32_t unit = unitq[cu_k % kUQ];
+            uint32_t p = unit;
+            cu_j0 = 0;
+            cu_jend = L;
+            if (split) {
+              p = fast_div(unit, a.nc_mul, a.nc_shr);
+              cu_j0 = (unit - p * a.n_chunks) * kChunk;
+              cu_jend = min(L, cu_j0 + kChunk);
+            }
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
+            cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
+            cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+            room = IU;
+          } else if (n_idle == 32 && exhausted && r_seq == s_issue) {
+            break;  // no walk left, none running, all retired
+          }
+        }
+      }
+      const uint32_t n = min(min(n_idle, room), cap);
+      if (!active) {
+        const uint32_t rank = __popc(idle & lanemask_lt());
+        if (rank < n) {
+          const uint32_t seq = s_issue + rank;
+          const uint32_t j = cu_j0 + (seq - (cu_end - IU));
+          blk = cu_k;
+          if (j < cu_jend) {
+            const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+            const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+            W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
+            l.seq = seq;
+            active = true;
+          } else {  // null item padding the point's last chunk: complete at once
+            atomicAdd(&cnt[blk % kSlots], 1u);
+          }
+        }
+      }
+      s_issue += n;
+      idle = __ballot_sync(WOS_FULL, !active);
+    }
+  } else
   while (true) {
     const int n_idle = __popc(idle);
     if (n_idle >= a.refill_min || n_idle == 32) {
