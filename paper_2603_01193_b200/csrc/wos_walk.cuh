@@ -188,22 +188,40 @@ struct Walker {
 
   // polygon: min distance over segments; records the first nearest segment in l.seg_i
   // (the closest point is rebuilt from that one segment only at termination)
-  // NATIVE scan over vertex records {v_k, e_k/|e_k|^2} (record k+1 supplies v_{k+1})
+  // NATIVE scan over vertex records {v_k, e_k/|e_k|^2} (record k+1 supplies v_{k+1}).
+  // Segments go in blocks of 4: the running minimum takes one FMNMX3 + FMNMX per
+  // block and only the first block attaining the minimum is remembered (*bi_out =
+  // its first segment); poly_project resolves the first nearest segment inside it,
+  // which is the global first nearest segment.
+  __device__ static __forceinline__ float seg_d2(float4 R, float4 Rn, float px, float py) {
+    const float ex = Rn.x - R.x, ey = Rn.y - R.y;
+    const float wx = px - R.x, wy = py - R.y;
+    const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
+    const float dx = fmaf(-t, ex, wx), dy = fmaf(-t, ey, wy);
+    return fmaf(dx, dx, dy * dy);
+  }
+
   template <class P>
   __device__ static __forceinline__ float poly_scan(const P rec, int n, float px, float py, int* bi_out) {
     float best = 3.0e38f;
     int bi = 0;
     float4 R = rec[0];
-#pragma unroll 4
-    for (int i = 0; i < n; ++i) {
+    const int n4 = n & ~3;
+#pragma unroll 2
+    for (int i = 0; i < n4; i += 4) {
+      const float4 R1 = rec[i + 1], R2 = rec[i + 2], R3 = rec[i + 3], R4 = rec[i + 4];
+      const float d0 = seg_d2(R, R1, px, py), d1 = seg_d2(R1, R2, px, py);
+      const float d2 = seg_d2(R2, R3, px, py), d3 = seg_d2(R3, R4, px, py);
+      const float m = fminf(fminf(fminf(d0, d1), d2), d3);
+      bi = m < best ? i : bi;
+      best = fminf(best, m);
+      R = R4;
+    }
+    for (int i = n4; i < n; ++i) {  // tail (n not a multiple of 4): exact per segment
       const float4 Rn = rec[i + 1];
-      const float ex = Rn.x - R.x, ey = Rn.y - R.y;
-      const float wx = px - R.x, wy = py - R.y;
-      const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
-      const float dx = fmaf(-t, ex, wx), dy = fmaf(-t, ey, wy);
-      const float d2 = fmaf(dx, dx, dy * dy);
-      bi = d2 < best ? i : bi;
-      best = fminf(best, d2);
+      const float d = seg_d2(R, Rn, px, py);
+      bi = d < best ? i : bi;
+      best = fminf(best, d);
       R = Rn;
     }
     *bi_out = bi;
@@ -245,18 +263,30 @@ struct Walker {
     }
   }
 
-  // closest point on the segment recorded by the last distance query
+  // closest point on the segment recorded by the last distance query (NATIVE: the
+  // first nearest segment of the recorded 4-segment block)
   __device__ static __forceinline__ void poly_project(const Lane& l, const KArgs& a, Real* q) {
-    const int i = l.seg_i;
+    const int i0 = l.seg_i;
     if constexpr (S::NATIVE) {
       const float4* rec = reinterpret_cast<const float4*>(a.segs) + l.rec_off;
-      const float4 R = __ldg(rec + i), Rn = __ldg(rec + i + 1);
+      const int i1 = (i0 + 4 <= (l.n_seg & ~3)) ? i0 + 4 : i0 + 1;  // block or tail segment
+      float best = 3.0e38f;
+      int bi = i0;
+      for (int i = i0; i < i1; ++i) {
+        const float d = seg_d2(__ldg(rec + i), __ldg(rec + i + 1), l.x[0], l.x[1]);
+        if (d < best) {
+          best = d;
+          bi = i;
+        }
+      }
+      const float4 R = __ldg(rec + bi), Rn = __ldg(rec + bi + 1);
       const float ex = Rn.x - R.x, ey = Rn.y - R.y;
       const float wx = l.x[0] - R.x, wy = l.x[1] - R.y;
       const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
       q[0] = fmaf(t, ex, R.x);
       q[1] = fmaf(t, ey, R.y);
     } else {
+      const int i = i0;
       const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
       const Real ax = seg[4 * i], ay = seg[4 * i + 1], ex = seg[4 * i + 2], ey = seg[4 * i + 3];
       const Real wx = l.x[0] - ax, wy = l.x[1] - ay;
