@@ -398,6 +398,24 @@ struct Walker {
       sine_row<K>(y[1], sy);
       if constexpr (DIM == 2) {
         Real f = Real(0);
+        if constexpr (S::NATIVE && (K % 4) == 0) {
+          // rows are 16-byte aligned (kSrcOff and the row stride are multiples of 4)
+          const float4* a4 = reinterpret_cast<const float4*>(a);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            float t = 0.f;
+#pragma unroll
+            for (int l4 = 0; l4 < K / 4; ++l4) {
+              const float4 c = a4[(k * K) / 4 + l4];
+              t = fmaf(c.x, sy[4 * l4], t);
+              t = fmaf(c.y, sy[4 * l4 + 1], t);
+              t = fmaf(c.z, sy[4 * l4 + 2], t);
+              t = fmaf(c.w, sy[4 * l4 + 3], t);
+            }
+            f = fmaf(sx[k], t, f);
+          }
+          return f;
+        }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           Real t = Real(0);
@@ -539,7 +557,20 @@ struct Walker {
           else if (dt <= dl) s = Real(2) + (Real(1) - u);
           else s = Real(3) + (Real(1) - v);
           Real g = Real(0);
-          for (int m = 1; m <= M; ++m) g = g + B[3 + m] * sin((Real)kTwoPi * (Real)m * s / Real(4));
+          if constexpr (S::NATIVE) {
+            // sin(m t), t = 2 pi s / 4, by the rotation recurrence from one sincos
+            float s1, c1;
+            sincosf(kTwoPiF * s * 0.25f, &s1, &c1);
+            float sm = s1, cm = c1;
+            for (int m = 1; m <= M; ++m) {
+              g = fmaf(B[3 + m], sm, g);
+              const float sn = fmaf(sm, c1, cm * s1);
+              cm = fmaf(cm, c1, -sm * s1);
+              sm = sn;
+            }
+          } else {
+            for (int m = 1; m <= M; ++m) g = g + B[3 + m] * sin((Real)kTwoPi * (Real)m * s / Real(4));
+          }
           return g;
         }
         return Real(0);
