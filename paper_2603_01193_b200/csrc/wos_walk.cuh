@@ -549,7 +549,15 @@ struct Walker {
         if constexpr (DIM == 2) {
           const Real x0 = B[0], y0 = B[1], side = B[2];
           const int M = a.bnd_M;
-          const Real u = (q[0] - x0) / side, v = (q[1] - y0) / side;
+          Real u, v;
+          if constexpr (S::NATIVE) {
+            const float inv = __frcp_rn(side);
+            u = (q[0] - x0) * inv;
+            v = (q[1] - y0) * inv;
+          } else {
+            u = (q[0] - x0) / side;
+            v = (q[1] - y0) / side;
+          }
           const Real db = pabs(v), dr = pabs(Real(1) - u), dt = pabs(Real(1) - v), dl = pabs(u);
           Real s;
           if (db <= dr && db <= dt && db <= dl) s = u;
@@ -560,7 +568,7 @@ struct Walker {
           if constexpr (S::NATIVE) {
             // sin(m t), t = 2 pi s / 4, by the rotation recurrence from one sincos
             float s1, c1;
-            sincosf(kTwoPiF * s * 0.25f, &s1, &c1);
+            __sincosf(kTwoPiF * s * 0.25f, &s1, &c1);
             float sm = s1, cm = c1;
             for (int m = 1; m <= M; ++m) {
               g = fmaf(B[3 + m], sm, g);
