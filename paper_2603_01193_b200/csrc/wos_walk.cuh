@@ -840,8 +840,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem + a.stage_bytes + a.seg_stage_bytes +
-                         (size_t)warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4);
+  // the warp's ring offset goes through a shuffle so that ptxas keeps it in a register
+  // instead of re-deriving it from %tid and the launch constants every iteration
+  const uint32_t woff = __shfl_sync(WOS_FULL, (uint32_t)(a.stage_bytes + a.seg_stage_bytes +
+                                    warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4)), 0);
+  unsigned char* wbase = smem + woff;
   Real* ring = reinterpret_cast<Real*>(wbase);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
   uint32_t* unitq = cnt + kSlots;
