@@ -127,6 +127,19 @@ struct Walker {
   static constexpr int DIM = S::DIM;
   static constexpr bool ONE = S::ONE;
 
+  static constexpr bool kHot = S::NATIVE && ONE;
+  static constexpr int kHotK = kHot ? 10 : 1;
+  // hot source coefficients: those the jump reads at compile-time offsets
+  static constexpr int kHotSrcN =
+      !kHot ? 0
+      : S::SRC == SRC_CONST ? 1
+      : S::SRC == SRC_RBF2 ? 6
+      : S::SRC == SRC_GAUSS ? 2 + DIM
+      : (S::SRC == SRC_SINE && (S::SK == 3 || S::SK == 4)) ? (DIM == 2 ? S::SK * S::SK : S::SK * S::SK * S::SK)
+      : 0;
+  static constexpr bool kHotSrc = kHotSrcN > 0;
+  static constexpr int kHotC = kHot ? kSrcOff + kHotSrcN : 1;
+
   struct Lane {
     Real x[DIM];
     Real acc;
@@ -138,6 +151,11 @@ struct Walker {
     uint32_t c1, c2, c3, k1;   // NATIVE counters / key
     int32_t seg_off, n_seg, rec_off;
     int32_t seg_i;  // polygon: nearest segment found by the last distance query
+    // single-instance NATIVE launches: the Philox round keys and the parameters the
+    // jump reads, copied once from the constant bank through a shuffle so that ptxas
+    // keeps them in (uniform) registers instead of reloading them every step
+    uint32_t hk0[kHotK], hk1[kHotK];
+    float hc[kHotC];
   };
 
   // instance parameters: constant bank (ONE) or the staged shared-memory row
@@ -146,7 +164,8 @@ struct Walker {
     else return l.row;
   }
   __device__ static __forceinline__ Real domp(const Lane& l, const KArgs& a, int i) {
-    if constexpr (ONE) return (Real)a.cp[kDomOff + i];
+    if constexpr (kHot) return l.hc[kDomOff + i];  // i is a compile-time constant here
+    else if constexpr (ONE) return (Real)a.cp[kDomOff + i];
     else return l.row[kDomOff + i];
   }
 
@@ -471,7 +490,9 @@ struct Walker {
   }
 
   __device__ static __forceinline__ Real source(const Lane& l, const KArgs& a, const Real* y) {
-    const Real* P = prow(l, a) + kSrcOff;
+    const Real* P;
+    if constexpr (kHotSrc) P = l.hc + kSrcOff;
+    else P = prow(l, a) + kSrcOff;
     if constexpr (S::SRC == SRC_CONST) {
       return P[0];
     } else if constexpr (S::SRC == SRC_RBF2) {
@@ -666,7 +687,7 @@ struct Walker {
 
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
     const uint4 c = make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3);
-    if constexpr (ONE) return philox4x32_rk(c, a.rk0, a.rk1);
+    if constexpr (ONE) return philox4x32_rk(c, l.hk0, l.hk1);
     else return philox4x32(c, a.nkey0, l.k1);
   }
 
@@ -874,6 +895,24 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   int cu_inst = 0;
 
   typename W::Lane l;
+  if constexpr (W::kHot) {
+    // Philox round keys and the jump's parameters go constant bank -> shared memory
+    // (warp 0's ring, not yet in use) -> shuffle: loop-invariant registers that ptxas
+    // cannot re-derive from the constant bank, so it keeps them in uniform registers
+    // instead of re-issuing the constant loads every step
+    uint32_t* hs = reinterpret_cast<uint32_t*>(smem + a.stage_bytes + a.seg_stage_bytes);
+    for (int i = threadIdx.x; i < 20 + W::kHotC; i += blockDim.x)
+      hs[i] = i < 10 ? a.rk0[i] : i < 20 ? a.rk1[i - 10] : __float_as_uint(a.cp[i - 20]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      l.hk0[r] = __shfl_sync(WOS_FULL, hs[r], 0);
+      l.hk1[r] = __shfl_sync(WOS_FULL, hs[10 + r], 0);
+    }
+#pragma unroll
+    for (int i = 0; i < W::kHotC; ++i) l.hc[i] = __uint_as_float(__shfl_sync(WOS_FULL, hs[20 + i], 0));
+    __syncthreads();
+  }
   bool active = false;
   uint32_t blk = 0;          // this lane's unit (stream index)
   unsigned idle = WOS_FULL;  // warp-uniform: lanes without a walk
