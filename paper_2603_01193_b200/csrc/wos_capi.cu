@@ -662,6 +662,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
       // instance row and Philox4x32 round keys ride in the kernel parameters
       a.stage_bytes = 0;
       memcpy(a.cp, s->h_row_n.data(), sizeof(float) * s->stride);
+      a.bnd_c = s->h_row_n[s->bnd_off];
       const uint32_t k0 = (uint32_t)cfg->rng_seed;
       const uint32_t k1 = (uint32_t)(cfg->rng_seed >> 32) ^ s->h_nkey1;
       for (int r = 0; r < 10; ++r) {

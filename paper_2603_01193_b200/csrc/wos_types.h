@@ -68,6 +68,7 @@ struct KArgs {
   int32_t bnd_kind;
   int32_t bnd_M;        // Fourier / arc-length order (uniform over the set; padded)
   int32_t refill_min;   // refill idle lanes once this many are idle
+  float bnd_c;          // single-instance NATIVE launches: the BND_CONST boundary value
   // ---- walk config ----
   double eps;
   float eps_f;          // eps rounded to fp32 (NATIVE / REPLAY_F32 compare in fp32)

@@ -127,7 +127,8 @@ struct Walker {
   static constexpr int DIM = S::DIM;
   static constexpr bool ONE = S::ONE;
 
-  static constexpr bool kHot = S::NATIVE && ONE;
+  // (not for polygons, whose segment scan needs the registers, nor for the ROWS sink)
+  static constexpr bool kHot = S::NATIVE && ONE && S::DOM != DOM_POLY && S::SINK == SINK_ESTIMATE;
   static constexpr int kHotK = kHot ? 10 : 1;
   // hot source coefficients: those the jump reads at compile-time offsets
   static constexpr int kHotSrcN =
@@ -146,7 +147,7 @@ struct Walker {
     Real sgn;
     const Real* row;  // this walk's instance row in the staged table (shared memory)
     int step;
-    uint32_t seq;
+    uint32_t seq;  // ESTIMATE: byte offset of the walk's ring slot; ROWS: row index
     uint64_t pid, tid, ikey;   // REPLAY counters / key
     uint32_t c1, c2, c3, k1;   // NATIVE counters / key
     int32_t seg_off, n_seg, rec_off;
@@ -616,6 +617,9 @@ struct Walker {
 
   // value at termination: acc + g(projection); constant g needs no projection
   __device__ static __forceinline__ Real finish_value(const Lane& l, const KArgs& a) {
+    if constexpr (ONE) {
+      if (a.bnd_kind == BND_CONST) return l.acc + a.bnd_c;
+    }
     if (a.bnd_kind == BND_CONST) return l.acc + prow(l, a)[a.bnd_off];
     Real q[DIM];
     project(l, a, q);
@@ -687,7 +691,8 @@ struct Walker {
 
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
     const uint4 c = make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3);
-    if constexpr (ONE) return philox4x32_rk(c, l.hk0, l.hk1);
+    if constexpr (kHot) return philox4x32_rk(c, l.hk0, l.hk1);
+    else if constexpr (ONE) return philox4x32_rk(c, a.rk0, a.rk1);
     else return philox4x32(c, a.nkey0, l.k1);
   }
 
@@ -743,6 +748,19 @@ struct Walker {
   }
 
   // ---------------- walk start ----------------
+  // single-instance NATIVE start from precomputed counter words (same state as start)
+  __device__ static __forceinline__ void start_native(Lane& l, const float* x0, float sgn,
+                                                      uint32_t c1, uint32_t c2, uint32_t c3) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) l.x[i] = x0[i];
+    l.acc = 0.0f;
+    l.sgn = sgn;
+    l.step = 0;
+    l.c1 = c1;
+    l.c2 = c2;
+    l.c3 = c3;
+  }
+
   template <class X>
   __device__ static __forceinline__ void start(Lane& l, const Real* table, const InstHdr* hdr,
                                                const KArgs& a, const X* x0, int inst,
@@ -893,6 +911,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   for (int i = 0; i < DIM; ++i) cu_x[i] = Real(0);
   uint64_t cu_pid = 0;
   int cu_inst = 0;
+  // single-instance NATIVE: Philox counter words of the cached unit's walk 0; walk
+  // j0 + jj has c2 = cu_c2b + jj while cu_fastc (no 32-bit carry inside the unit)
+  uint32_t cu_c1 = 0, cu_c2b = 0, cu_c3 = 0;
+  bool cu_fastc = false;
 
   typename W::Lane l;
   if constexpr (W::kHot) {
@@ -914,7 +936,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     __syncthreads();
   }
   bool active = false;
-  uint32_t blk = 0;          // this lane's unit (stream index)
+  uint32_t blk = 0;          // byte offset of this lane's unit counter in cnt (ESTIMATE)
   unsigned idle = WOS_FULL;  // warp-uniform: lanes without a walk
   unsigned long long lane_steps = 0ull;
   uint32_t refills = 0;
@@ -1001,8 +1023,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       if (fin) {  // record: walker.py:275-281, value = acc + g(projection)
         const Real v = W::finish_value(l, a);
         lane_steps += (unsigned long long)l.step;
-        ring[l.seq % kRing] = v;
-        atomicAdd(&cnt[blk % kSlots], 1u);
+        *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = v;
+        atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
         active = false;
       }
       const uint32_t n_idle = (uint32_t)__popc(idle);
@@ -1058,15 +1080,15 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         if (rank < n) {
           const uint32_t seq = s_issue + rank;
           const uint32_t j = cu_j0 + (seq - (cu_end - IU));
-          blk = cu_k;
+          blk = (cu_k % kSlots) * 4u;
           if (j < cu_jend) {
             const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
             const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
             W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
-            l.seq = seq;
+            l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
             active = true;
           } else {  // null item padding the point's last chunk: complete at once
-            atomicAdd(&cnt[blk % kSlots], 1u);
+            atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
           }
         }
       }
@@ -1123,6 +1145,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
               cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
               cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+              if constexpr (S::NATIVE && S::ONE) {
+                // walk j0 + jj has tid = traj_start + j0 + jj (antithetic: jj even; j0 even)
+                const uint64_t tid0 = a.traj_start + cu_j0;
+                cu_c1 = (uint32_t)cu_pid;
+                cu_c2b = (uint32_t)tid0;
+                cu_c3 = (uint32_t)(tid0 >> 32) ^ ((uint32_t)(cu_pid >> 32) * 0x85EBCA6Bu);
+                cu_fastc = (uint64_t)(uint32_t)tid0 + (cu_jend - cu_j0) <= 0x100000000ull;
+              }
               room = IU;
             } else if (n_idle == 32 && exhausted && r_seq == s_issue) {
               break;  // no walk left, none running, all retired
@@ -1134,16 +1164,27 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint32_t rank = __popc(idle & lanemask_lt());
           if (rank < n) {
             const uint32_t seq = s_issue + rank;
-            const uint32_t j = cu_j0 + (seq - (cu_end - IU));
-            blk = cu_k;
+            const uint32_t jr = seq - (cu_end - IU);
+            const uint32_t j = cu_j0 + jr;
+            blk = (cu_k % kSlots) * 4u;
             if (j < cu_jend) {
-              const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
-              const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
-              W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
-              l.seq = seq;
+              bool started = false;
+              if constexpr (S::NATIVE && S::ONE) {
+                if (cu_fastc) {
+                  W::start_native(l, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
+                                  cu_c2b + (anti ? (jr & ~1u) : jr), cu_c3);
+                  started = true;
+                }
+              }
+              if (!started) {
+                const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+                const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
+                W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
+              }
+              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
               active = true;
             } else {  // null item padding the point's last chunk: complete at once
-              atomicAdd(&cnt[blk % kSlots], 1u);
+              atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
             }
           }
         }
@@ -1185,17 +1226,17 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             const uint32_t pl = fast_div(r, a.l_mul, a.l_shr);
             const uint32_t j = r - pl * L;
             const uint64_t p = (uint64_t)unit * U + pl;
-            blk = k;
+            blk = (k % kSlots) * 4u;
             if (p < a.n_points) {
               const int inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
               const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
               const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
               W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
                        a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p, tid, sg);
-              l.seq = seq;
+              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
               active = true;
             } else {  // null item padding the last unit: complete at once
-              atomicAdd(&cnt[blk % kSlots], 1u);
+              atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
             }
           } else {
             const uint64_t row = (uint64_t)unit * IU + r;
@@ -1219,8 +1260,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const Real v = W::finish_value(l, a);
         lane_steps += (unsigned long long)l.step;
         if constexpr (est) {
-          ring[l.seq % kRing] = v;
-          atomicAdd(&cnt[blk % kSlots], 1u);
+          *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = v;
+          atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
         } else {
           a.out_values[l.seq] = (double)v;
           a.out_steps[l.seq] = (int64_t)l.step;
