@@ -61,6 +61,8 @@ __device__ __forceinline__ float fast_ex2(float x) {
 }
 // (w >> 9) | 1.0f  ->  [1, 2); u = f - 1 = (w >> 9) 2^-23 exactly (one LEA.HI)
 __device__ __forceinline__ float f12(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)); }
+// the same 23 bits with exponent 2^1: 2 f exactly, so z = 2u - 1 = f2(w) - 3 takes one FADD
+__device__ __forceinline__ float f2x(uint32_t w) { return __uint_as_float(0x40000000u | (w >> 9)); }
 
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
@@ -714,7 +716,7 @@ struct Walker {
       l.x[0] = fmaf(sd, cth, l.x[0]);
       l.x[1] = fmaf(sd, sth, l.x[1]);
     } else if constexpr (S::SRC == SRC_NONE) {
-      const float z = fmaf(2.0f, f12(A.x), -3.0f);
+      const float z = f2x(A.x) - 3.0f;
       const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
       __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
@@ -726,11 +728,11 @@ struct Walker {
       float u[7];
       native_uniforms7(A, u);
       // z = 2u - 1 is exact for u = f - 1 (23-bit f in [1, 2)), so fmaf(-z, z, 1) >= 0
-      const float z = fmaf(2.0f, u[0], -3.0f);
+      const float z = f2x(A.x) - 3.0f;
       const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
       __sincosf(fmaf(u[1], kTwoPiF, -kTwoPiF), &sph, &cph);
-      const float vz = fmaf(2.0f, u[2], -3.0f);
+      const float vz = f2x(A.z) - 3.0f;
       const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
       float vsp, vcp;
       __sincosf(fmaf(u[3], kTwoPiF, -kTwoPiF), &vsp, &vcp);
