@@ -224,6 +224,38 @@ int wos_estimate_host(wos_context* ctx, const wos_problem_set* set,
  * wos_estimate / wos_estimate_host since the last call (-1 if none), resetting it. */
 int wos_context_exterior(wos_context* ctx, void* stream, int64_t* out_first_exterior);
 
+/* ---- epoch-averaged estimate cache (estimator.EstimateCache) -----------
+ * replaces                                                      by
+ *   EstimateCache.update / cache_update (estimator.py:217-244, 338-341)  wos_cache_fold
+ *   EstimateCache.targets              (estimator.py:251-255)       wos_cache_targets
+ *   training-label epoch: estimate(traj_start = epoch L) + cache_update
+ *                                      (surrogate.py:288-298)       wos_estimate_fold
+ * The cache is caller-owned device state over the frozen, sorted key set
+ * (estimator.py:206-215): mean_sum, mean, m2 fp64 [n_keys], n int64 [n_keys].
+ * Folding fresh estimate k into entry slot[k] (k itself if slot is NULL) does
+ *   mean_sum += mean_k;  (n, mean, m2) <- chan_merge((n, mean, m2), (n_k, mean_k, m2_k))
+ * in fp64 with the reference's operation order (estimator.py:41-53), so targets are
+ * bit-identical to the reference cache fed the same estimates. n_k comes from
+ * fresh_n [n_fresh] int64 (device) or, if fresh_n is NULL, fresh_n_all. Slots must
+ * be distinct within one call. Device pointers, ordered on `stream`. */
+int wos_cache_fold(wos_context* ctx, int64_t n_fresh, const int64_t* slot,
+                   const double* fresh_mean, const double* fresh_m2, const int64_t* fresh_n,
+                   int64_t fresh_n_all, double* mean_sum, int64_t* n, double* mean, double* m2,
+                   void* stream);
+
+/* out[k] = mean_sum[k] / epoch (epoch >= 1). */
+int wos_cache_targets(wos_context* ctx, int64_t n_keys, const double* mean_sum, int64_t epoch,
+                      double* out, void* stream);
+
+/* One training-label epoch on the device: wos_estimate of the points (arguments as
+ * there) folded straight into the cache entries slot[p] (NULL: p) with n = L (L/2
+ * antithetic); the epoch's estimates never leave the device. */
+int wos_estimate_fold(wos_context* ctx, const wos_problem_set* set, const wos_walk_config* cfg,
+                      int64_t n_points, const double* points, const int64_t* point_ids,
+                      const int32_t* inst_index, int64_t L, uint64_t traj_start,
+                      const int64_t* slot, double* mean_sum, int64_t* n, double* mean,
+                      double* m2, uint64_t* out_total_steps, void* stream);
+
 /* ---- counter-based generators (known-answer tests) --------------------
  * Device pointers; ctr/out are [n, 4] words. */
 int wos_philox4x64(wos_context* ctx, int64_t n, const uint64_t* ctr, uint64_t key0,

@@ -2,11 +2,13 @@
 
 Drop-in for the reference package ``spherewalk``'s estimator path:
 ``WalkConfig``, ``Problem``, ``walk_poisson_values``, ``walk_poisson``,
-``walk_poisson_antithetic``, ``estimate``, ``PointEstimate`` — backed by
+``walk_poisson_antithetic``, ``estimate``, ``PointEstimate``, and the
+epoch-averaged ``EstimateCache`` of the training-label loop — backed by
 hand-written sm_100a CUDA kernels in ``libwos_b200.so`` behind the C ABI of
 ``include/wos_b200.h``. There is no CPU fallback.
 """
 
+from .cache import CacheShapeError, EstimateCache, cache_update, export_csv
 from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, estimate_tensors
 from .engine import UnsupportedProblemError
 from .geometry import BallDomain, BoxDomain, ExteriorQueryError, PolygonDomain, star_polygon
@@ -26,6 +28,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BallDomain",
+    "CacheShapeError",
+    "EstimateCache",
     "BoxDomain",
     "ExteriorQueryError",
     "PointEstimate",
@@ -37,10 +41,12 @@ __all__ = [
     "TrajectoryStream",
     "UnsupportedProblemError",
     "WalkConfig",
+    "cache_update",
     "chan_merge",
     "estimate",
     "estimate_arrays",
     "estimate_tensors",
+    "export_csv",
     "star_polygon",
     "walk_poisson",
     "walk_poisson_antithetic",

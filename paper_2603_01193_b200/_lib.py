@@ -106,6 +106,16 @@ _SIGNATURES = {
         [_P, _P, POINTER(WosWalkConfig), c_int64, _P, _P, _P, c_int64, c_uint64, _P, _P, _P],
     ),
     "wos_context_exterior": (c_int32, [_P, _P, POINTER(c_int64)]),
+    "wos_cache_fold": (
+        c_int32,
+        [_P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P],
+    ),
+    "wos_cache_targets": (c_int32, [_P, c_int64, _P, c_int64, _P, _P]),
+    "wos_estimate_fold": (
+        c_int32,
+        [_P, _P, POINTER(WosWalkConfig), c_int64, _P, _P, _P, c_int64, c_uint64, _P, _P, _P,
+         _P, _P, _P, _P],
+    ),
     "wos_philox4x64": (c_int32, [_P, c_int64, _P, c_uint64, c_uint64, _P, _P]),
     "wos_philox4x32": (c_int32, [_P, c_int64, _P, c_uint32, c_uint32, _P, _P]),
     "wos_set_tuning": (c_int32, [_P, c_int32, c_int32]),

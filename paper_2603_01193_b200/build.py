@@ -34,6 +34,7 @@ UNITS = {
     "wos_kernels_native_rows.cu": [],
     "wos_kernels_replay_f64.cu": ["--fmad=false"],
     "wos_kernels_replay_f32.cu": ["--fmad=false"],
+    "wos_cache.cu": ["--fmad=false"],
 }
 HEADERS = ["wos_types.h", "wos_rng.cuh", "wos_walk.cuh", "wos_kernels.h", "wos_kernels_native.inc"]
 

@@ -87,6 +87,15 @@ struct wos_problem_set {
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
 
+int wos_fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int wos_context_device(const wos_context* c) { return c->device; }
+
 extern "C" int wos_abi_version(void) { return WOS_ABI_VERSION; }
 extern "C" const char* wos_last_error(void) { return g_err; }
 
@@ -854,6 +863,29 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
                             void* stream) {
   return estimate_impl(c, s, cfg, P, points, point_ids, inst_index, L, traj_start, out_mean, out_m2,
                        out_total_steps, (cudaStream_t)stream, 0);
+}
+
+extern "C" int wos_estimate_fold(wos_context* c, const wos_problem_set* s,
+                                 const wos_walk_config* cfg, int64_t P, const double* points,
+                                 const int64_t* point_ids, const int32_t* inst_index, int64_t L,
+                                 uint64_t traj_start, const int64_t* slot, double* mean_sum,
+                                 int64_t* n, double* mean, double* m2, uint64_t* out_total_steps,
+                                 void* stream) {
+  if (!c || !cfg) return fail(WOS_ERR_INVALID, "wos_estimate_fold: null argument");
+  if (P < 0) return fail(WOS_ERR_INVALID, "wos_estimate_fold: negative point count");
+  if (P == 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  // the epoch's fresh (mean, m2) live only in stream-ordered scratch
+  double* fresh = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&fresh, 2 * (size_t)P * sizeof(double), st));
+  int r = estimate_impl(c, s, cfg, P, points, point_ids, inst_index, L, traj_start, fresh,
+                        fresh + P, out_total_steps, st, 0);
+  if (r == WOS_OK)
+    r = wos_cache_fold(c, P, slot, fresh, fresh + P, nullptr, cfg->antithetic ? L / 2 : L,
+                       mean_sum, n, mean, m2, stream);
+  cudaFreeAsync(fresh, st);
+  return r;
 }
 
 // ---- host-buffer variants ------------------------------------------------

@@ -9,3 +9,8 @@ const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows);
 // one = single-instance launch (instance row + Philox keys in the kernel parameters)
 const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows);
 }  // namespace wos
+
+// host helpers shared by the C-ABI units (defined in wos_capi.cu)
+struct wos_context;
+int wos_fail(int code, const char* fmt, ...);     // sets wos_last_error(), returns code
+int wos_context_device(const wos_context* ctx);  // CUDA device ordinal of ctx

@@ -22,6 +22,7 @@ __all__ = [
     "Context",
     "ProblemSet",
     "get_context",
+    "problem_set",
     "mode_code",
 ]
 
@@ -197,6 +198,29 @@ class ProblemSet:
             self.close()
         except Exception:
             pass
+
+
+_pset_lock = threading.Lock()
+_psets: "dict[tuple, ProblemSet]" = {}
+_PSET_CACHE_MAX = 64
+
+
+def problem_set(ctx: Context, problems) -> ProblemSet:
+    """Device problem set for ``problems``, reused across calls with the same specs.
+
+    Keyed by the problems' spec records (and the context), so a training loop that
+    estimates the same instance every epoch uploads its table once.
+    """
+    recs = tuple(problem_record(p) for p in problems)
+    key = (id(ctx), recs)
+    with _pset_lock:
+        ps = _psets.get(key)
+        if ps is None:
+            if len(_psets) >= _PSET_CACHE_MAX:
+                _psets.pop(next(iter(_psets))).close()
+            ps = ProblemSet(ctx, problems)
+            _psets[key] = ps
+        return ps
 
 
 def walk_config_struct(eps: float, max_steps: int, antithetic: bool, mode, seed: int):

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .engine import ProblemSet, get_context, raise_exterior, walk_config_struct
+from .engine import get_context, problem_set, raise_exterior, walk_config_struct
 from .geometry import ExteriorQueryError
 
 __all__ = [
@@ -84,7 +84,7 @@ def _validate_counts(L, antithetic):
 
 def _estimate_one_device(device, problems, pts, pids, inst, L, cfg, eps, traj_start):
     ctx = get_context(device)
-    pset = ProblemSet(ctx, problems)
+    pset = problem_set(ctx, problems)
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
     P = pts.shape[0]
@@ -139,7 +139,7 @@ def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None
     if L < 1 or (cfg.antithetic and L % 2):
         # the reference checks the interior first (estimator.py:156-163)
         ctx = get_context()
-        pset = ProblemSet(ctx, problems)
+        pset = problem_set(ctx, problems)
         first = c_int64(-1)
         _lib.check(ctx._lib.wos_check_interior_host(
             ctx.handle, pset.handle, P, pts.ctypes.data, None if inst is None else inst.ctypes.data,

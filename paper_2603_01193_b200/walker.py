@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _lib
 from .engine import (
-    ProblemSet,
+    problem_set,
     UnsupportedProblemError,
     get_context,
     mode_code,
@@ -135,7 +135,7 @@ def walk_poisson_values(inst, points, point_ids, traj_ids, signs, cfg):
     n = pts.shape[0]
     pid, tid, sgn = _streams_as_arrays(point_ids, traj_ids, signs, n)
     ctx = get_context()
-    pset = ProblemSet(ctx, [inst])
+    pset = problem_set(ctx, [inst])
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
     wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode, cfg.rng_seed)
@@ -156,7 +156,7 @@ def walk_poisson_values(inst, points, point_ids, traj_ids, signs, cfg):
 def _require_interior(inst, xi):
     """walker.py:426-428, evaluated on the GPU (wos_check_interior)."""
     ctx = get_context()
-    pset = ProblemSet(ctx, [inst])
+    pset = problem_set(ctx, [inst])
     pts = np.ascontiguousarray(np.asarray(xi, dtype=np.float64).reshape(1, -1))
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected a point of dimension {pset.dim}")
