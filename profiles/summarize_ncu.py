@@ -21,6 +21,8 @@ KEYS = [
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe % of peak"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % of peak"),
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe % of peak"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "FMA-heavy pipe cycles % (elapsed)"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "ALU pipe cycles % (elapsed)"),
     ("dram__bytes_read.sum", "DRAM bytes read"),
     ("dram__bytes_write.sum", "DRAM bytes written"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
