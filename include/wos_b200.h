@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define WOS_ABI_VERSION 1
+#define WOS_ABI_VERSION 2
 
 /* ---- status codes ---------------------------------------------------- */
 typedef enum wos_status {
@@ -50,7 +50,8 @@ typedef enum wos_status {
   WOS_ERR_UNSUPPORTED = 2, /* domain/source/boundary kind not GPU-codeable       */
   WOS_ERR_CUDA = 3,        /* CUDA runtime error                                 */
   WOS_ERR_EXTERIOR = 4,    /* a start point lies outside the domain              */
-  WOS_ERR_NOMEM = 5
+  WOS_ERR_NOMEM = 5,
+  WOS_ERR_MAJORANT = 6     /* delta tracking: sigma' exceeded sigma_bar (walker.py:51-52) */
 } wos_status;
 
 /* ---- numeric modes --------------------------------------------------- */
@@ -101,8 +102,27 @@ enum {
   WOS_SRC_CONST = 1,
   WOS_SRC_RBF2 = 2,
   WOS_SRC_SINE = 3,
-  WOS_SRC_GAUSS = 4
+  WOS_SRC_GAUSS = 4,
+  WOS_SRC_SCREENED_CONST = 5,
+  WOS_SRC_SCREENED_VC = 6
 };
+
+/* ---- delta tracking (walker.ScreenedProblem, walker.py:120-136, 322-418) ----
+ * A screened problem is walked by delta tracking with the majorant
+ * wos_walk_config.sigma_bar: each step exits to the sphere with probability
+ * q / sinh q (q = sqrt(sigma_bar) d) or lands at a volume event drawn from the
+ * screened Green's function, where the source deposits thr f'/sigma_bar and the
+ * throughput thr picks up 1 - sigma'/sigma_bar (greens.py:100-193,
+ * _kernels.py:476-558). The value is (acc + thr g'(exit)) / sqrt_alpha(start).
+ * 3D ball or box domains. REPLAY_F64 follows the reference's Philox4x64 layout
+ * (w0 event, w1/w2 direction, w3 radius; 64-step bisection of the radial CDF);
+ * NATIVE_F32 uses one Philox4x32 block per step and Newton for the radial CDF.
+ * WOS_SRC_SCREENED_CONST  [s', f', has_f' (0/1), sqrt_alpha], boundary WOS_BND_CONST [g']
+ *                         = ScreenedProblem.const_coeffs (_kernels.walk_screened_ball3;
+ *                         a walk whose throughput reaches 0 with has_f' = 0 stops, hit = 1)
+ * WOS_SRC_SCREENED_VC     [phi, a_min, a_max], boundary WOS_BND_VC [phi]: the paper's
+ *                         varying-coefficient family pde.VcInstance (pde.py:138-243):
+ *                         sigma', f', g' = sqrt(alpha) u and sqrt(alpha) in closed form */
 
 /* ---- boundary kinds (g evaluated at the projected exit point) -------- */
 /* WOS_BND_CONST          [c]                                (_kernels.BND_CONST)
@@ -116,14 +136,17 @@ enum {
  *                        length of q from corner (x0, y0) of the square
  *                        [x0, x0+side] x [y0, y0+side], g = sum_m c_m sin(2 pi m s / (4 side))
  * WOS_BND_QUADRATIC      2D: [axx, ayy, axy, ax, ay, a0],
- *                        g = axx x^2 + ayy y^2 + axy x y + ax x + ay y + a0         */
+ *                        g = axx x^2 + ayy y^2 + axy x y + ax x + ay y + a0
+ * WOS_BND_VC             3D: [phi], g' = sqrt(alpha) u of the varying-coefficient
+ *                        family (pde.py:197-199); only with WOS_SRC_SCREENED_VC    */
 enum {
   WOS_BND_CONST = 0,
   WOS_BND_FOURIER5 = 1,
   WOS_BND_LINEAR = 2,
   WOS_BND_FOURIER = 3,
   WOS_BND_SQUARE_ARCSINE = 4,
-  WOS_BND_QUADRATIC = 5
+  WOS_BND_QUADRATIC = 5,
+  WOS_BND_VC = 6
 };
 
 /* One PDE instance: a walker.Problem (walker.py:102-116) reduced to its
@@ -150,6 +173,7 @@ typedef struct wos_walk_config {
   int32_t antithetic;  /* estimate only: mirrored pairs share a traj id */
   int32_t mode;        /* wos_mode */
   uint64_t rng_seed;   /* first Philox key word */
+  double sigma_bar;    /* delta tracking majorant (WalkConfig.sigma_bar); ignored otherwise */
 } wos_walk_config;
 
 typedef struct wos_context wos_context;         /* per-device scratch + streams */
@@ -219,6 +243,11 @@ int wos_estimate_host(wos_context* ctx, const wos_problem_set* set,
                       const int64_t* point_ids, const int32_t* inst_index, int64_t L,
                       uint64_t traj_start, double* out_mean, double* out_m2,
                       uint64_t* out_total_steps);
+
+/* Synchronizes `stream` and returns (then resets) the largest sigma' above sigma_bar
+ * met by a delta-tracking volume event since the last call, or -1 if none. The
+ * *_host entry points report it themselves as WOS_ERR_MAJORANT. */
+int wos_context_majorant(wos_context* ctx, void* stream, double* out_worst_sigma_prime);
 
 /* Synchronizes `stream` and returns the first exterior point index seen by
  * wos_estimate / wos_estimate_host since the last call (-1 if none), resetting it. */

@@ -65,6 +65,8 @@ def load():
         L.oracle_philox4x32.argtypes = [c_int64, P, c_uint32, c_uint32, P]
         L.oracle_contains.argtypes = [P, P]
         L.oracle_contains.restype = c_int
+        L.oracle_set_sigma_bar.argtypes = [c_double]
+        L.oracle_majorant.restype = c_double
         _lib = L
     return _lib
 
@@ -110,9 +112,14 @@ def default_threads():
 
 
 def walk_rows(problem, points, point_ids, traj_ids, signs, *, seed, eps, max_steps, native=False,
-              nthreads=None):
-    """(values, steps, hits) like walker.walk_poisson_values (reference form by default)."""
+              nthreads=None, sigma_bar=0.0):
+    """(values, steps, hits) like walker.walk_poisson_values (reference form by default).
+
+    Screened problems walk by delta tracking with majorant ``sigma_bar``
+    (walker.walk_screened_values); ``majorant()`` then reports a violation.
+    """
     lib = load()
+    lib.oracle_set_sigma_bar(float(sigma_bar))
     pr = _Problems([problem])
     pts = np.ascontiguousarray(np.asarray(points, np.float64))
     n = pts.shape[0]
@@ -130,9 +137,10 @@ def walk_rows(problem, points, point_ids, traj_ids, signs, *, seed, eps, max_ste
 
 
 def estimate(problems, points, L, *, seed, eps, max_steps, point_ids=None, inst_index=None,
-             traj_start=0, antithetic=False, native=False, nthreads=None):
+             traj_start=0, antithetic=False, native=False, nthreads=None, sigma_bar=0.0):
     """(mean, m2, total_steps) like estimator.estimate (two-pass moments per point)."""
     lib = load()
+    lib.oracle_set_sigma_bar(float(sigma_bar))
     if not isinstance(problems, (list, tuple)) or (isinstance(problems, tuple) and len(problems) == 8
                                                    and isinstance(problems[0], int)):
         problems = [problems]
@@ -151,6 +159,11 @@ def estimate(problems, points, L, *, seed, eps, max_steps, point_ids=None, inst_
                         mean.ctypes.data, m2.ctypes.data, ctypes.addressof(tot),
                         int(nthreads or default_threads()))
     return mean, m2, tot.value
+
+
+def majorant():
+    """Largest sigma' above sigma_bar met by the last screened call, or -1."""
+    return float(load().oracle_majorant())
 
 
 def contains(problem, points):

@@ -264,11 +264,177 @@ static double boundary(const wos_problem* pb, const double* q) {
 }
 
 /* ------------------------------------------------------------------ */
+/* Delta tracking (walker.py:322-418, _kernels.py:476-558,             */
+/* greens.py:100-193, pde.py:138-213)                                  */
+/* ------------------------------------------------------------------ */
+void oracle_native_keys(uint64_t seed, uint64_t ikey, uint32_t* k0, uint32_t* k1);
+#define oracle_native_keys_fwd oracle_native_keys
+static double u23(uint32_t w);
+static double g_sigma_bar = 0.0; /* WalkConfig.sigma_bar for the screened walks */
+static double g_majorant = -1.0; /* worst sigma' > sigma_bar met (walker.py:409-413) */
+static pthread_mutex_t g_mu = PTHREAD_MUTEX_INITIALIZER;
+
+void oracle_set_sigma_bar(double s) {
+  g_sigma_bar = s;
+  g_majorant = -1.0;
+}
+double oracle_majorant(void) { return g_majorant; }
+
+/* pde._vc_log_alpha (pde.py:138-151): h, grad h, lap h with a = 4 pi phi, b = 3 pi phi */
+static void vc_log_alpha(double phi, const double* x, double* h, double* g, double* lap) {
+  const double a = 4.0 * PI * phi, b = 3.0 * PI * phi;
+  const double ca = cos(a * x[0]), sa = sin(a * x[0]), cb = cos(b * x[1]), sb = sin(b * x[1]);
+  *h = -x[1] * x[1] + ca * sb;
+  g[0] = -a * sa * sb;
+  g[1] = -2.0 * x[1] + b * ca * cb;
+  g[2] = 0.0;
+  *lap = -2.0 - (a * a + b * b) * ca * sb;
+}
+/* pde._vc_solution (pde.py:154-173) */
+static void vc_solution(double phi, const double* x, double* u, double* gu, double* lu) {
+  const double p = PI * phi;
+  const double s1 = sin(p * x[0]), c1 = cos(p * x[0]);
+  const double s2 = sin(2.0 * p * x[1]), c2 = cos(2.0 * p * x[1]);
+  const double s3 = sin(3.0 * p * x[2]);
+  *u = s1 * c2 + (1.0 - c1) * (1.0 - s2) + s3 * s3;
+  if (gu) {
+    gu[0] = p * c1 * c2 + p * s1 * (1.0 - s2);
+    gu[1] = -2.0 * p * s1 * s2 - 2.0 * p * (1.0 - c1) * c2;
+    gu[2] = 3.0 * p * sin(6.0 * p * x[2]);
+    *lu = -p * p * s1 * c2 + p * p * c1 * (1.0 - s2) - 4.0 * p * p * s1 * c2 +
+          4.0 * p * p * (1.0 - c1) * s2 + 18.0 * p * p * cos(6.0 * p * x[2]);
+  }
+}
+/* pde._vc_sigma, _vc_sigma_prime, _vc_source(_prime), _vc_sqrt_alpha (pde.py:176-212) */
+static void vc_coeffs(const double* P, const double* y, double* sp, double* fp) {
+  double h, gh[3], lh, u, gu[3], lu;
+  vc_log_alpha(P[0], y, &h, gh, &lh);
+  const double sigma =
+      P[1] + (P[2] - P[1]) * (1.0 + 0.5 * sin(2.0 * PI * y[0]) * cos(0.5 * PI * y[1]));
+  *sp = sigma * exp(-h) + 0.5 * lh + 0.25 * (gh[0] * gh[0] + gh[1] * gh[1] + gh[2] * gh[2]);
+  vc_solution(P[0], y, &u, gu, &lu);
+  const double alpha = exp(h);
+  const double f = -alpha * lu - alpha * (gh[0] * gu[0] + gh[1] * gu[1] + gh[2] * gu[2]) + sigma * u;
+  *fp = f / exp(0.5 * h);
+}
+static double vc_solution_u(double phi, const double* x) {
+  double u;
+  vc_solution(phi, x, &u, NULL, NULL);
+  return u;
+}
+static double vc_sqrt_alpha(double phi, const double* x) {
+  double h, g[3], lap;
+  vc_log_alpha(phi, x, &h, g, &lap);
+  return exp(0.5 * h);
+}
+/* greens.radial_event_cdf / _kernels._radial_cdf */
+static double radial_cdf(double q, double t) {
+  if (q < 1.0e-4) return t * t * (3.0 - 2.0 * t);
+  return (sinh(q) - q * t * cosh(q * (1.0 - t)) - sinh(q * (1.0 - t))) / (sinh(q) - q);
+}
+/* greens.invert_radial_event_cdf: fixed 64-step bisection */
+static double invert_bisect(double q, double u) {
+  double lo = 0.0, hi = 1.0;
+  for (int it = 0; it < 64; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (radial_cdf(q, mid) < u) lo = mid;
+    else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+static void note_majorant(double sp) {
+  pthread_mutex_lock(&g_mu);
+  if (sp > g_majorant) g_majorant = sp;
+  pthread_mutex_unlock(&g_mu);
+}
+
+/* One delta-tracking walk. native = 0: the reference's Philox4x64 layout and the
+ * 64-step bisection; const coefficients follow _kernels.walk_screened_ball3 (early
+ * exit of a dead walk), the family follows walker._screened_generic. native = 1: the
+ * product's NATIVE layout (one Philox4x32 block: x event, y direction z, z direction
+ * phi, w radius) with the radial CDF inverted to convergence. */
+static void walk_screened_one(const wos_problem* pb, const double* x0, uint64_t pid,
+                              uint64_t tid, double sgn, uint64_t seed, double eps,
+                              int64_t max_steps, int native, double* value, int64_t* steps,
+                              uint8_t* hit) {
+  const double sigma_bar = g_sigma_bar, sqrt_sig = sqrt(sigma_bar);
+  const int vc = pb->src_kind == WOS_SRC_SCREENED_VC;
+  const double* P = pb->src;
+  const double sa0 = vc ? vc_sqrt_alpha(P[0], x0) : P[3];
+  double x[3] = {x0[0], x0[1], x0[2]}, q[3], acc = 0.0, thr = 1.0;
+  uint32_t k0n = 0, k1n = 0;
+  if (native) oracle_native_keys_fwd(seed, pb->instance_key, &k0n, &k1n);
+  const uint32_t c1 = (uint32_t)pid, c2 = (uint32_t)tid;
+  const uint32_t c3 = (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu);
+  for (int64_t step = 0;; ++step) {
+    const double d = query(pb, x, q);
+    const int shell = d < eps;
+    if (shell || step >= max_steps) {
+      const double g = vc ? vc_sqrt_alpha(P[0], q) * (vc_solution_u(P[0], q)) : pb->bnd[0];
+      *value = (acc + thr * g) / sa0;
+      *steps = step;
+      *hit = (uint8_t)shell;
+      return;
+    }
+    if (!vc && thr == 0.0 && P[2] == 0.0) { /* _kernels.py:533-538 */
+      *value = acc / sa0;
+      *steps = step;
+      *hit = 1;
+      return;
+    }
+    double qq = sqrt_sig * d;
+    if (qq > 500.0) qq = 500.0;
+    const double surf = qq < 1.0e-6 ? 1.0 - qq * qq / 6.0 : qq / sinh(qq);
+    double ue, uz, uphi, ur;
+    if (native) {
+      uint32_t ca[4] = {(uint32_t)(2 * step), c1, c2, c3}, u[4];
+      philox4x32(ca, k0n, k1n, u);
+      ue = u23(u[0]);
+      uz = u23(u[1]);
+      uphi = u23(u[2]);
+      ur = u23(u[3]) + 0x1p-24;
+    } else {
+      uint64_t c[4] = {2 * (uint64_t)step, pid, tid, 0}, w[4];
+      philox4x64(c, seed, pb->instance_key, w);
+      ue = u53(w[0]);
+      uz = u53(w[1]);
+      uphi = u53(w[2]);
+      ur = u53(w[3]);
+    }
+    const double z = 2.0 * uz - 1.0; /* walker._sphere_dirs_3d */
+    const double s = sqrt(fmax(0.0, 1.0 - z * z));
+    const double phi = TWO_PI * uphi;
+    const double dir[3] = {s * cos(phi), s * sin(phi), z};
+    const int vol = ue >= surf;
+    const double rad = vol ? d * invert_bisect(qq, ur) : d;
+    for (int i = 0; i < 3; ++i) x[i] += sgn * rad * dir[i];
+    if (vol) {
+      double sp, fp = 0.0;
+      int has_f = 1;
+      if (vc) {
+        vc_coeffs(P, x, &sp, &fp);
+      } else {
+        sp = P[0];
+        fp = P[1];
+        has_f = P[2] != 0.0;
+      }
+      if (sp > sigma_bar) note_majorant(sp);
+      if (has_f) acc += thr * fp / sigma_bar;
+      thr *= 1.0 - sp / sigma_bar;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
 /* One reference-form trajectory (walker.py:257-314)                   */
 /* ------------------------------------------------------------------ */
 static void walk_ref_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
                          double sgn, uint64_t seed, double eps, int64_t max_steps,
                          double* value, int64_t* steps, uint8_t* hit) {
+  if (pb->src_kind == WOS_SRC_SCREENED_CONST || pb->src_kind == WOS_SRC_SCREENED_VC) {
+    walk_screened_one(pb, x0, pid, tid, sgn, seed, eps, max_steps, 0, value, steps, hit);
+    return;
+  }
   const int dim = pb->dim;
   const int has_src = pb->src_kind != WOS_SRC_NONE;
   const uint64_t k0 = seed, k1 = pb->instance_key;
@@ -343,6 +509,10 @@ static double med3(double a, double b, double c) {
 static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
                             double sgn, uint64_t seed, double eps, int64_t max_steps,
                             double* value, int64_t* steps, uint8_t* hit) {
+  if (pb->src_kind == WOS_SRC_SCREENED_CONST || pb->src_kind == WOS_SRC_SCREENED_VC) {
+    walk_screened_one(pb, x0, pid, tid, sgn, seed, eps, max_steps, 1, value, steps, hit);
+    return;
+  }
   const int dim = pb->dim;
   const int has_src = pb->src_kind != WOS_SRC_NONE;
   uint32_t k0, k1;

@@ -13,6 +13,10 @@ from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, est
 from .engine import UnsupportedProblemError
 from .geometry import BallDomain, BoxDomain, ExteriorQueryError, PolygonDomain, star_polygon
 from .walker import (
+    MajorantViolationError,
+    ScreenedProblem,
+    walk_screened_delta,
+    walk_screened_values,
     TERM_BOUNDARY,
     TERM_MAX_STEPS,
     Problem,
@@ -32,9 +36,11 @@ __all__ = [
     "EstimateCache",
     "BoxDomain",
     "ExteriorQueryError",
+    "MajorantViolationError",
     "PointEstimate",
     "PolygonDomain",
     "Problem",
+    "ScreenedProblem",
     "TERM_BOUNDARY",
     "TERM_MAX_STEPS",
     "TrajectoryResult",
@@ -51,4 +57,6 @@ __all__ = [
     "walk_poisson",
     "walk_poisson_antithetic",
     "walk_poisson_values",
+    "walk_screened_delta",
+    "walk_screened_values",
 ]

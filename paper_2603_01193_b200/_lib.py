@@ -35,6 +35,8 @@ WOS_ERR_UNSUPPORTED = 2
 WOS_ERR_CUDA = 3
 WOS_ERR_EXTERIOR = 4
 WOS_ERR_NOMEM = 5
+WOS_ERR_MAJORANT = 6
+ABI_VERSION = 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("WOS_B200_LIB") or os.path.join(_HERE, "libwos_b200.so")
@@ -76,6 +78,7 @@ class WosWalkConfig(ctypes.Structure):
         ("antithetic", c_int32),
         ("mode", c_int32),
         ("rng_seed", c_uint64),
+        ("sigma_bar", c_double),
     ]
 
 
@@ -106,6 +109,7 @@ _SIGNATURES = {
         [_P, _P, POINTER(WosWalkConfig), c_int64, _P, _P, _P, c_int64, c_uint64, _P, _P, _P],
     ),
     "wos_context_exterior": (c_int32, [_P, _P, POINTER(c_int64)]),
+    "wos_context_majorant": (c_int32, [_P, _P, POINTER(c_double)]),
     "wos_cache_fold": (
         c_int32,
         [_P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P],
@@ -148,7 +152,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.wos_abi_version() != 1:
+        if handle.wos_abi_version() != ABI_VERSION:
             raise WosUnavailableError("libwos_b200.so ABI version mismatch")
         if path is None:
             _lib = handle

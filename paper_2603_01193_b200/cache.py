@@ -18,13 +18,21 @@ from __future__ import annotations
 
 import csv
 import struct
-from ctypes import byref, c_int64
+from ctypes import byref, c_double, c_int64
 
 import numpy as np
 
 from . import _lib
-from .engine import _stream_ptr, get_context, problem_set, raise_exterior, walk_config_struct
+from .engine import (
+    _stream_ptr,
+    get_context,
+    is_screened,
+    problem_set,
+    raise_exterior,
+    walk_config_struct,
+)
 from .estimator import PointEstimate
+from .walker import MajorantViolationError, check_screened
 
 __all__ = [
     "CacheShapeError",
@@ -268,11 +276,36 @@ class EstimateCache:
         pids = None
         if point_ids is not None:
             pids = torch.as_tensor(np.asarray(point_ids, dtype=np.int64)).to(dev).contiguous()
+        screened = is_screened(problem)
+        if screened and (cfg.sigma_bar is None or cfg.sigma_bar <= 0.0):
+            raise ValueError("delta tracking requires a positive cfg.sigma_bar")
         wc = walk_config_struct(cfg.resolve_eps(problem.domain), cfg.max_steps, cfg.antithetic,
-                                cfg.mode, cfg.rng_seed)
+                                cfg.mode, cfg.rng_seed, cfg.sigma_bar)
         ms, cn, cm, c2 = self._state
         if total_steps is None:
             total_steps = torch.zeros(1, dtype=torch.int64, device=dev)
+        if screened:
+            # a majorant violation surfaces only after the walks: estimate into scratch,
+            # check, then fold, so a failing epoch leaves the cache untouched (the
+            # reference raises inside estimate, before cache_update)
+            mean = torch.empty(P, dtype=torch.float64, device=dev)
+            m2 = torch.empty(P, dtype=torch.float64, device=dev)
+            check_screened(ctx._lib.wos_estimate(
+                ctx.handle, pset.handle, byref(wc), P, pts.data_ptr(),
+                None if pids is None else pids.data_ptr(), None, int(L),
+                (self.epoch * int(L)) & ((1 << 64) - 1), mean.data_ptr(), m2.data_ptr(),
+                total_steps.data_ptr(), _stream_ptr(stream)))
+            worst = c_double(-1.0)
+            _lib.check(ctx._lib.wos_context_majorant(ctx.handle, _stream_ptr(stream), byref(worst)))
+            if worst.value >= 0.0:
+                raise MajorantViolationError(
+                    f"majorant violated: sigma'={worst.value!r} > sigma_bar={cfg.sigma_bar!r}")
+            _lib.check(ctx._lib.wos_cache_fold(
+                ctx.handle, P, None if slots is None else slots.data_ptr(), mean.data_ptr(),
+                m2.data_ptr(), None, L // 2 if cfg.antithetic else L, ms.data_ptr(), cn.data_ptr(),
+                cm.data_ptr(), c2.data_ptr(), _stream_ptr(stream)))
+            self.epoch += 1
+            return self.targets_tensor()
         _lib.check(
             ctx._lib.wos_estimate_fold(
                 ctx.handle, pset.handle, byref(wc), P, pts.data_ptr(),

@@ -59,6 +59,7 @@ struct wos_context {
   unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
   unsigned long long* d_steps = nullptr;     // total-steps scratch of the *_host variants
   unsigned int* d_watchdog = nullptr;        // kernel iteration-limit flag
+  unsigned long long* d_majorant = nullptr;  // delta tracking: worst sigma' > sigma_bar (fp64 bits)
   int64_t host_exterior = -1;
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -84,6 +85,7 @@ struct wos_problem_set {
   float4* d_segs_n = nullptr;             // NATIVE: per polygon n + 1 records {v_k, e_k/|e_k|^2}
   size_t bytes_segs_n = 0;
   std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
+  double scr_sprime_max = -1.0;           // SRC_SCR_CONST: largest s' of the set (majorant check)
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
 
@@ -131,6 +133,8 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_watchdog, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->d_watchdog, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_majorant, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_majorant, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->d_exterior, 0xff, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     delete c;
@@ -147,6 +151,7 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_exterior);
   cudaFree(c->d_steps);
   cudaFree(c->d_watchdog);
+  cudaFree(c->d_majorant);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -218,9 +223,25 @@ static int validate(const wos_problem& p) {
       if ((r = need(p.n_src, 2 + p.dim, "Gaussian source"))) return r;
       if (!(p.src[1] > 0.0)) return fail(WOS_ERR_INVALID, "Gaussian sigma must be positive");
       break;
+    case WOS_SRC_SCREENED_CONST:
+      if (p.dim != 3) return fail(WOS_ERR_UNSUPPORTED, "delta tracking is 3D only (walker.py:322-418)");
+      if ((r = need(p.n_src, 4, "screened constant coefficients"))) return r;
+      if (p.bnd_kind != WOS_BND_CONST)
+        return fail(WOS_ERR_INVALID, "screened constant coefficients take a constant boundary g'");
+      if (!(p.src[3] > 0.0)) return fail(WOS_ERR_INVALID, "sqrt(alpha) must be positive");
+      break;
+    case WOS_SRC_SCREENED_VC:
+      if (p.dim != 3) return fail(WOS_ERR_UNSUPPORTED, "delta tracking is 3D only (walker.py:322-418)");
+      if ((r = need(p.n_src, 3, "varying-coefficient family"))) return r;
+      if (p.bnd_kind != WOS_BND_VC)
+        return fail(WOS_ERR_INVALID, "the varying-coefficient family takes the WOS_BND_VC boundary");
+      break;
     default:
       return fail(WOS_ERR_UNSUPPORTED, "unknown source kind %d", p.src_kind);
   }
+  if (p.dom_kind == WOS_DOM_POLYGON &&
+      (p.src_kind == WOS_SRC_SCREENED_CONST || p.src_kind == WOS_SRC_SCREENED_VC))
+    return fail(WOS_ERR_UNSUPPORTED, "delta tracking needs a 3D ball or box");
   switch (p.bnd_kind) {
     case WOS_BND_CONST:
       if ((r = need(p.n_bnd, 1, "constant boundary"))) return r;
@@ -251,6 +272,13 @@ static int validate(const wos_problem& p) {
     case WOS_BND_QUADRATIC:
       if (p.dim != 2) return fail(WOS_ERR_UNSUPPORTED, "quadratic boundary is 2D only");
       if ((r = need(p.n_bnd, 6, "quadratic boundary"))) return r;
+      break;
+    case WOS_BND_VC:
+      if (p.src_kind != WOS_SRC_SCREENED_VC)
+        return fail(WOS_ERR_INVALID, "WOS_BND_VC belongs to the varying-coefficient family");
+      if ((r = need(p.n_bnd, 1, "varying-coefficient boundary"))) return r;
+      if (p.bnd[0] != p.src[0])
+        return fail(WOS_ERR_INVALID, "boundary and coefficients must share phi");
       break;
     default:
       return fail(WOS_ERR_UNSUPPORTED, "unknown boundary kind %d", p.bnd_kind);
@@ -335,6 +363,8 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     case WOS_SRC_RBF2: ns = 6; break;
     case WOS_SRC_SINE: ns = dim == 2 ? Kt * Kt : Kt * Kt * Kt; break;
     case WOS_SRC_GAUSS: ns = 2 + dim; break;
+    case WOS_SRC_SCREENED_CONST: ns = 4; break;
+    case WOS_SRC_SCREENED_VC: ns = 6; break;
     default: ns = 0;
   }
   int nb = 0;
@@ -345,6 +375,7 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     case WOS_BND_FOURIER: nb = 2 + 2 * M; break;
     case WOS_BND_SQUARE_ARCSINE: nb = 4 + M; break;
     case WOS_BND_QUADRATIC: nb = 6; break;
+    case WOS_BND_VC: nb = 4; break;
   }
   s->bnd_off = kSrcOff + ns;
   s->stride = (kSrcOff + ns + nb + 3) & ~3;
@@ -436,6 +467,21 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       case WOS_SRC_GAUSS:
         for (int k = 0; k < 2 + dim; ++k) sd[k] = p.src[k];
         break;
+      case WOS_SRC_SCREENED_CONST:
+        for (int k = 0; k < 4; ++k) sd[k] = p.src[k];
+        s->scr_sprime_max = std::max(s->scr_sprime_max, p.src[0]);
+        break;
+      case WOS_SRC_SCREENED_VC: {
+        // pde.py:141-142,157: a = 4 pi phi, b = 3 pi phi, p = pi phi (Python's left-to-right products)
+        const double phi = p.src[0];
+        sd[0] = phi;
+        sd[1] = p.src[1];
+        sd[2] = p.src[2];
+        sd[3] = (4.0 * M_PI) * phi;
+        sd[4] = (3.0 * M_PI) * phi;
+        sd[5] = M_PI * phi;
+        break;
+      }
     }
     if (p.src_kind != WOS_SRC_SINE)
       for (int k = 0; k < ns; ++k) sn[k] = (float)sd[k];
@@ -460,6 +506,14 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
         bd[2] = p.bnd[2];
         bd[3] = M;
         for (int m = 1; m <= Mi; ++m) bd[3 + m] = p.bnd[3 + m];
+        break;
+      }
+      case WOS_BND_VC: {
+        const double phi = p.bnd[0];
+        bd[0] = phi;
+        bd[1] = (4.0 * M_PI) * phi;
+        bd[2] = (3.0 * M_PI) * phi;
+        bd[3] = M_PI * phi;
         break;
       }
       default:
@@ -575,6 +629,36 @@ static int check_watchdog(wos_context* c, cudaStream_t st) {
     cudaMemsetAsync(c->d_watchdog, 0, sizeof(w), st);
     return fail(WOS_ERR_CUDA, "walk kernel watchdog tripped (iteration limit): results invalid");
   }
+  return WOS_OK;
+}
+
+// delta tracking: report (and reset) a volume event whose sigma' exceeded sigma_bar
+// (walker.py:409-413); the stream must already be synchronized
+static int check_majorant(wos_context* c, const wos_walk_config* cfg, cudaStream_t st) {
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, c->d_majorant, sizeof(v), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (v) {
+    CUDA_TRY(cudaMemsetAsync(c->d_majorant, 0, sizeof(v), st));
+    double w;
+    memcpy(&w, &v, sizeof(w));
+    return fail(WOS_ERR_MAJORANT, "majorant violated: sigma'=%.17g > sigma_bar=%.17g", w,
+                cfg->sigma_bar);
+  }
+  return WOS_OK;
+}
+
+extern "C" int wos_context_majorant(wos_context* c, void* stream, double* out) {
+  if (!c || !out) return fail(WOS_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, c->d_majorant, sizeof(v), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(c->d_majorant, 0, sizeof(v), st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  double w = -1.0;
+  if (v) memcpy(&w, &v, sizeof(w));
+  *out = w;
   return WOS_OK;
 }
 
@@ -694,6 +778,19 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.seed = cfg->rng_seed;
   a.nkey0 = (uint32_t)cfg->rng_seed;
   a.nkey1_seed = (uint32_t)(cfg->rng_seed >> 32);
+  if (s->src_kind == WOS_SRC_SCREENED_CONST || s->src_kind == WOS_SRC_SCREENED_VC) {
+    // walker.py:324-325: delta tracking needs a positive majorant; the constant-coefficient
+    // kernel path rejects s' > sigma_bar before walking (walker.py:336-340)
+    if (!(cfg->sigma_bar > 0.0))
+      return fail(WOS_ERR_INVALID, "delta tracking requires a positive sigma_bar");
+    if (s->scr_sprime_max > cfg->sigma_bar) {
+      return fail(WOS_ERR_MAJORANT, "majorant violated: sigma'=%.17g > sigma_bar=%.17g",
+                  s->scr_sprime_max, cfg->sigma_bar);
+    }
+  }
+  a.sigma_bar = cfg->sigma_bar;
+  a.sqrt_sig = sqrt(cfg->sigma_bar > 0.0 ? cfg->sigma_bar : 0.0);
+  a.majorant = c->d_majorant;
   const size_t smem = smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes, k.elem);
   if (smem > 220 * 1024)
     return fail(WOS_ERR_UNSUPPORTED,
@@ -934,7 +1031,9 @@ extern "C" int wos_walk_rows_host(wos_context* c, const wos_problem_set* s,
   CUDA_TRY(cudaMemcpyAsync(out_steps, d_stp, n * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(out_hits, d_hit, n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  return check_watchdog(c, st);
+  r = check_watchdog(c, st);
+  if (r) return r;
+  return check_majorant(c, cfg, st);
 }
 
 extern "C" int wos_check_interior_host(wos_context* c, const wos_problem_set* s, int64_t n,
@@ -1026,6 +1125,8 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   CUDA_TRY(cudaStreamSynchronize(xs));
   if (out_total_steps) *out_total_steps = steps;
   r = check_watchdog(c, cs);
+  if (r) return r;
+  r = check_majorant(c, cfg, cs);
   if (r) return r;
   if (ext != ~0ull) {
     c->host_exterior = (int64_t)ext;

@@ -6,13 +6,16 @@ namespace wos {
 
 enum : int { DOM_BALL = 0, DOM_POLAR = 1, DOM_BOX = 2, DOM_POLY = 3 };
 enum : int { SRC_NONE = 0, SRC_CONST = 1, SRC_RBF2 = 2, SRC_SINE = 3, SRC_GAUSS = 4 };
+// delta-tracking (screened) walks: the "source" slot selects the transformed coefficients
+enum : int { SRC_SCR_CONST = 5, SRC_SCR_VC = 6 };
 enum : int {
   BND_CONST = 0,
   BND_FOURIER5 = 1,
   BND_LINEAR = 2,
   BND_FOURIER = 3,
   BND_SQUARE_ARCSINE = 4,
-  BND_QUADRATIC = 5
+  BND_QUADRATIC = 5,
+  BND_VC = 6  // varying-coefficient family: g' = sqrt(alpha) u_exact at the exit point
 };
 enum : int { MODE_REPLAY_F64 = 0, MODE_REPLAY_F32 = 1, MODE_NATIVE_F32 = 2 };
 enum : int { SINK_ROWS = 0, SINK_ESTIMATE = 1 };
@@ -106,6 +109,10 @@ struct KArgs {
   unsigned long long* total_steps;
   unsigned int* work_counter;
   unsigned int* watchdog;      // set to 1 if a warp hit the iteration limit
+  // ---- delta tracking (screened walks) ----
+  double sigma_bar;            // absorption majorant (WalkConfig.sigma_bar)
+  double sqrt_sig;             // sqrt(sigma_bar)
+  unsigned long long* majorant;  // max violating sigma' seen (fp64 bits), 0 = none
   uint32_t iter_limit;         // max(2^27, 4 * max_steps) loop iterations per warp
   // ---- single-instance NATIVE launches: the instance row and the Philox round
   // keys live in the kernel-parameter constant bank (FFMA / LOP3 c[] operands) ----

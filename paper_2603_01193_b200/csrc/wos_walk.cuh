@@ -74,6 +74,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void psincos(double a, double* s, double* c) { sincos(a, s, c); }
 __device__ __forceinline__ void psincos(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ double psin(double a) { return sin(a); }
+__device__ __forceinline__ float psin(float a) { return sinf(a); }
+__device__ __forceinline__ double pcos(double a) { return cos(a); }
+__device__ __forceinline__ float pcos(float a) { return cosf(a); }
 __device__ __forceinline__ double psqrt(double a) { return sqrt(a); }
 __device__ __forceinline__ float psqrt(float a) { return sqrtf(a); }
 __device__ __forceinline__ double plog(double a) { return log(a); }
@@ -129,8 +133,10 @@ struct Walker {
   static constexpr int DIM = S::DIM;
   static constexpr bool ONE = S::ONE;
 
-  // (not for polygons, whose segment scan needs the registers, nor for the ROWS sink)
-  static constexpr bool kHot = S::NATIVE && ONE && S::DOM != DOM_POLY && S::SINK == SINK_ESTIMATE;
+  // (not for polygons, whose segment scan needs the registers, nor for the fp64-heavy
+  // delta-tracking step, nor for the ROWS sink)
+  static constexpr bool kHot = S::NATIVE && ONE && S::DOM != DOM_POLY && S::SINK == SINK_ESTIMATE &&
+                               S::SRC != SRC_SCR_CONST && S::SRC != SRC_SCR_VC;
   static constexpr int kHotK = kHot ? 10 : 1;
   // hot source coefficients: those the jump reads at compile-time offsets
   static constexpr int kHotSrcN =
@@ -154,6 +160,8 @@ struct Walker {
     uint32_t c1, c2, c3, k1;   // NATIVE counters / key
     int32_t seg_off, n_seg, rec_off;
     int32_t seg_i;  // polygon: nearest segment found by the last distance query
+    Real thr;       // delta tracking: throughput (walker.py:365, _kernels.py:539)
+    Real sa;        // delta tracking: sqrt(alpha) at the start point (walker.py:352-354)
     // single-instance NATIVE launches: the Philox round keys and the parameters the
     // jump reads, copied once from the constant bank through a shuffle so that ptxas
     // keeps them in (uniform) registers instead of reloading them every step
@@ -617,8 +625,190 @@ struct Walker {
     }
   }
 
+  // ---------------- delta tracking (screened walks) ----------------
+  // Transformed problem  Laplacian U - sigma' U = -f'  walked with a majorant sigma_bar
+  // (walker.py:322-418, _kernels.py:476-558, greens.py:100-193). Row layouts:
+  //   SRC_SCR_CONST [s', f', has_f', sqrt_alpha]     (ScreenedProblem.const_coeffs)
+  //   SRC_SCR_VC    [phi, a_min, a_max, 4 pi phi, 3 pi phi, pi phi]   (pde.VcInstance)
+  //   BND_VC        [phi, 4 pi phi, 3 pi phi, pi phi]
+  static constexpr bool kScr = S::SRC == SRC_SCR_CONST || S::SRC == SRC_SCR_VC;
+
+  // h = log(alpha) = -x1^2 + cos(a x0) sin(b x1), its gradient and Laplacian (pde.py:138-151)
+  __device__ static __forceinline__ void vc_log_alpha(Real a_, Real b_, const Real* x, Real* h,
+                                                      Real* g, Real* lap) {
+    Real sa_, ca_, sb_, cb_;
+    psincos(a_ * x[0], &sa_, &ca_);
+    psincos(b_ * x[1], &sb_, &cb_);
+    *h = -x[1] * x[1] + ca_ * sb_;
+    g[0] = -a_ * sa_ * sb_;
+    g[1] = Real(-2) * x[1] + b_ * ca_ * cb_;
+    g[2] = Real(0);
+    *lap = Real(-2) - (a_ * a_ + b_ * b_) * ca_ * sb_;
+  }
+  // sigma(x) (pde.py:176-181)
+  __device__ static __forceinline__ Real vc_sigma(Real amin, Real amax, const Real* x) {
+    return amin + (amax - amin) * (Real(1) + Real(0.5) * psin((Real)kTwoPi * x[0]) *
+                                                  pcos((Real)(0.5 * kPi) * x[1]));
+  }
+  // manufactured solution u with gradient and Laplacian (pde.py:154-173)
+  __device__ static __forceinline__ void vc_solution(Real p, const Real* x, Real* u, Real* gu,
+                                                     Real* lu) {
+    Real s1, c1, s2, c2;
+    psincos(p * x[0], &s1, &c1);
+    psincos(Real(2) * p * x[1], &s2, &c2);
+    const Real s3 = psin(Real(3) * p * x[2]);
+    *u = s1 * c2 + (Real(1) - c1) * (Real(1) - s2) + s3 * s3;
+    if (gu) {
+      gu[0] = p * c1 * c2 + p * s1 * (Real(1) - s2);
+      gu[1] = Real(-2) * p * s1 * s2 - Real(2) * p * (Real(1) - c1) * c2;
+      gu[2] = Real(3) * p * psin(Real(6) * p * x[2]);
+      *lu = -p * p * s1 * c2 + p * p * c1 * (Real(1) - s2) - Real(4) * p * p * s1 * c2 +
+            Real(4) * p * p * (Real(1) - c1) * s2 + Real(18) * p * p * pcos(Real(6) * p * x[2]);
+    }
+  }
+  // sigma' = sigma e^-h + lap(h)/2 + |grad h|^2/4 and f' = f / sqrt(alpha) (pde.py:184-212)
+  __device__ static __forceinline__ void vc_coeffs(const Real* P, const Real* y, Real* sp,
+                                                   Real* fp) {
+    Real h, gh[3], lh;
+    vc_log_alpha(P[3], P[4], y, &h, gh, &lh);
+    const Real sigma = vc_sigma(P[1], P[2], y);
+    *sp = sigma * pexp(-h) + Real(0.5) * lh + Real(0.25) * (gh[0] * gh[0] + gh[1] * gh[1] + gh[2] * gh[2]);
+    Real u, gu[3], lu;
+    vc_solution(P[5], y, &u, gu, &lu);
+    const Real alpha = pexp(h);
+    const Real f = -alpha * lu - alpha * (gh[0] * gu[0] + gh[1] * gu[1] + gh[2] * gu[2]) + sigma * u;
+    *fp = f / pexp(Real(0.5) * h);
+  }
+  __device__ static __forceinline__ Real vc_sqrt_alpha(Real a_, Real b_, const Real* x) {
+    Real h, g[3], lap;
+    vc_log_alpha(a_, b_, x, &h, g, &lap);
+    return pexp(Real(0.5) * h);
+  }
+  // g' = sqrt(alpha) u at the exit point (pde.py:197-199)
+  __device__ static __forceinline__ Real vc_boundary(const Real* B, const Real* q) {
+    Real u;
+    vc_solution(B[3], q, &u, nullptr, nullptr);
+    return vc_sqrt_alpha(B[1], B[2], q) * u;
+  }
+
+  // fp64 volume-event radius-fraction CDF (greens.py:154-170, _kernels.py:491-495)
+  __device__ static __forceinline__ double radial_cdf(double q, double t) {
+    if (q < 1.0e-4) return t * t * (3.0 - 2.0 * t);
+    return (sinh(q) - q * t * cosh(q * (1.0 - t)) - sinh(q * (1.0 - t))) / (sinh(q) - q);
+  }
+  // REPLAY: fixed 64-step bisection (greens.py:173-186, _kernels.py:498-511)
+  __device__ static __forceinline__ double invert_radial_bisect(double q, double u) {
+    double lo = 0.0, hi = 1.0;
+    for (int it = 0; it < 64; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (radial_cdf(q, mid) < u) lo = mid;
+      else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+  }
+  // NATIVE: safeguarded Newton on the same CDF (pdf = q^2 t sinh(q (1-t)) / (sinh q - q)),
+  // started from the harmonic (q -> 0) inverse t = 1/2 - sin(asin(1 - 2u) / 3); every
+  // iterate stays inside the bracket [lo, hi] that the CDF values maintain
+  __device__ static __forceinline__ double invert_radial_newton(double q, double u) {
+    double t = 0.5 - sin(asin(1.0 - 2.0 * u) * (1.0 / 3.0));
+    if (q < 1.0e-4) return t;
+    const double sq = sinh(q), den = sq - q;
+    double lo = 0.0, hi = 1.0;
+    for (int it = 0; it < 40; ++it) {
+      const double e = exp(q * (1.0 - t)), ei = 1.0 / e;
+      const double sh = 0.5 * (e - ei), ch = 0.5 * (e + ei);
+      const double F = (sq - q * t * ch - sh) / den - u;
+      if (F < 0.0) lo = t;
+      else hi = t;
+      const double pdf = q * q * t * sh / den;
+      double tn = (pdf > 0.0) ? t - F / pdf : 0.5 * (lo + hi);
+      if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+      if (fabs(tn - t) < 1.0e-13) return tn;
+      t = tn;
+    }
+    return t;
+  }
+  __device__ static __forceinline__ void note_majorant(const KArgs& a, double sp) {
+    atomicMax(a.majorant, (unsigned long long)__double_as_longlong(sp));
+  }
+  // const-coefficient kernel path: a walk whose throughput died carries nothing more
+  // (_kernels.py:533-538)
+  __device__ static __forceinline__ bool dead(const Lane& l, const KArgs& a) {
+    if constexpr (S::SRC == SRC_SCR_CONST) return l.thr == Real(0) && prow(l, a)[kSrcOff + 2] == Real(0);
+    else return false;
+  }
+
+  // one delta-tracking step (walker.py:372-416; _kernels.py:539-557)
+  __device__ static __forceinline__ void screened_event(Lane& l, const KArgs& a) {
+    const Real* P = prow(l, a) + kSrcOff;
+    Real sp, fp = Real(0);
+    bool has_f = true;
+    if constexpr (S::SRC == SRC_SCR_CONST) {
+      sp = P[0];
+      fp = P[1];
+      has_f = P[2] != Real(0);
+    } else {
+      vc_coeffs(P, l.x, &sp, &fp);
+    }
+    if ((double)sp > a.sigma_bar) note_majorant(a, (double)sp);
+    const Real sb = (Real)a.sigma_bar;
+    if (has_f) l.acc = l.acc + l.thr * fp / sb;
+    l.thr = l.thr * (Real(1) - sp / sb);
+  }
+
+  __device__ static __forceinline__ void advance_screened_replay(Lane& l, Real d, const KArgs& a) {
+    uint64_t w[4];
+    philox4x64(2ull * (uint64_t)l.step, l.pid, l.tid, 0ull, a.seed, l.ikey, w);
+    double q = a.sqrt_sig * (double)d;
+    if (q > 500.0) q = 500.0;
+    const double surf = (q < 1.0e-6) ? 1.0 - q * q / 6.0 : q / sinh(q);
+    const Real z = Real(2) * (Real)u01_53(w[1]) - Real(1);
+    const Real s = psqrt(pmax(Real(0), Real(1) - z * z));
+    const Real phi = (Real)kTwoPi * (Real)u01_53(w[2]);
+    Real sph, cph;
+    psincos(phi, &sph, &cph);
+    const Real dir[3] = {s * cph, s * sph, z};
+    const bool vol = u01_53(w[0]) >= surf;
+    const Real rad = vol ? d * (Real)invert_radial_bisect(q, u01_53(w[3])) : d;
+    const Real sr = l.sgn * rad;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) l.x[i] = l.x[i] + sr * dir[i];
+    if (vol) screened_event(l, a);
+  }
+
+  __device__ static __forceinline__ void advance_screened_native(Lane& l, float d, const KArgs& a) {
+    const uint4 A = native_block(l, a);
+    double q = a.sqrt_sig * (double)d;
+    if (q > 500.0) q = 500.0;
+    const double surf = (q < 1.0e-6) ? 1.0 - q * q / 6.0 : q / sinh(q);
+    const float z = f2x(A.y) - 3.0f;
+    const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
+    float sph, cph;
+    __sincosf(fmaf(f12(A.z), kTwoPiF, -kTwoPiF), &sph, &cph);
+    const bool vol = (double)(f12(A.x) - 1.0f) >= surf;
+    float rad = d;
+    if (vol) rad = d * (float)invert_radial_newton(q, (double)(f12(A.w) - 1.0f) + 0x1p-24);
+    const float sr = l.sgn * rad, srxy = sr * sxy;
+    l.x[0] = fmaf(srxy, cph, l.x[0]);
+    l.x[1] = fmaf(srxy, sph, l.x[1]);
+    l.x[2] = fmaf(sr, z, l.x[2]);
+    if (vol) screened_event(l, a);
+  }
+
   // value at termination: acc + g(projection); constant g needs no projection
   __device__ static __forceinline__ Real finish_value(const Lane& l, const KArgs& a) {
+    if constexpr (kScr) {
+      // values = (acc + thr g'(q)) / sqrt_alpha(x0)  (walker.py:356-357,368-369)
+      Real g;
+      if constexpr (S::SRC == SRC_SCR_VC) {
+        Real q[DIM];
+        project(l, a, q);
+        g = vc_boundary(prow(l, a) + a.bnd_off, q);
+      } else {
+        g = prow(l, a)[a.bnd_off];
+      }
+      return (l.acc + l.thr * g) / l.sa;
+    }
     if constexpr (ONE) {
       if (a.bnd_kind == BND_CONST) return l.acc + a.bnd_c;
     }
@@ -795,6 +985,12 @@ struct Walker {
       l.seg_off = h.seg_off;
       l.n_seg = h.n_seg;
       l.rec_off = h.rec_off;
+    }
+    if constexpr (kScr) {
+      l.thr = Real(1);
+      const Real* P = prow(l, a) + kSrcOff;
+      if constexpr (S::SRC == SRC_SCR_VC) l.sa = vc_sqrt_alpha(P[3], P[4], l.x);
+      else l.sa = P[3];
     }
   }
 };
@@ -1012,10 +1208,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       bool fin = false;
       if (active) {
         const Real d = W::dist(l, a, srec);
-        if (d < eps || l.step >= a.max_steps) {
+        if (d < eps || l.step >= a.max_steps || W::dead(l, a)) {
           fin = true;
         } else {
-          if constexpr (S::NATIVE) W::advance_native(l, d, a);
+          if constexpr (W::kScr) {
+            if constexpr (S::NATIVE) W::advance_screened_native(l, d, a);
+            else W::advance_screened_replay(l, d, a);
+          } else if constexpr (S::NATIVE) W::advance_native(l, d, a);
           else W::advance_replay(l, d, a);
           l.step += 1;
         }
@@ -1171,7 +1370,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             blk = (cu_k % kSlots) * 4u;
             if (j < cu_jend) {
               bool started = false;
-              if constexpr (S::NATIVE && S::ONE) {
+              if constexpr (S::NATIVE && S::ONE && !W::kScr) {
                 if (cu_fastc) {
                   W::start_native(l, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
                                   cu_c2b + (anti ? (jr & ~1u) : jr), cu_c3);
@@ -1257,7 +1456,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     // ================= one step of every active walk =================
     if (active) {
       const Real d = W::dist(l, a, srec);
-      if (d < eps || l.step >= a.max_steps) {
+      if (d < eps || l.step >= a.max_steps || W::dead(l, a)) {
         // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
         const Real v = W::finish_value(l, a);
         lane_steps += (unsigned long long)l.step;
@@ -1267,11 +1466,15 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         } else {
           a.out_values[l.seq] = (double)v;
           a.out_steps[l.seq] = (int64_t)l.step;
-          a.out_hits[l.seq] = (uint8_t)(d < eps);
+          // a dead walk (const kernel path) reports hit = 1 unless it also ran out of steps
+          a.out_hits[l.seq] = (uint8_t)(d < eps || (l.step < a.max_steps && W::dead(l, a)));
         }
         active = false;
       } else {
-        if constexpr (S::NATIVE) W::advance_native(l, d, a);
+        if constexpr (W::kScr) {
+          if constexpr (S::NATIVE) W::advance_screened_native(l, d, a);
+          else W::advance_screened_replay(l, d, a);
+        } else if constexpr (S::NATIVE) W::advance_native(l, d, a);
         else W::advance_replay(l, d, a);
         l.step += 1;
       }

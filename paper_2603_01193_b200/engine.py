@@ -23,6 +23,7 @@ __all__ = [
     "ProblemSet",
     "get_context",
     "problem_set",
+    "is_screened",
     "mode_code",
 ]
 
@@ -49,15 +50,57 @@ def mode_code(mode) -> int:
         raise ValueError(f"unknown walk mode {mode!r}; expected one of {sorted(_MODES)}") from None
 
 
+def _screened_record(inst, dom_kind, dom_params, dim):
+    """Spec record of a delta-tracking problem (walker.py:120-136).
+
+    Constant coefficients come from ``const_coeffs = (s', f' or None, g')`` (the
+    reference's compiled form, walker.py:331-347); the paper's varying-coefficient
+    family (pde.VcInstance) from ``vc_params = (phi, a_min, a_max)``. ``sqrt_alpha``
+    must be None or a number for constant coefficients (it is implied for the family).
+    """
+    if dim != 3:
+        raise UnsupportedProblemError("delta tracking is 3D only (walker.py:322-418)")
+    ikey = int(getattr(inst, "instance_key", 0)) & ((1 << 64) - 1)
+    vc = getattr(inst, "vc_params", None)
+    if vc is not None:
+        phi, a_min, a_max = (float(v) for v in vc)
+        return (dim, dom_kind, tuple(dom_params), specs.SRC_SCREENED_VC, (phi, a_min, a_max),
+                specs.BND_VC, (phi,), ikey)
+    cc = getattr(inst, "const_coeffs", None)
+    if cc is None:
+        raise UnsupportedProblemError(
+            "screened problem without const_coeffs or vc_params: callable coefficients have "
+            "no GPU encoding (no CPU fallback)"
+        )
+    sprime, fprime, gprime = cc
+    sa = getattr(inst, "sqrt_alpha", None)
+    if sa is None:
+        sa = 1.0
+    elif callable(sa):
+        raise UnsupportedProblemError("a callable sqrt_alpha has no GPU encoding; pass a number")
+    return (dim, dom_kind, tuple(dom_params), specs.SRC_SCREENED_CONST,
+            (float(sprime), 0.0 if fprime is None else float(fprime),
+             0.0 if fprime is None else 1.0, float(sa)),
+            specs.BND_CONST, (float(gprime),), ikey)
+
+
+def is_screened(inst) -> bool:
+    inst = getattr(inst, "problem", inst)
+    return hasattr(inst, "sigma_prime") or hasattr(inst, "const_coeffs") or hasattr(inst, "vc_params")
+
+
 def problem_record(inst):
     """Reduce a Problem (ours or the reference's) to a plain spec record.
 
     Mirrors ``walker._specs_for_kernel`` (walker.py:160-171): the boundary must
     carry a ``boundary_spec``; a present source must carry a ``source_spec``.
+    Screened (delta-tracking) problems reduce to their coefficient specs.
     """
     inst = getattr(inst, "problem", inst)
     dom = inst.domain
     dom_kind, dom_params, dim = domain_spec(dom)
+    if is_screened(inst):
+        return _screened_record(inst, dom_kind, dom_params, dim)
     bspec = getattr(inst, "boundary_spec", None)
     if bspec is None:
         raise UnsupportedProblemError(
@@ -223,10 +266,11 @@ def problem_set(ctx: Context, problems) -> ProblemSet:
         return ps
 
 
-def walk_config_struct(eps: float, max_steps: int, antithetic: bool, mode, seed: int):
+def walk_config_struct(eps: float, max_steps: int, antithetic: bool, mode, seed: int,
+                       sigma_bar=None):
     return _lib.WosWalkConfig(
         float(eps), int(max_steps), int(bool(antithetic)), mode_code(mode),
-        int(seed) & ((1 << 64) - 1),
+        int(seed) & ((1 << 64) - 1), 0.0 if sigma_bar is None else float(sigma_bar),
     )
 
 

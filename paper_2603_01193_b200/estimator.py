@@ -24,8 +24,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .engine import get_context, problem_set, raise_exterior, walk_config_struct
+from .engine import get_context, is_screened, problem_set, raise_exterior, walk_config_struct
 from .geometry import ExteriorQueryError
+from .walker import check_screened
 
 __all__ = [
     "PointEstimate",
@@ -88,7 +89,8 @@ def _estimate_one_device(device, problems, pts, pids, inst, L, cfg, eps, traj_st
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
     P = pts.shape[0]
-    wc = walk_config_struct(eps, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed)
+    wc = walk_config_struct(eps, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed,
+                            cfg.sigma_bar)
     mean = np.empty(P, dtype=np.float64)
     m2 = np.empty(P, dtype=np.float64)
     steps = c_uint64(0)
@@ -99,7 +101,7 @@ def _estimate_one_device(device, problems, pts, pids, inst, L, cfg, eps, traj_st
     )
     if status == _lib.WOS_ERR_EXTERIOR:
         return None, None, ctx.exterior(), 0
-    _lib.check(status)
+    check_screened(status)
     return mean, m2, -1, steps.value
 
 
@@ -136,6 +138,8 @@ def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None
         if inst.shape != (P,) or (P and (inst.min() < 0 or inst.max() >= len(problems))):
             raise ValueError("inst_index must map every point to a problem")
     eps = cfg.resolve_eps(problems[0].domain)
+    if is_screened(problems[0]) and (cfg.sigma_bar is None or cfg.sigma_bar <= 0.0):
+        raise ValueError("delta tracking requires a positive cfg.sigma_bar")
     if L < 1 or (cfg.antithetic and L % 2):
         # the reference checks the interior first (estimator.py:156-163)
         ctx = get_context()
@@ -212,7 +216,7 @@ def estimate_tensors(pset, points, point_ids, L, cfg, *, inst_index=None, traj_s
     if stream is None:
         stream = torch.cuda.current_stream(points.device)
     e = eps if eps is not None else cfg.eps_shell
-    wc = walk_config_struct(e, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed)
+    wc = walk_config_struct(e, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed, cfg.sigma_bar)
     _lib.check(
         ctx._lib.wos_estimate(
             ctx.handle, pset.handle, byref(wc), P, points.data_ptr(), point_ids.data_ptr(),

@@ -23,6 +23,9 @@ SRC_CONST = 1
 SRC_RBF2 = 2
 SRC_SINE = 3
 SRC_GAUSS = 4
+# delta tracking: transformed coefficients of a ScreenedProblem (walker.py:120-136)
+SRC_SCREENED_CONST = 5
+SRC_SCREENED_VC = 6
 
 # boundary kinds (_kernels.py:39-42 for the first three)
 BND_CONST = 0
@@ -31,6 +34,7 @@ BND_LINEAR = 2
 BND_FOURIER = 3
 BND_SQUARE_ARCSINE = 4
 BND_QUADRATIC = 5
+BND_VC = 6
 
 # domain kinds (_kernels.py:44-46: DOM_DISK = 0, DOM_POLAR = 1)
 DOM_BALL = 0
@@ -38,7 +42,8 @@ DOM_POLAR = 1
 DOM_BOX = 2
 DOM_POLYGON = 3
 
-SRC_NAMES = {SRC_NONE: "none", SRC_CONST: "const", SRC_RBF2: "rbf2", SRC_SINE: "sine", SRC_GAUSS: "gauss"}
+SRC_NAMES = {SRC_NONE: "none", SRC_CONST: "const", SRC_RBF2: "rbf2", SRC_SINE: "sine", SRC_GAUSS: "gauss",
+             SRC_SCREENED_CONST: "screened_const", SRC_SCREENED_VC: "screened_vc"}
 BND_NAMES = {
     BND_CONST: "const",
     BND_FOURIER5: "fourier5",
@@ -46,6 +51,7 @@ BND_NAMES = {
     BND_FOURIER: "fourier",
     BND_SQUARE_ARCSINE: "square_arcsine",
     BND_QUADRATIC: "quadratic",
+    BND_VC: "vc",
 }
 
 

@@ -34,6 +34,10 @@ from .engine import (
 from .geometry import ExteriorQueryError
 
 __all__ = [
+    "MajorantViolationError",
+    "ScreenedProblem",
+    "walk_screened_delta",
+    "walk_screened_values",
     "WalkConfig",
     "TrajectoryResult",
     "TrajectoryStream",
@@ -106,6 +110,38 @@ class Problem:
     source_spec: tuple | None = None
 
 
+class MajorantViolationError(RuntimeError):
+    """sigma' exceeded the delta-tracking majorant sigma_bar (walker.py:51-52)."""
+
+
+@dataclass(frozen=True)
+class ScreenedProblem:
+    """Transformed screened problem for delta tracking (walker.py:120-136).
+
+    The GPU walker reads the coefficient codes: ``const_coeffs = (s', f' or None, g')``
+    (the reference's compiled form; ``sqrt_alpha`` then None or a number), or
+    ``vc_params = (phi, a_min, a_max)`` for the paper's varying-coefficient family
+    (pde.VcInstance, pde.py:138-243: sigma', f', g' and sqrt(alpha) in closed form).
+    The callable fields are kept for signature compatibility only.
+    """
+
+    domain: object
+    sigma_prime: object = None
+    boundary_prime: object = None
+    source_prime: object = None
+    sqrt_alpha: object = None
+    instance_key: int = 0
+    const_coeffs: tuple | None = None
+    vc_params: tuple | None = None
+
+
+def check_screened(status: int) -> None:
+    """_lib.check with WOS_ERR_MAJORANT mapped to MajorantViolationError."""
+    if status == _lib.WOS_ERR_MAJORANT:
+        raise MajorantViolationError(_lib.last_error())
+    _lib.check(status)
+
+
 def _cfg_of(cfg):
     return cfg if cfg is not None else WalkConfig()
 
@@ -151,6 +187,55 @@ def walk_poisson_values(inst, points, point_ids, traj_ids, signs, cfg):
             )
         )
     return values, steps, hits
+
+
+def walk_screened_values(inst, points, point_ids, traj_ids, signs, cfg):
+    """Batch interface of the delta-tracking walker, one row per walk (walker.py:322-357).
+
+    Returns (values, steps, hits) like ``walk_poisson_values``; values are already
+    divided by sqrt(alpha) at the start point.
+    """
+    inst = getattr(inst, "problem", inst)
+    cfg = _cfg_of(cfg)
+    if cfg.sigma_bar is None or cfg.sigma_bar <= 0.0:
+        raise ValueError("delta tracking requires a positive cfg.sigma_bar")
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    if pts.ndim != 2:
+        raise ValueError("points must be an (n, d) array")
+    n = pts.shape[0]
+    pid, tid, sgn = _streams_as_arrays(point_ids, traj_ids, signs, n)
+    ctx = get_context()
+    pset = problem_set(ctx, [inst])
+    if pts.shape[1] != pset.dim:
+        raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
+    wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode,
+                            cfg.rng_seed, cfg.sigma_bar)
+    values = np.empty(n, dtype=np.float64)
+    steps = np.empty(n, dtype=np.int64)
+    hits = np.empty(n, dtype=np.uint8)
+    if n:
+        check_screened(
+            ctx._lib.wos_walk_rows_host(
+                ctx.handle, pset.handle, byref(wc), n, pts.ctypes.data, pid.ctypes.data,
+                tid.ctypes.data, sgn.ctypes.data, values.ctypes.data, steps.ctypes.data,
+                hits.ctypes.data,
+            )
+        )
+    return values, steps, hits
+
+
+def walk_screened_delta(inst, xi, cfg, stream: TrajectoryStream | None = None) -> TrajectoryResult:
+    """One delta-tracking trajectory from the interior point xi (walker.py:465-475)."""
+    inst = getattr(inst, "problem", inst)
+    cfg = _cfg_of(cfg)
+    if cfg.sigma_bar is None or cfg.sigma_bar <= 0.0:
+        raise ValueError("delta tracking requires a positive cfg.sigma_bar")
+    _require_interior(inst, xi)
+    s = stream or TrajectoryStream()
+    out = walk_screened_values(
+        inst, np.asarray(xi, dtype=np.float64)[None, :], [s.point_id], [s.traj_id], [s.sign], cfg
+    )
+    return _as_result(*out)
 
 
 def _require_interior(inst, xi):
