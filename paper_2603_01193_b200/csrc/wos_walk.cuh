@@ -632,13 +632,32 @@ struct Walker {
   //   SRC_SCR_VC    [phi, a_min, a_max, 4 pi phi, 3 pi phi, pi phi]   (pde.VcInstance)
   //   BND_VC        [phi, 4 pi phi, 3 pi phi, pi phi]
   static constexpr bool kScr = S::SRC == SRC_SCR_CONST || S::SRC == SRC_SCR_VC;
+  // family coefficients: libm-accurate in REPLAY (the reference's numpy), MUFU fast math
+  // in NATIVE (arguments stay below ~25 rad, where __sinf/__expf keep ~1e-6 absolute /
+  // relative error, far under the Monte Carlo error)
+  __device__ static __forceinline__ void tsincos(Real x, Real* s_, Real* c_) {
+    if constexpr (S::NATIVE) __sincosf(x, s_, c_);
+    else psincos(x, s_, c_);
+  }
+  __device__ static __forceinline__ Real tsin(Real x) {
+    if constexpr (S::NATIVE) return __sinf(x);
+    else return psin(x);
+  }
+  __device__ static __forceinline__ Real tcos(Real x) {
+    if constexpr (S::NATIVE) return __cosf(x);
+    else return pcos(x);
+  }
+  __device__ static __forceinline__ Real texp(Real x) {
+    if constexpr (S::NATIVE) return __expf(x);
+    else return pexp(x);
+  }
 
   // h = log(alpha) = -x1^2 + cos(a x0) sin(b x1), its gradient and Laplacian (pde.py:138-151)
   __device__ static __forceinline__ void vc_log_alpha(Real a_, Real b_, const Real* x, Real* h,
                                                       Real* g, Real* lap) {
     Real sa_, ca_, sb_, cb_;
-    psincos(a_ * x[0], &sa_, &ca_);
-    psincos(b_ * x[1], &sb_, &cb_);
+    tsincos(a_ * x[0], &sa_, &ca_);
+    tsincos(b_ * x[1], &sb_, &cb_);
     *h = -x[1] * x[1] + ca_ * sb_;
     g[0] = -a_ * sa_ * sb_;
     g[1] = Real(-2) * x[1] + b_ * ca_ * cb_;
@@ -647,23 +666,23 @@ struct Walker {
   }
   // sigma(x) (pde.py:176-181)
   __device__ static __forceinline__ Real vc_sigma(Real amin, Real amax, const Real* x) {
-    return amin + (amax - amin) * (Real(1) + Real(0.5) * psin((Real)kTwoPi * x[0]) *
-                                                  pcos((Real)(0.5 * kPi) * x[1]));
+    return amin + (amax - amin) * (Real(1) + Real(0.5) * tsin((Real)kTwoPi * x[0]) *
+                                                  tcos((Real)(0.5 * kPi) * x[1]));
   }
   // manufactured solution u with gradient and Laplacian (pde.py:154-173)
   __device__ static __forceinline__ void vc_solution(Real p, const Real* x, Real* u, Real* gu,
                                                      Real* lu) {
     Real s1, c1, s2, c2;
-    psincos(p * x[0], &s1, &c1);
-    psincos(Real(2) * p * x[1], &s2, &c2);
-    const Real s3 = psin(Real(3) * p * x[2]);
+    tsincos(p * x[0], &s1, &c1);
+    tsincos(Real(2) * p * x[1], &s2, &c2);
+    const Real s3 = tsin(Real(3) * p * x[2]);
     *u = s1 * c2 + (Real(1) - c1) * (Real(1) - s2) + s3 * s3;
     if (gu) {
       gu[0] = p * c1 * c2 + p * s1 * (Real(1) - s2);
       gu[1] = Real(-2) * p * s1 * s2 - Real(2) * p * (Real(1) - c1) * c2;
-      gu[2] = Real(3) * p * psin(Real(6) * p * x[2]);
+      gu[2] = Real(3) * p * tsin(Real(6) * p * x[2]);
       *lu = -p * p * s1 * c2 + p * p * c1 * (Real(1) - s2) - Real(4) * p * p * s1 * c2 +
-            Real(4) * p * p * (Real(1) - c1) * s2 + Real(18) * p * p * pcos(Real(6) * p * x[2]);
+            Real(4) * p * p * (Real(1) - c1) * s2 + Real(18) * p * p * tcos(Real(6) * p * x[2]);
     }
   }
   // sigma' = sigma e^-h + lap(h)/2 + |grad h|^2/4 and f' = f / sqrt(alpha) (pde.py:184-212)
@@ -672,17 +691,17 @@ struct Walker {
     Real h, gh[3], lh;
     vc_log_alpha(P[3], P[4], y, &h, gh, &lh);
     const Real sigma = vc_sigma(P[1], P[2], y);
-    *sp = sigma * pexp(-h) + Real(0.5) * lh + Real(0.25) * (gh[0] * gh[0] + gh[1] * gh[1] + gh[2] * gh[2]);
+    *sp = sigma * texp(-h) + Real(0.5) * lh + Real(0.25) * (gh[0] * gh[0] + gh[1] * gh[1] + gh[2] * gh[2]);
     Real u, gu[3], lu;
     vc_solution(P[5], y, &u, gu, &lu);
-    const Real alpha = pexp(h);
+    const Real alpha = texp(h);
     const Real f = -alpha * lu - alpha * (gh[0] * gu[0] + gh[1] * gu[1] + gh[2] * gu[2]) + sigma * u;
-    *fp = f / pexp(Real(0.5) * h);
+    *fp = f / texp(Real(0.5) * h);
   }
   __device__ static __forceinline__ Real vc_sqrt_alpha(Real a_, Real b_, const Real* x) {
     Real h, g[3], lap;
     vc_log_alpha(a_, b_, x, &h, g, &lap);
-    return pexp(Real(0.5) * h);
+    return texp(Real(0.5) * h);
   }
   // g' = sqrt(alpha) u at the exit point (pde.py:197-199)
   __device__ static __forceinline__ Real vc_boundary(const Real* B, const Real* q) {
@@ -780,12 +799,22 @@ struct Walker {
     const uint4 A = native_block(l, a);
     double q = a.sqrt_sig * (double)d;
     if (q > 500.0) q = 500.0;
-    const double surf = (q < 1.0e-6) ? 1.0 - q * q / 6.0 : q / sinh(q);
+    // surface probability q / sinh q in fp32 (it is compared with a 23-bit uniform):
+    // series below 0.125, 2 q e^-q / (1 - e^-2q) above (no overflow up to q = 500)
+    const float qf = (float)q;
+    float surf;
+    if (qf < 0.125f) {
+      const float q2 = qf * qf;
+      surf = fmaf(q2, fmaf(q2, fmaf(q2, -31.0f / 15120.0f, 7.0f / 360.0f), -1.0f / 6.0f), 1.0f);
+    } else {
+      const float e = __expf(-qf);
+      surf = 2.0f * qf * e / fmaf(-e, e, 1.0f);
+    }
     const float z = f2x(A.y) - 3.0f;
     const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
     float sph, cph;
     __sincosf(fmaf(f12(A.z), kTwoPiF, -kTwoPiF), &sph, &cph);
-    const bool vol = (double)(f12(A.x) - 1.0f) >= surf;
+    const bool vol = (f12(A.x) - 1.0f) >= surf;
     float rad = d;
     if (vol) rad = d * (float)invert_radial_newton(q, (double)(f12(A.w) - 1.0f) + 0x1p-24);
     const float sr = l.sgn * rad, srxy = sr * sxy;
