@@ -74,7 +74,13 @@ typedef enum wos_mode {
 /* ---- domain kinds and parameter layouts (double[]) ------------------ */
 /* WOS_DOM_BALL     disk (dim 2) or ball (dim 3):      [c_0..c_{dim-1}, R]
  *                  = geometry.BallDomain (geometry.py:172-238)
- * WOS_DOM_POLAR    reserved for the reference's PolarDomain; not supported
+ * WOS_DOM_POLAR    2D star curve r(t) = r0 (1 + c1 cos 4t + c2 cos 8t) = geometry.PolarDomain
+ *                  (geometry.py:83-153): [r0, c1, c2] (the library tabulates the curve at
+ *                  4096 angles with its own libm) or [r0, c1, c2, stride, n, bx_0..bx_{n-1},
+ *                  by_0..by_{n-1}] with the reference's own table (PolarDomain._bx/_by,
+ *                  _stride) for bit-level replay. Distance and closest point follow
+ *                  _kernels.polar_query_fast (strided table scan + window + one parabolic
+ *                  refinement, _kernels.py:121-219); inside = |x| < r(atan2(y, x))
  * WOS_DOM_BOX      axis-aligned box:                   [lo_0..lo_{dim-1}, hi_0..hi_{dim-1}]
  *                  distance = min over faces, closest point = projection on the
  *                  first nearest face (axis order, lower face before upper face)

@@ -102,9 +102,52 @@ static double nonzero_u(double u, uint64_t draw, uint64_t pid, uint64_t tid, uin
 /* ------------------------------------------------------------------ */
 /* Domains: distance to the boundary and the closest boundary point    */
 /* ------------------------------------------------------------------ */
+/* PolarDomain (geometry.py:83-153): table form [r0, c1, c2, stride, n, bx.., by..] */
+static double polar_r(const double* P, double t) {
+  return P[0] * (1.0 + P[1] * cos(4.0 * t) + P[2] * cos(8.0 * t)); /* _kernels.py:110-112 */
+}
+static double polar_curve_d2(const double* P, double t, double px, double py) {
+  const double r = polar_r(P, t);
+  const double dx = r * cos(t) - px, dy = r * sin(t) - py;
+  return dx * dx + dy * dy;
+}
+/* _kernels.polar_query_fast (_kernels.py:121-148, 185-219) */
+static double polar_query(const double* P, double px, double py, double* qx, double* qy) {
+  const int stride = (int)P[3], n = (int)P[4];
+  const double *bx = P + 5, *by = P + 5 + n;
+  double best = 1.0e300;
+  int bj = 0;
+  for (int j = 0; j < n; j += stride) {
+    const double dx = bx[j] - px, dy = by[j] - py, d2 = dx * dx + dy * dy;
+    if (d2 < best) { best = d2; bj = j; }
+  }
+  if (stride > 1) {
+    const int lo = bj - stride;
+    for (int off = 0; off <= 2 * stride; ++off) {
+      int jj = (lo + off) % n;
+      if (jj < 0) jj += n;
+      const double dx = bx[jj] - px, dy = by[jj] - py, d2 = dx * dx + dy * dy;
+      if (d2 < best) { best = d2; bj = jj; }
+    }
+  }
+  const double h = TWO_PI / n, t0 = bj * h;
+  const double fm = polar_curve_d2(P, t0 - h, px, py), fp = polar_curve_d2(P, t0 + h, px, py);
+  const double denom = fm - 2.0 * best + fp;
+  double shift = denom > 0.0 ? 0.5 * h * (fm - fp) / denom : 0.0;
+  if (shift > h) shift = h;
+  else if (shift < -h) shift = -h;
+  const double tm = t0 + shift, r = polar_r(P, tm);
+  const double cx = r * cos(tm), cy = r * sin(tm);
+  const double dx = cx - px, dy = cy - py, dm = dx * dx + dy * dy;
+  if (best < dm) { *qx = bx[bj]; *qy = by[bj]; return sqrt(best); }
+  *qx = cx; *qy = cy;
+  return sqrt(dm);
+}
+
 static double query(const wos_problem* pb, const double* x, double* q) {
   const int dim = pb->dim;
   const double* P = pb->dom;
+  if (pb->dom_kind == WOS_DOM_POLAR) return polar_query(P, x[0], x[1], &q[0], &q[1]);
   if (pb->dom_kind == WOS_DOM_BALL) {
     /* geometry.py:196-206 */
     double u[3], s = 0.0;
@@ -154,6 +197,10 @@ static double query(const wos_problem* pb, const double* x, double* q) {
 int oracle_contains(const wos_problem* pb, const double* x) {
   const int dim = pb->dim;
   const double* P = pb->dom;
+  if (pb->dom_kind == WOS_DOM_POLAR) { /* geometry.py:129-134 */
+    const double th = atan2(x[1], x[0]);
+    return hypot(x[0], x[1]) < polar_r(P, th);
+  }
   if (pb->dom_kind == WOS_DOM_BALL) {
     double s = 0.0;
     for (int i = 0; i < dim; ++i) s += (x[i] - P[i]) * (x[i] - P[i]);

@@ -84,6 +84,9 @@ struct wos_problem_set {
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
   float4* d_segs_n = nullptr;             // NATIVE: per polygon n + 1 records {v_k, e_k/|e_k|^2}
   size_t bytes_segs_n = 0;
+  double* d_polar_d = nullptr;            // POLAR: per instance n (bx, by) pairs, fp64
+  float* d_polar_f = nullptr;             //        the same, fp32
+  size_t bytes_polar_d = 0, bytes_polar_f = 0;
   std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
   double scr_sprime_max = -1.0;           // SRC_SCR_CONST: largest s' of the set (majorant check)
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
@@ -196,8 +199,20 @@ static int validate(const wos_problem& p) {
       if (nv < 3 || p.n_dom != 1 + 2 * nv) return fail(WOS_ERR_INVALID, "polygon parameter count mismatch");
       break;
     }
-    case WOS_DOM_POLAR:
-      return fail(WOS_ERR_UNSUPPORTED, "PolarDomain has no GPU encoding");
+    case WOS_DOM_POLAR: {
+      if (p.dim != 2) return fail(WOS_ERR_INVALID, "polar domains are 2D");
+      if (p.n_dom != 3 && p.n_dom < 5) return fail(WOS_ERR_INVALID, "polar domain needs [r0, c1, c2(, stride, n, table)]");
+      if (!(p.dom[0] > 0.0)) return fail(WOS_ERR_INVALID, "r0 must be positive");
+      if (!(fabs(p.dom[1]) + fabs(p.dom[2]) < 1.0))
+        return fail(WOS_ERR_INVALID, "|c1| + |c2| must be < 1 for a valid boundary");
+      if (p.n_dom > 3) {
+        const int st = (int)p.dom[3], nt = (int)p.dom[4];
+        if (nt < 8 || nt > (1 << 16) || st < 1 || st > nt)
+          return fail(WOS_ERR_INVALID, "polar table size / stride out of range");
+        if (p.n_dom != 5 + 2 * nt) return fail(WOS_ERR_INVALID, "polar table parameter count mismatch");
+      }
+      break;
+    }
     default:
       return fail(WOS_ERR_UNSUPPORTED, "unknown domain kind %d", p.dom_kind);
   }
@@ -385,6 +400,7 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   std::vector<InstHdr> hd(n);
   std::vector<double> segd;
   std::vector<float4> segn;
+  std::vector<double> polard;  // POLAR tables, (bx, by) pairs
   for (int i = 0; i < n; ++i) {
     const wos_problem& p = probs[i];
     double* rd = td.data() + (size_t)i * stride;
@@ -396,6 +412,31 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     if (p.dom_kind == WOS_DOM_BALL) {
       for (int k = 0; k < dim; ++k) rd[k] = p.dom[k];
       rd[3] = p.dom[dim];
+    } else if (p.dom_kind == WOS_DOM_POLAR) {
+      // geometry.py:97-112: the curve tabulated at n angles, strided scan for mild curves
+      const double r0 = p.dom[0], c1 = p.dom[1], c2 = p.dom[2];
+      rd[0] = r0;
+      rd[1] = c1;
+      rd[2] = c2;
+      int nt = 4096, st = (fabs(c1) + fabs(c2) <= 0.45) ? 64 : 1;
+      if (p.n_dom > 3) {
+        st = (int)p.dom[3];
+        nt = (int)p.dom[4];
+      }
+      hd[i].seg_off = (int)(polard.size() / 2);
+      hd[i].n_seg = nt;
+      hd[i].rec_off = st;
+      for (int k = 0; k < nt; ++k) {
+        if (p.n_dom > 3) {
+          polard.push_back(p.dom[5 + k]);
+          polard.push_back(p.dom[5 + nt + k]);
+        } else {
+          const double th = (double)k * (2.0 * M_PI / nt);
+          const double r = r0 * (1.0 + c1 * cos(4.0 * th) + c2 * cos(8.0 * th));
+          polard.push_back(r * cos(th));
+          polard.push_back(r * sin(th));
+        }
+      }
     } else if (p.dom_kind == WOS_DOM_BOX) {
       for (int k = 0; k < dim; ++k) {
         rd[k] = p.dom[k];
@@ -542,6 +583,16 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   if (e == cudaSuccess) e = cudaMemcpy(s->d_table_f, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(s->d_table_n, tn.data(), tn.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(s->d_hdr, hd.data(), sizeof(InstHdr) * n, cudaMemcpyHostToDevice);
+  if (!polard.empty()) {
+    std::vector<float> polarf(polard.size());
+    for (size_t k = 0; k < polard.size(); ++k) polarf[k] = (float)polard[k];
+    s->bytes_polar_d = polard.size() * 8;
+    s->bytes_polar_f = polarf.size() * 4;
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_polar_d, s->bytes_polar_d);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_polar_f, s->bytes_polar_f);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_polar_d, polard.data(), s->bytes_polar_d, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_polar_f, polarf.data(), s->bytes_polar_f, cudaMemcpyHostToDevice);
+  }
   if (!segd.empty()) {
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_d, segd.size() * 8);
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_f, segf.size() * 4);
@@ -570,6 +621,8 @@ extern "C" void wos_problem_set_destroy(wos_problem_set* s) {
   cudaFree(s->d_segs_d);
   cudaFree(s->d_segs_f);
   cudaFree(s->d_segs_n);
+  cudaFree(s->d_polar_d);
+  cudaFree(s->d_polar_f);
   delete s;
 }
 
@@ -593,6 +646,10 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
       inside = sqrt(s) < row[3];
     } else if (dom_kind == WOS_DOM_BOX) {
       for (int k = 0; k < dim; ++k) inside = inside && (x[k] > row[k]) && (x[k] < row[4 + k]);
+    } else if (dom_kind == WOS_DOM_POLAR) {
+      // PolarDomain.contains (geometry.py:129-134): rho < r(atan2(y, x))
+      const double th = atan2(x[1], x[0]);
+      inside = hypot(x[0], x[1]) < row[0] * (1.0 + row[1] * cos(4.0 * th) + row[2] * cos(8.0 * th));
     } else {
       const InstHdr h = hdr[i];
       const double* S = segs + 4 * (size_t)h.seg_off;
@@ -763,6 +820,14 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
         a.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
       }
     }
+  }
+  if (s->dom_kind == WOS_DOM_POLAR) {
+    // the curve table goes to shared memory when it fits (single-instance sets)
+    const bool f64 = cfg->mode == WOS_MODE_REPLAY_F64;
+    a.segs = f64 ? (const void*)s->d_polar_d : (const void*)s->d_polar_f;
+    const size_t b = f64 ? s->bytes_polar_d : s->bytes_polar_f;
+    a.seg_stage_bytes = (b + 15) / 16 * 16 <= kSegStageMax ? (int)((b + 15) / 16 * 16) : 0;
+    if (a.seg_stage_bytes && b % 16) a.seg_stage_bytes = 0;  // staged as 16-byte words
   }
   a.hdr = s->d_hdr;
   a.n_inst = s->n;

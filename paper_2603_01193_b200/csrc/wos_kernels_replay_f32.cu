@@ -26,6 +26,11 @@ const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows) 
   WOS_K(2, DOM_POLY, SRC_CONST, 0)
   WOS_K(2, DOM_POLY, SRC_SINE, 0)
   WOS_K(2, DOM_POLY, SRC_GAUSS, 0)
+  // polar star curves (geometry.PolarDomain; the linear family uses RBF2 + FOURIER5)
+  WOS_K(2, DOM_POLAR, SRC_NONE, 0)
+  WOS_K(2, DOM_POLAR, SRC_CONST, 0)
+  WOS_K(2, DOM_POLAR, SRC_RBF2, 0)
+  WOS_K(2, DOM_POLAR, SRC_GAUSS, 0)
   // 3D
   WOS_K(3, DOM_BALL, SRC_NONE, 0)
   WOS_K(3, DOM_BALL, SRC_CONST, 0)

@@ -211,6 +211,9 @@ struct Walker {
         }
         return d;
       }
+    } else if constexpr (S::DOM == DOM_POLAR) {
+      Real qx, qy;
+      return polar_query(l, a, srec, l.x[0], l.x[1], &qx, &qy);
     } else {
       return poly_dist(l, a, srec);
     }
@@ -362,9 +365,99 @@ struct Walker {
       }
 #pragma unroll
       for (int i = 0; i < DIM; ++i) q[i] = (i == axis) ? face : l.x[i];
+    } else if constexpr (S::DOM == DOM_POLAR) {
+      polar_query(l, a, nullptr, l.x[0], l.x[1], &q[0], &q[1]);
     } else {
       poly_project(l, a, q);
     }
+  }
+
+  // ---------------- polar star curves (geometry.PolarDomain) ----------------
+  __device__ static __forceinline__ Real sq2(Real x, Real y) {
+    if constexpr (S::NATIVE) return fmaf(x, x, y * y);
+    else return x * x + y * y;
+  }
+  // r(t) = r0 (1 + c1 cos 4t + c2 cos 8t) (_kernels.polar_radius_nb, _kernels.py:110-112)
+  __device__ static __forceinline__ Real polar_r(const Lane& l, const KArgs& a, Real t) {
+    // NATIVE: explicit FMAs so every kernel variant rounds alike
+    if constexpr (S::NATIVE)
+      return domp(l, a, 0) * fmaf(domp(l, a, 2), __cosf(8.0f * t), fmaf(domp(l, a, 1), __cosf(4.0f * t), 1.0f));
+    else
+      return domp(l, a, 0) * (Real(1) + domp(l, a, 1) * pcos(Real(4) * t) + domp(l, a, 2) * pcos(Real(8) * t));
+  }
+  __device__ static __forceinline__ Real polar_curve_d2(const Lane& l, const KArgs& a, Real t, Real px,
+                                                        Real py) {
+    const Real r = polar_r(l, a, t);
+    Real st, ct;
+    if constexpr (S::NATIVE) __sincosf(t, &st, &ct);
+    else psincos(t, &st, &ct);
+    if constexpr (S::NATIVE) {
+      const float dx = fmaf(r, ct, -px), dy = fmaf(r, st, -py);
+      return fmaf(dx, dx, dy * dy);
+    }
+    const Real dx = r * ct - px, dy = r * st - py;
+    return dx * dx + dy * dy;
+  }
+  // _kernels.polar_query_fast (_kernels.py:121-148, 185-219): strided scan of the curve
+  // table plus a window around the winner, then one parabolic refinement of the squared
+  // distance through the winner's neighbours; the table sample wins if it is closer.
+  // `stab` is the table staged in shared memory (or null: read through L1).
+  __device__ static __forceinline__ Real polar_query(const Lane& l, const KArgs& a, const float4* stab,
+                                                     Real px, Real py, Real* qx, Real* qy) {
+    using T2 = typename std::conditional<sizeof(Real) == 8, double2, float2>::type;
+    const T2* tab = (stab ? reinterpret_cast<const T2*>(stab) : reinterpret_cast<const T2*>(a.segs)) +
+                    l.seg_off;
+    const int n = l.n_seg, stride = l.rec_off;
+    Real best = Real(1e30);
+    int bj = 0;
+    for (int j = 0; j < n; j += stride) {
+      const T2 b = tab[j];
+      const Real dx = b.x - px, dy = b.y - py;
+      const Real d2 = sq2(dx, dy);
+      if (d2 < best) {
+        best = d2;
+        bj = j;
+      }
+    }
+    if (stride > 1) {
+      const int lo = bj - stride;
+      for (int off = 0; off <= 2 * stride; ++off) {
+        int jj = (lo + off) % n;
+        if (jj < 0) jj += n;
+        const T2 b = tab[jj];
+        const Real dx = b.x - px, dy = b.y - py;
+        const Real d2 = sq2(dx, dy);
+        if (d2 < best) {
+          best = d2;
+          bj = jj;
+        }
+      }
+    }
+    const Real h = (Real)kTwoPi / (Real)n;
+    const Real t0 = (Real)bj * h;
+    const Real fm = polar_curve_d2(l, a, t0 - h, px, py);
+    const Real fp = polar_curve_d2(l, a, t0 + h, px, py);
+    const Real denom = (fm - Real(2) * best) + fp;
+    Real shift = denom > Real(0) ? Real(0.5) * h * (fm - fp) / denom : Real(0);
+    if (shift > h) shift = h;
+    else if (shift < -h) shift = -h;
+    const Real tm = t0 + shift;
+    const Real r = polar_r(l, a, tm);
+    Real st, ct;
+    if constexpr (S::NATIVE) __sincosf(tm, &st, &ct);
+    else psincos(tm, &st, &ct);
+    const Real cx = r * ct, cy = r * st;
+    const Real dx = cx - px, dy = cy - py;
+    const Real dm = sq2(dx, dy);
+    if (best < dm) {
+      const T2 b = tab[bj];
+      *qx = b.x;
+      *qy = b.y;
+      return psqrt(best);
+    }
+    *qx = cx;
+    *qy = cy;
+    return psqrt(dm);
   }
 
   // ---------------- problem terms ----------------
@@ -509,9 +602,9 @@ struct Walker {
     } else if constexpr (S::SRC == SRC_RBF2) {
       // _kernels.py:248-259
       const Real d1x = y[0] - P[2], d1y = y[1] - P[3], d2x = y[0] - P[4], d2y = y[1] - P[5];
-      if constexpr (S::NATIVE)
-        return P[0] * fast_ex2(-(d1x * d1x + d1y * d1y) * kLog2e) +
-               P[1] * fast_ex2(-(d2x * d2x + d2y * d2y) * kLog2e);
+      if constexpr (S::NATIVE)  // explicit FMAs: identical rounding in every kernel variant
+        return fmaf(P[0], fast_ex2(-fmaf(d1x, d1x, d1y * d1y) * kLog2e),
+                    P[1] * fast_ex2(-fmaf(d2x, d2x, d2y * d2y) * kLog2e));
       else
         return P[0] * pexp(-(d1x * d1x + d1y * d1y)) + P[1] * pexp(-(d2x * d2x + d2y * d2y));
     } else if constexpr (S::SRC == SRC_SINE) {
@@ -538,10 +631,23 @@ struct Walker {
       case BND_CONST:
         return B[0];
       case BND_LINEAR:
+        // NATIVE terms use explicit FMAs so every kernel variant (single- / multi-instance)
+        // rounds alike; REPLAY keeps the reference's unfused order
+        if constexpr (S::NATIVE) {
+          if constexpr (DIM == 2) return fmaf(B[1], q[1], fmaf(B[0], q[0], B[2]));
+          else return fmaf(B[2], q[2], fmaf(B[1], q[1], fmaf(B[0], q[0], B[3])));
+        }
         if constexpr (DIM == 2) return B[0] * q[0] + B[1] * q[1] + B[2];
         else return B[0] * q[0] + B[1] * q[1] + B[2] * q[2] + B[3];
       case BND_FOURIER5: {
         if constexpr (DIM == 2) {
+          if constexpr (S::NATIVE) {
+            const float r = sqrtf(fmaf(q[0], q[0], q[1] * q[1]));
+            const float c = (r == 0.0f) ? 1.0f : q[0] / r;
+            const float s = (r == 0.0f) ? 0.0f : q[1] / r;
+            return fmaf(B[4], 2.0f * c * s,
+                        fmaf(B[3], fmaf(c, c, -(s * s)), fmaf(B[2], s, fmaf(B[1], c, B[0]))));
+          }
           const Real r = psqrt(q[0] * q[0] + q[1] * q[1]);
           const Real c = (r == Real(0)) ? Real(1) : q[0] / r;
           const Real s = (r == Real(0)) ? Real(0) : q[1] / r;
@@ -1004,12 +1110,12 @@ struct Walker {
       const InstHdr h = hdr[inst];
       if constexpr (S::NATIVE) l.k1 = a.nkey1_seed ^ h.nkey1;
       else l.ikey = h.ikey;
-      if constexpr (S::DOM == DOM_POLY) {
+      if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR) {
         l.seg_off = h.seg_off;
         l.n_seg = h.n_seg;
         l.rec_off = h.rec_off;
       }
-    } else if constexpr (S::DOM == DOM_POLY) {
+    } else if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR) {
       const InstHdr h = hdr[0];
       l.seg_off = h.seg_off;
       l.n_seg = h.n_seg;
@@ -1097,7 +1203,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   }
   // ---- stage NATIVE polygon records after the table ----
   const float4* srec = nullptr;
-  if constexpr (S::NATIVE && S::DOM == DOM_POLY) {
+  if constexpr ((S::NATIVE && S::DOM == DOM_POLY) || S::DOM == DOM_POLAR) {
     if (a.seg_stage_bytes > 0) {
       float4* dst = reinterpret_cast<float4*>(smem + a.stage_bytes);
       const float4* src = reinterpret_cast<const float4*>(a.segs);
@@ -1399,7 +1505,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             blk = (cu_k % kSlots) * 4u;
             if (j < cu_jend) {
               bool started = false;
-              if constexpr (S::NATIVE && S::ONE && !W::kScr) {
+              if constexpr (S::NATIVE && S::ONE && !W::kScr && S::DOM != DOM_POLY &&
+                            S::DOM != DOM_POLAR) {
                 if (cu_fastc) {
                   W::start_native(l, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
                                   cu_c2b + (anti ? (jr & ~1u) : jr), cu_c3);

@@ -25,7 +25,9 @@ __all__ = [
     "UnsupportedDomainError",
     "BallDomain",
     "BoxDomain",
+    "PolarDomain",
     "PolygonDomain",
+    "polar_params",
     "star_polygon",
     "domain_spec",
 ]
@@ -36,7 +38,7 @@ class ExteriorQueryError(ValueError):
 
 
 class UnsupportedDomainError(TypeError):
-    """The domain has no GPU encoding (e.g. PolarDomain, MeshDomain)."""
+    """The domain has no GPU encoding (e.g. MeshDomain)."""
 
 
 def _as_points(x, dim):
@@ -164,6 +166,61 @@ class PolygonDomain:
         return f"PolygonDomain(n={self.vertices.shape[0]})"
 
 
+class PolarDomain:
+    """Star-shaped 2D domain r(t) = r0 (1 + c1 cos 4t + c2 cos 8t) (geometry.py:83-153).
+
+    Same constructor, table and scan stride as the reference: the curve is tabulated
+    at ``table_size`` angles with numpy (so the GPU replays the reference's table bit
+    for bit) and mild curves (|c1| + |c2| <= 0.45) are scanned with stride 64.
+    """
+
+    dim = 2
+    _FAST_SCAN_LIMIT = 0.45
+
+    def __init__(self, r0=1.0, c1=0.0, c2=0.0, *, table_size=4096):
+        if r0 <= 0.0:
+            raise ValueError("r0 must be positive")
+        if abs(c1) + abs(c2) >= 1.0:
+            raise ValueError("|c1| + |c2| must be < 1 for a valid boundary")
+        self.r0, self.c1, self.c2 = float(r0), float(c1), float(c2)
+        self.table_size = int(table_size)
+        theta = np.arange(self.table_size) * (2.0 * np.pi / self.table_size)
+        r = self.radius(theta)
+        self._bx = np.ascontiguousarray(r * np.cos(theta))
+        self._by = np.ascontiguousarray(r * np.sin(theta))
+        self._stride = 64 if abs(c1) + abs(c2) <= self._FAST_SCAN_LIMIT else 1
+        self._lo = np.array([self._bx.min(), self._by.min()])
+        self._hi = np.array([self._bx.max(), self._by.max()])
+
+    def radius(self, theta):
+        theta = np.asarray(theta, dtype=np.float64)
+        return self.r0 * (1.0 + self.c1 * np.cos(4.0 * theta) + self.c2 * np.cos(8.0 * theta))
+
+    def bounding_box(self):
+        return self._lo.copy(), self._hi.copy()
+
+    def bounding_radius(self):
+        center = 0.5 * (self._lo + self._hi)
+        return float(np.hypot(self._bx - center[0], self._by - center[1]).max())
+
+    def contains(self, x):
+        pts, single = _as_points(x, 2)
+        inside = np.hypot(pts[:, 0], pts[:, 1]) < self.radius(np.arctan2(pts[:, 1], pts[:, 0]))
+        return bool(inside[0]) if single else inside
+
+    def spec(self):
+        return specs.DOM_POLAR, polar_params(self)
+
+    def __repr__(self):
+        return f"PolarDomain(r0={self.r0}, c1={self.c1}, c2={self.c2})"
+
+
+def polar_params(dom):
+    """[r0, c1, c2, stride, n, bx..., by...] of a PolarDomain (ours or the reference's)."""
+    return ((float(dom.r0), float(dom.c1), float(dom.c2), float(dom._stride), float(dom._bx.size))
+            + tuple(np.asarray(dom._bx, np.float64).tolist()) + tuple(np.asarray(dom._by, np.float64).tolist()))
+
+
 def star_polygon(alpha, beta, n_vertices=128, r0=1.0):
     """Star-shaped polygon r(t) = r0 (1 + sum_m alpha_m cos(m t) + beta_m sin(m t)), m = 2.., at
     t_j = 2 pi j / n (BASELINE config 3)."""
@@ -185,6 +242,8 @@ def domain_spec(dom):
     if name == "BallDomain" and hasattr(dom, "center") and hasattr(dom, "radius"):
         c = np.asarray(dom.center, dtype=np.float64)
         return specs.DOM_BALL, tuple(c.tolist()) + (float(dom.radius),), int(c.shape[0])
+    if name == "PolarDomain" and hasattr(dom, "_bx") and hasattr(dom, "r0"):
+        return specs.DOM_POLAR, polar_params(dom), 2
     raise UnsupportedDomainError(
-        f"{name} has no GPU encoding (supported: BallDomain, BoxDomain, PolygonDomain)"
+        f"{name} has no GPU encoding (supported: BallDomain, BoxDomain, PolygonDomain, PolarDomain)"
     )
