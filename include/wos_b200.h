@@ -87,12 +87,19 @@ typedef enum wos_mode {
  * WOS_DOM_POLYGON  closed 2D polygon, n vertices:      [n, x_0, y_0, ..., x_{n-1}, y_{n-1}]
  *                  segments v_i -> v_{(i+1) mod n}; distance = min over segments,
  *                  closest point on the first nearest segment; inside = crossing
- *                  number (even-odd) test                                       */
+ *                  number (even-odd) test
+ * WOS_DOM_MESH     closed, consistently oriented 3D triangle mesh = geometry.MeshDomain
+ *                  (geometry.py:400-580): [nv, nf, v_0.x, v_0.y, v_0.z, ..., f_0.i, f_0.j,
+ *                  f_0.k, ...] (face indices as doubles). The library builds a BVH;
+ *                  distance / closest point = nearest triangle (closest_on_triangles,
+ *                  geometry.py:259-323); inside = angle-weighted pseudo-normal test of
+ *                  the closest feature (geometry.py:480-520)                      */
 enum {
   WOS_DOM_BALL = 0,
   WOS_DOM_POLAR = 1,
   WOS_DOM_BOX = 2,
-  WOS_DOM_POLYGON = 3
+  WOS_DOM_POLYGON = 3,
+  WOS_DOM_MESH = 4
 };
 
 /* ---- source kinds (f in the reference's  Laplacian(u) = f  convention) */

@@ -144,10 +144,114 @@ static double polar_query(const double* P, double px, double py, double* qx, dou
   return sqrt(dm);
 }
 
+/* MeshDomain (geometry.py:259-323, 470-533): closest point on a triangle with its
+ * feature region, the reference's operation order and region priority */
+enum { R_A, R_B, R_C, R_AB, R_BC, R_CA, R_FACE };
+static double dot3(const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; }
+static double clip01(double t) { return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t); }
+static double sdiv(double n, double d) { return n / (d == 0.0 ? 1.0 : d); }
+static int closest_tri(const double* p, const double* a, const double* b, const double* c, double* q) {
+  double ab[3], ac[3], ap[3], bp[3], cp[3];
+  for (int i = 0; i < 3; ++i) {
+    ab[i] = b[i] - a[i]; ac[i] = c[i] - a[i]; ap[i] = p[i] - a[i]; bp[i] = p[i] - b[i]; cp[i] = p[i] - c[i];
+  }
+  const double d1 = dot3(ab, ap), d2 = dot3(ac, ap), d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+  const double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+  const double vc = d1 * d4 - d3 * d2, vb = d5 * d2 - d1 * d6, va = d3 * d6 - d5 * d4;
+  if (d1 <= 0.0 && d2 <= 0.0) { for (int i = 0; i < 3; ++i) q[i] = a[i]; return R_A; }
+  if (d3 >= 0.0 && d4 <= d3) { for (int i = 0; i < 3; ++i) q[i] = b[i]; return R_B; }
+  if (d6 >= 0.0 && d5 <= d6) { for (int i = 0; i < 3; ++i) q[i] = c[i]; return R_C; }
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    const double t = clip01(sdiv(d1, d1 - d3));
+    for (int i = 0; i < 3; ++i) q[i] = a[i] + ab[i] * t;
+    return R_AB;
+  }
+  if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+    const double t = clip01(sdiv(d4 - d3, (d4 - d3) + (d5 - d6)));
+    for (int i = 0; i < 3; ++i) q[i] = b[i] + (c[i] - b[i]) * t;
+    return R_BC;
+  }
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    const double t = clip01(sdiv(d2, d2 - d6));
+    for (int i = 0; i < 3; ++i) q[i] = a[i] + ac[i] * t;
+    return R_CA;
+  }
+  const double den = va + vb + vc, v = sdiv(vb, den), w = sdiv(vc, den);
+  for (int i = 0; i < 3; ++i) q[i] = a[i] + ab[i] * v + ac[i] * w;
+  return R_FACE;
+}
+/* brute-force nearest triangle (MeshDomain._closest_brute: first index attaining the minimum) */
+static double mesh_nearest(const double* P, const double* x, double* q, int64_t* tri, int* reg) {
+  const int64_t nv = (int64_t)P[0], nf = (int64_t)P[1];
+  const double *V = P + 2, *F = P + 2 + 3 * nv;
+  double best = INFINITY;
+  for (int64_t t = 0; t < nf; ++t) {
+    double qq[3];
+    const int r = closest_tri(x, V + 3 * (int64_t)F[3 * t], V + 3 * (int64_t)F[3 * t + 1],
+                              V + 3 * (int64_t)F[3 * t + 2], qq);
+    const double df[3] = {qq[0] - x[0], qq[1] - x[1], qq[2] - x[2]};
+    const double d2 = dot3(df, df);
+    if (d2 < best) {
+      best = d2; q[0] = qq[0]; q[1] = qq[1]; q[2] = qq[2]; *tri = t; *reg = r;
+    }
+  }
+  return best;
+}
+/* MeshDomain._build_normals + _feature_normal (geometry.py:434-508) for one query */
+static void mesh_feature_normal(const double* P, int64_t t, int reg, double* n) {
+  const int64_t nv = (int64_t)P[0], nf = (int64_t)P[1];
+  const double *V = P + 2, *F = P + 2 + 3 * nv;
+  const int64_t id[3] = {(int64_t)F[3 * t], (int64_t)F[3 * t + 1], (int64_t)F[3 * t + 2]};
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t s = 0; s < nf; ++s) {
+    const int64_t js[3] = {(int64_t)F[3 * s], (int64_t)F[3 * s + 1], (int64_t)F[3 * s + 2]};
+    double e1[3], e2[3], fn[3];
+    for (int c = 0; c < 3; ++c) { e1[c] = V[3 * js[1] + c] - V[3 * js[0] + c]; e2[c] = V[3 * js[2] + c] - V[3 * js[0] + c]; }
+    fn[0] = e1[1] * e2[2] - e1[2] * e2[1];
+    fn[1] = e1[2] * e2[0] - e1[0] * e2[2];
+    fn[2] = e1[0] * e2[1] - e1[1] * e2[0];
+    const double len = sqrt(fn[0] * fn[0] + fn[1] * fn[1] + fn[2] * fn[2]);
+    for (int c = 0; c < 3; ++c) fn[c] /= len;
+    if (reg == R_FACE) {
+      if (s == t) { for (int c = 0; c < 3; ++c) n[c] = fn[c]; return; }
+      continue;
+    }
+    if (reg <= R_C) { /* angle-weighted vertex normal */
+      const int64_t vid = id[reg];
+      for (int l = 0; l < 3; ++l) {
+        if (js[l] != vid) continue;
+        double a1[3], a2[3];
+        for (int c = 0; c < 3; ++c) {
+          a1[c] = V[3 * js[(l + 1) % 3] + c] - V[3 * js[l] + c];
+          a2[c] = V[3 * js[(l + 2) % 3] + c] - V[3 * js[l] + c];
+        }
+        const double cs = dot3(a1, a2) / (sqrt(dot3(a1, a1)) * sqrt(dot3(a2, a2)));
+        const double ang = acos(cs < -1.0 ? -1.0 : (cs > 1.0 ? 1.0 : cs));
+        for (int c = 0; c < 3; ++c) acc[c] += ang * fn[c];
+      }
+    } else { /* edge normal: faces sharing the edge */
+      const int l0 = reg == R_AB ? 0 : (reg == R_BC ? 1 : 2);
+      const int64_t u = id[l0], w = id[(l0 + 1) % 3];
+      for (int l = 0; l < 3; ++l) {
+        const int64_t a = js[l], b = js[(l + 1) % 3];
+        if ((a == u && b == w) || (a == w && b == u))
+          for (int c = 0; c < 3; ++c) acc[c] += fn[c];
+      }
+    }
+  }
+  const double len = sqrt(dot3(acc, acc));
+  for (int c = 0; c < 3; ++c) n[c] = acc[c] / (len == 0.0 ? 1.0 : len);
+}
+
 static double query(const wos_problem* pb, const double* x, double* q) {
   const int dim = pb->dim;
   const double* P = pb->dom;
   if (pb->dom_kind == WOS_DOM_POLAR) return polar_query(P, x[0], x[1], &q[0], &q[1]);
+  if (pb->dom_kind == WOS_DOM_MESH) {
+    int64_t t;
+    int reg;
+    return sqrt(mesh_nearest(P, x, q, &t, &reg));
+  }
   if (pb->dom_kind == WOS_DOM_BALL) {
     /* geometry.py:196-206 */
     double u[3], s = 0.0;
@@ -197,6 +301,14 @@ static double query(const wos_problem* pb, const double* x, double* q) {
 int oracle_contains(const wos_problem* pb, const double* x) {
   const int dim = pb->dim;
   const double* P = pb->dom;
+  if (pb->dom_kind == WOS_DOM_MESH) { /* MeshDomain.signed_distance < 0 (geometry.py:510-525) */
+    double q[3], n[3];
+    int64_t t;
+    int reg;
+    mesh_nearest(P, x, q, &t, &reg);
+    mesh_feature_normal(P, t, reg, n);
+    return (x[0] - q[0]) * n[0] + (x[1] - q[1]) * n[1] + (x[2] - q[2]) * n[2] < 0.0;
+  }
   if (pb->dom_kind == WOS_DOM_POLAR) { /* geometry.py:129-134 */
     const double th = atan2(x[1], x[0]);
     return hypot(x[0], x[1]) < polar_r(P, th);

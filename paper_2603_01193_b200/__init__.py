@@ -11,7 +11,15 @@ hand-written sm_100a CUDA kernels in ``libwos_b200.so`` behind the C ABI of
 from .cache import CacheShapeError, EstimateCache, cache_update, export_csv
 from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, estimate_tensors
 from .engine import UnsupportedProblemError
-from .geometry import BallDomain, BoxDomain, ExteriorQueryError, PolarDomain, PolygonDomain, star_polygon
+from .geometry import (
+    BallDomain,
+    BoxDomain,
+    ExteriorQueryError,
+    MeshDomain,
+    PolarDomain,
+    PolygonDomain,
+    star_polygon,
+)
 from .walker import (
     MajorantViolationError,
     ScreenedProblem,
@@ -38,6 +46,7 @@ __all__ = [
     "ExteriorQueryError",
     "MajorantViolationError",
     "PointEstimate",
+    "MeshDomain",
     "PolarDomain",
     "PolygonDomain",
     "Problem",

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -16,6 +17,9 @@
 #include "wos_kernels.h"
 #include "wos_rng.cuh"
 #include "wos_types.h"
+#include "wos_mesh.cuh"
+#include <map>
+#include <utility>
 
 using namespace wos;
 
@@ -84,6 +88,11 @@ struct wos_problem_set {
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
   float4* d_segs_n = nullptr;             // NATIVE: per polygon n + 1 records {v_k, e_k/|e_k|^2}
   size_t bytes_segs_n = 0;
+  MeshNode<double>* d_mesh_nodes_d = nullptr;  // MESH: BVH nodes and leaf-ordered triangles
+  MeshNode<float>* d_mesh_nodes_f = nullptr;
+  double* d_mesh_tris_d = nullptr;
+  float* d_mesh_tris_f = nullptr;
+  double* d_mesh_fnorm = nullptr;         //       feature normals (21 per triangle), fp64
   double* d_polar_d = nullptr;            // POLAR: per instance n (bx, by) pairs, fp64
   float* d_polar_f = nullptr;             //        the same, fp32
   size_t bytes_polar_d = 0, bytes_polar_f = 0;
@@ -199,6 +208,19 @@ static int validate(const wos_problem& p) {
       if (nv < 3 || p.n_dom != 1 + 2 * nv) return fail(WOS_ERR_INVALID, "polygon parameter count mismatch");
       break;
     }
+    case WOS_DOM_MESH: {
+      if (p.dim != 3) return fail(WOS_ERR_INVALID, "mesh domains are 3D");
+      if (p.n_dom < 2) return fail(WOS_ERR_INVALID, "mesh needs [nv, nf, vertices, faces]");
+      const int64_t nv = (int64_t)p.dom[0], nf = (int64_t)p.dom[1];
+      if (nv < 4 || nf < 4) return fail(WOS_ERR_INVALID, "mesh needs >= 4 vertices and faces");
+      if (p.n_dom != 2 + 3 * nv + 3 * nf) return fail(WOS_ERR_INVALID, "mesh parameter count mismatch");
+      for (int64_t k = 0; k < 3 * nf; ++k) {
+        const double f = p.dom[2 + 3 * nv + k];
+        if (!(f >= 0.0 && f < (double)nv) || f != floor(f))
+          return fail(WOS_ERR_INVALID, "face index out of range");
+      }
+      break;
+    }
     case WOS_DOM_POLAR: {
       if (p.dim != 2) return fail(WOS_ERR_INVALID, "polar domains are 2D");
       if (p.n_dom != 3 && p.n_dom < 5) return fail(WOS_ERR_INVALID, "polar domain needs [r0, c1, c2(, stride, n, table)]");
@@ -297,6 +319,147 @@ static int validate(const wos_problem& p) {
       break;
     default:
       return fail(WOS_ERR_UNSUPPORTED, "unknown boundary kind %d", p.bnd_kind);
+  }
+  return WOS_OK;
+}
+
+// ---- closed triangle meshes (geometry.MeshDomain, geometry.py:400-580) ----
+// Feature normals as in MeshDomain._build_normals (geometry.py:434-468): unit face
+// normals, angle-weighted vertex normals, edge normals from the two adjacent faces;
+// a median-split BVH (largest box extent, leaves of <= 8 triangles, geometry.py:326-358)
+// laid out depth first with the left child next to its parent.
+struct MeshBuild {
+  std::vector<MeshNode<double>> nodes;
+  std::vector<double> tris;   // leaf order, 9 per triangle
+  std::vector<double> fnorm;  // leaf order, 21 per triangle
+};
+
+static int build_mesh(const wos_problem& p, MeshBuild* out) {
+  const int64_t nv = (int64_t)p.dom[0], nf = (int64_t)p.dom[1];
+  const double* V = p.dom + 2;
+  const double* F = p.dom + 2 + 3 * nv;
+  auto vtx = [&](int64_t i, int c) { return V[3 * i + c]; };
+  std::vector<double> fn(3 * nf), vn(3 * nv, 0.0);
+  std::map<std::pair<int64_t, int64_t>, std::array<double, 3>> en;
+  for (int64_t t = 0; t < nf; ++t) {
+    const int64_t id[3] = {(int64_t)F[3 * t], (int64_t)F[3 * t + 1], (int64_t)F[3 * t + 2]};
+    double e1[3], e2[3], n[3];
+    for (int c = 0; c < 3; ++c) {
+      e1[c] = vtx(id[1], c) - vtx(id[0], c);
+      e2[c] = vtx(id[2], c) - vtx(id[0], c);
+    }
+    n[0] = e1[1] * e2[2] - e1[2] * e2[1];
+    n[1] = e1[2] * e2[0] - e1[0] * e2[2];
+    n[2] = e1[0] * e2[1] - e1[1] * e2[0];
+    const double len = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    if (len == 0.0) return fail(WOS_ERR_INVALID, "degenerate triangle in mesh");
+    for (int c = 0; c < 3; ++c) fn[3 * t + c] = n[c] / len;
+    for (int l = 0; l < 3; ++l) {
+      double a1[3], a2[3];
+      for (int c = 0; c < 3; ++c) {
+        a1[c] = vtx(id[(l + 1) % 3], c) - vtx(id[l], c);
+        a2[c] = vtx(id[(l + 2) % 3], c) - vtx(id[l], c);
+      }
+      const double dt = a1[0] * a2[0] + a1[1] * a2[1] + a1[2] * a2[2];
+      const double ln = sqrt(a1[0] * a1[0] + a1[1] * a1[1] + a1[2] * a1[2]) *
+                        sqrt(a2[0] * a2[0] + a2[1] * a2[1] + a2[2] * a2[2]);
+      const double ang = acos(std::min(1.0, std::max(-1.0, dt / ln)));
+      for (int c = 0; c < 3; ++c) vn[3 * id[l] + c] += ang * fn[3 * t + c];
+    }
+    for (int l = 0; l < 3; ++l) {
+      int64_t u = id[l], w = id[(l + 1) % 3];
+      auto key = u < w ? std::make_pair(u, w) : std::make_pair(w, u);
+      auto it = en.find(key);
+      if (it == en.end()) it = en.emplace(key, std::array<double, 3>{0.0, 0.0, 0.0}).first;
+      for (int c = 0; c < 3; ++c) it->second[c] += fn[3 * t + c];
+    }
+  }
+  auto unit = [](double* v) {
+    const double l = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    const double d = l == 0.0 ? 1.0 : l;
+    for (int c = 0; c < 3; ++c) v[c] /= d;
+  };
+  for (int64_t i = 0; i < nv; ++i) unit(&vn[3 * i]);
+  for (auto& kv : en) unit(kv.second.data());
+  // BVH over triangle boxes
+  std::vector<double> lo(3 * nf), hi(3 * nf), cen(3 * nf);
+  for (int64_t t = 0; t < nf; ++t)
+    for (int c = 0; c < 3; ++c) {
+      double mn = 1e300, mx = -1e300;
+      for (int l = 0; l < 3; ++l) {
+        const double v = vtx((int64_t)F[3 * t + l], c);
+        mn = std::min(mn, v);
+        mx = std::max(mx, v);
+      }
+      lo[3 * t + c] = mn;
+      hi[3 * t + c] = mx;
+      cen[3 * t + c] = 0.5 * (mn + mx);
+    }
+  std::vector<int64_t> order(nf);
+  for (int64_t t = 0; t < nf; ++t) order[t] = t;
+  out->nodes.clear();
+  std::vector<int64_t> leaf_order;
+  leaf_order.reserve(nf);
+  // iterative DFS build: (start, stop, parent slot to patch with the right child)
+  struct Job { int64_t start, stop; int64_t patch; };
+  std::vector<Job> todo{{0, nf, -1}};
+  while (!todo.empty()) {
+    Job j = todo.back();
+    todo.pop_back();
+    const int idx = (int)out->nodes.size();
+    if (j.patch >= 0) out->nodes[j.patch].right = idx;
+    MeshNode<double> nd;
+    for (int c = 0; c < 3; ++c) {
+      nd.lo[c] = 1e300;
+      nd.hi[c] = -1e300;
+    }
+    for (int64_t k = j.start; k < j.stop; ++k)
+      for (int c = 0; c < 3; ++c) {
+        nd.lo[c] = std::min(nd.lo[c], lo[3 * order[k] + c]);
+        nd.hi[c] = std::max(nd.hi[c], hi[3 * order[k] + c]);
+      }
+    nd.right = -1;
+    nd.first = 0;
+    nd.count = 0;
+    nd.pad = 0;
+    if (j.stop - j.start <= 8) {
+      nd.first = (int32_t)leaf_order.size();
+      nd.count = (int32_t)(j.stop - j.start);
+      for (int64_t k = j.start; k < j.stop; ++k) leaf_order.push_back(order[k]);
+      out->nodes.push_back(nd);
+      continue;
+    }
+    int axis = 0;
+    for (int c = 1; c < 3; ++c)
+      if (nd.hi[c] - nd.lo[c] > nd.hi[axis] - nd.lo[axis]) axis = c;
+    const int64_t mid = j.start + (j.stop - j.start) / 2;
+    std::nth_element(order.begin() + j.start, order.begin() + mid, order.begin() + j.stop,
+                     [&](int64_t x, int64_t y) {
+                       return cen[3 * x + axis] < cen[3 * y + axis] ||
+                              (cen[3 * x + axis] == cen[3 * y + axis] && x < y);
+                     });
+    out->nodes.push_back(nd);
+    // right subtree is built after the left one (it sits after it in DFS order)
+    todo.push_back({mid, j.stop, (int64_t)idx});
+    todo.push_back({j.start, mid, -1});
+  }
+  out->tris.resize(9 * (size_t)nf);
+  out->fnorm.resize(21 * (size_t)nf);
+  for (int64_t k = 0; k < nf; ++k) {
+    const int64_t t = leaf_order[k];
+    const int64_t id[3] = {(int64_t)F[3 * t], (int64_t)F[3 * t + 1], (int64_t)F[3 * t + 2]};
+    for (int l = 0; l < 3; ++l)
+      for (int c = 0; c < 3; ++c) out->tris[9 * k + 3 * l + c] = vtx(id[l], c);
+    double* N = &out->fnorm[21 * k];
+    for (int c = 0; c < 3; ++c) N[c] = fn[3 * t + c];
+    for (int l = 0; l < 3; ++l)
+      for (int c = 0; c < 3; ++c) N[3 + 3 * l + c] = vn[3 * id[l] + c];
+    for (int l = 0; l < 3; ++l) {  // edges ab, bc, ca
+      int64_t u = id[l], w = id[(l + 1) % 3];
+      auto key = u < w ? std::make_pair(u, w) : std::make_pair(w, u);
+      const auto& e = en[key];
+      for (int c = 0; c < 3; ++c) N[12 + 3 * l + c] = e[c];
+    }
   }
   return WOS_OK;
 }
@@ -401,6 +564,8 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   std::vector<double> segd;
   std::vector<float4> segn;
   std::vector<double> polard;  // POLAR tables, (bx, by) pairs
+  std::vector<MeshNode<double>> mnodes;  // MESH: all instances' BVHs, triangles, normals
+  std::vector<double> mtris, mfnorm;
   for (int i = 0; i < n; ++i) {
     const wos_problem& p = probs[i];
     double* rd = td.data() + (size_t)i * stride;
@@ -412,6 +577,19 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     if (p.dom_kind == WOS_DOM_BALL) {
       for (int k = 0; k < dim; ++k) rd[k] = p.dom[k];
       rd[3] = p.dom[dim];
+    } else if (p.dom_kind == WOS_DOM_MESH) {
+      MeshBuild mb;
+      const int r = build_mesh(p, &mb);
+      if (r) {
+        delete s;
+        return r;
+      }
+      hd[i].seg_off = (int)mnodes.size();
+      hd[i].n_seg = (int)mb.nodes.size();
+      hd[i].rec_off = (int)(mtris.size() / 9);
+      mnodes.insert(mnodes.end(), mb.nodes.begin(), mb.nodes.end());
+      mtris.insert(mtris.end(), mb.tris.begin(), mb.tris.end());
+      mfnorm.insert(mfnorm.end(), mb.fnorm.begin(), mb.fnorm.end());
     } else if (p.dom_kind == WOS_DOM_POLAR) {
       // geometry.py:97-112: the curve tabulated at n angles, strided scan for mild curves
       const double r0 = p.dom[0], c1 = p.dom[1], c2 = p.dom[2];
@@ -583,6 +761,34 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   if (e == cudaSuccess) e = cudaMemcpy(s->d_table_f, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(s->d_table_n, tn.data(), tn.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(s->d_hdr, hd.data(), sizeof(InstHdr) * n, cudaMemcpyHostToDevice);
+  if (!mnodes.empty()) {
+    std::vector<MeshNode<float>> nf(mnodes.size());
+    for (size_t k = 0; k < mnodes.size(); ++k) {
+      for (int c = 0; c < 3; ++c) {
+        // round the boxes outward so fp32 pruning never drops a closer triangle
+        nf[k].lo[c] = nextafterf((float)mnodes[k].lo[c], -INFINITY);
+        nf[k].hi[c] = nextafterf((float)mnodes[k].hi[c], INFINITY);
+      }
+      nf[k].right = mnodes[k].right;
+      nf[k].first = mnodes[k].first;
+      nf[k].count = mnodes[k].count;
+      nf[k].pad = 0;
+    }
+    std::vector<float> tf(mtris.size());
+    for (size_t k = 0; k < mtris.size(); ++k) tf[k] = (float)mtris[k];
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_mesh_nodes_d, mnodes.size() * sizeof(MeshNode<double>));
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_mesh_nodes_f, nf.size() * sizeof(MeshNode<float>));
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_mesh_tris_d, mtris.size() * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_mesh_tris_f, tf.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_mesh_fnorm, mfnorm.size() * 8);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->d_mesh_nodes_d, mnodes.data(), mnodes.size() * sizeof(MeshNode<double>), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->d_mesh_nodes_f, nf.data(), nf.size() * sizeof(MeshNode<float>), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_mesh_tris_d, mtris.data(), mtris.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_mesh_tris_f, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_mesh_fnorm, mfnorm.data(), mfnorm.size() * 8, cudaMemcpyHostToDevice);
+  }
   if (!polard.empty()) {
     std::vector<float> polarf(polard.size());
     for (size_t k = 0; k < polard.size(); ++k) polarf[k] = (float)polard[k];
@@ -623,6 +829,11 @@ extern "C" void wos_problem_set_destroy(wos_problem_set* s) {
   cudaFree(s->d_segs_n);
   cudaFree(s->d_polar_d);
   cudaFree(s->d_polar_f);
+  cudaFree(s->d_mesh_nodes_d);
+  cudaFree(s->d_mesh_nodes_f);
+  cudaFree(s->d_mesh_tris_d);
+  cudaFree(s->d_mesh_tris_f);
+  cudaFree(s->d_mesh_fnorm);
   delete s;
 }
 
@@ -633,7 +844,10 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
                                     const int32_t* __restrict__ inst, const double* __restrict__ table,
                                     int stride, const InstHdr* __restrict__ hdr,
                                     const double* __restrict__ segs, int dim, int dom_kind,
-                                    unsigned long long* first, int64_t idx_base) {
+                                    unsigned long long* first, int64_t idx_base,
+                                    const MeshNode<double>* __restrict__ mnodes,
+                                    const double* __restrict__ mtris,
+                                    const double* __restrict__ mfnorm) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int i = inst ? inst[p] : 0;
@@ -646,6 +860,16 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
       inside = sqrt(s) < row[3];
     } else if (dom_kind == WOS_DOM_BOX) {
       for (int k = 0; k < dim; ++k) inside = inside && (x[k] > row[k]) && (x[k] < row[4 + k]);
+    } else if (dom_kind == WOS_DOM_MESH) {
+      // MeshDomain.contains (geometry.py:510-525): the closest feature's pseudo-normal
+      const InstHdr h = hdr[i];
+      double q[3];
+      int reg, tri;
+      mesh_nearest<double>(mnodes + h.seg_off, mtris + 9 * (size_t)h.rec_off, x, q, &reg, &tri);
+      const double* N = mfnorm + 21 * ((size_t)h.rec_off + tri);
+      const double* nn = reg == MREG_FACE ? N : (reg <= MREG_C ? N + 3 + 3 * reg : N + 12 + 3 * (reg - MREG_AB));
+      const double dot = (x[0] - q[0]) * nn[0] + (x[1] - q[1]) * nn[1] + (x[2] - q[2]) * nn[2];
+      inside = dot < 0.0;
     } else if (dom_kind == WOS_DOM_POLAR) {
       // PolarDomain.contains (geometry.py:129-134): rho < r(atan2(y, x))
       const double th = atan2(x[1], x[0]);
@@ -673,7 +897,8 @@ static int launch_interior(wos_context* c, const wos_problem_set* s, int64_t n, 
   if (n <= 0) return WOS_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->num_sms * 8);
   wos_interior_kernel<<<blocks, 256, 0, st>>>(n, pts, inst, s->d_table_d, s->stride, s->d_hdr,
-                                              s->d_segs_d, s->dim, s->dom_kind, c->d_exterior, idx_base);
+                                              s->d_segs_d, s->dim, s->dom_kind, c->d_exterior, idx_base,
+                                              s->d_mesh_nodes_d, s->d_mesh_tris_d, s->d_mesh_fnorm);
   CUDA_TRY(cudaGetLastError());
   return WOS_OK;
 }
@@ -820,6 +1045,12 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
         a.rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
       }
     }
+  }
+  if (s->dom_kind == WOS_DOM_MESH) {
+    const bool f64 = cfg->mode == WOS_MODE_REPLAY_F64;
+    a.segs = f64 ? (const void*)s->d_mesh_tris_d : (const void*)s->d_mesh_tris_f;
+    a.nodes = f64 ? (const void*)s->d_mesh_nodes_d : (const void*)s->d_mesh_nodes_f;
+    a.seg_stage_bytes = 0;
   }
   if (s->dom_kind == WOS_DOM_POLAR) {
     // the curve table goes to shared memory when it fits (single-instance sets)

@@ -40,6 +40,12 @@ const void* get_kernel_replay_f64(int dim, int dom, int src, int sk, bool rows) 
   WOS_K(3, DOM_BOX, SRC_CONST, 0)
   WOS_K(3, DOM_BOX, SRC_SINE, 0)
   WOS_K(3, DOM_BOX, SRC_GAUSS, 0)
+  // closed triangle meshes (geometry.MeshDomain)
+  WOS_K(3, DOM_MESH, SRC_NONE, 0)
+  WOS_K(3, DOM_MESH, SRC_CONST, 0)
+  WOS_K(3, DOM_MESH, SRC_GAUSS, 0)
+  WOS_K(3, DOM_MESH, SRC_SCR_CONST, 0)
+  WOS_K(3, DOM_MESH, SRC_SCR_VC, 0)
   // delta tracking (screened walks)
   WOS_K(3, DOM_BALL, SRC_SCR_CONST, 0)
   WOS_K(3, DOM_BALL, SRC_SCR_VC, 0)

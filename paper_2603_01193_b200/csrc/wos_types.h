@@ -4,7 +4,7 @@
 
 namespace wos {
 
-enum : int { DOM_BALL = 0, DOM_POLAR = 1, DOM_BOX = 2, DOM_POLY = 3 };
+enum : int { DOM_BALL = 0, DOM_POLAR = 1, DOM_BOX = 2, DOM_POLY = 3, DOM_MESH = 4 };
 enum : int { SRC_NONE = 0, SRC_CONST = 1, SRC_RBF2 = 2, SRC_SINE = 3, SRC_GAUSS = 4 };
 // delta-tracking (screened) walks: the "source" slot selects the transformed coefficients
 enum : int { SRC_SCR_CONST = 5, SRC_SCR_VC = 6 };
@@ -61,7 +61,8 @@ struct KArgs {
   // ---- problem set (device) ----
   const void* table;    // Real rows [n_inst][stride]
   const InstHdr* hdr;   // [n_inst]
-  const void* segs;     // polygon segments (mode-specific layout)
+  const void* segs;     // polygon segments / polar tables / mesh triangles (mode-specific layout)
+  const void* nodes;    // mesh BVH nodes (MeshNode<Real>)
   int32_t n_inst;
   int32_t stride;       // Real elements per table row
   int32_t bnd_off;      // boundary params offset in a row

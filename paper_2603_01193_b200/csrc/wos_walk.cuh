@@ -40,6 +40,7 @@
 #include <type_traits>
 
 #include "wos_rng.cuh"
+#include "wos_mesh.cuh"
 #include "wos_types.h"
 
 namespace wos {
@@ -214,6 +215,10 @@ struct Walker {
     } else if constexpr (S::DOM == DOM_POLAR) {
       Real qx, qy;
       return polar_query(l, a, srec, l.x[0], l.x[1], &qx, &qy);
+    } else if constexpr (S::DOM == DOM_MESH) {
+      // MeshDomain.boundary_query (geometry.py:527-533): |p - closest|
+      Real q[3];
+      return psqrt(mesh_d2(l, a, q));
     } else {
       return poly_dist(l, a, srec);
     }
@@ -367,9 +372,19 @@ struct Walker {
       for (int i = 0; i < DIM; ++i) q[i] = (i == axis) ? face : l.x[i];
     } else if constexpr (S::DOM == DOM_POLAR) {
       polar_query(l, a, nullptr, l.x[0], l.x[1], &q[0], &q[1]);
+    } else if constexpr (S::DOM == DOM_MESH) {
+      mesh_d2(l, a, q);
     } else {
       poly_project(l, a, q);
     }
+  }
+
+  // ---------------- closed triangle meshes (geometry.MeshDomain) ----------------
+  __device__ static __forceinline__ Real mesh_d2(const Lane& l, const KArgs& a, Real* q) {
+    int reg, tri;
+    return mesh_nearest<Real>(reinterpret_cast<const MeshNode<Real>*>(a.nodes) + l.seg_off,
+                              reinterpret_cast<const Real*>(a.segs) + 9 * (size_t)l.rec_off, l.x, q,
+                              &reg, &tri);
   }
 
   // ---------------- polar star curves (geometry.PolarDomain) ----------------
@@ -1110,12 +1125,12 @@ struct Walker {
       const InstHdr h = hdr[inst];
       if constexpr (S::NATIVE) l.k1 = a.nkey1_seed ^ h.nkey1;
       else l.ikey = h.ikey;
-      if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR) {
+      if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR || S::DOM == DOM_MESH) {
         l.seg_off = h.seg_off;
         l.n_seg = h.n_seg;
         l.rec_off = h.rec_off;
       }
-    } else if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR) {
+    } else if constexpr (S::DOM == DOM_POLY || S::DOM == DOM_POLAR || S::DOM == DOM_MESH) {
       const InstHdr h = hdr[0];
       l.seg_off = h.seg_off;
       l.n_seg = h.n_seg;
@@ -1506,7 +1521,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             if (j < cu_jend) {
               bool started = false;
               if constexpr (S::NATIVE && S::ONE && !W::kScr && S::DOM != DOM_POLY &&
-                            S::DOM != DOM_POLAR) {
+                            S::DOM != DOM_POLAR && S::DOM != DOM_MESH) {
                 if (cu_fastc) {
                   W::start_native(l, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
                                   cu_c2b + (anti ? (jr & ~1u) : jr), cu_c3);

@@ -25,8 +25,10 @@ __all__ = [
     "UnsupportedDomainError",
     "BallDomain",
     "BoxDomain",
+    "MeshDomain",
     "PolarDomain",
     "PolygonDomain",
+    "mesh_params",
     "polar_params",
     "star_polygon",
     "domain_spec",
@@ -38,7 +40,7 @@ class ExteriorQueryError(ValueError):
 
 
 class UnsupportedDomainError(TypeError):
-    """The domain has no GPU encoding (e.g. MeshDomain)."""
+    """The domain has no GPU encoding."""
 
 
 def _as_points(x, dim):
@@ -215,6 +217,55 @@ class PolarDomain:
         return f"PolarDomain(r0={self.r0}, c1={self.c1}, c2={self.c2})"
 
 
+class MeshDomain:
+    """Closed, consistently oriented triangle mesh (3D), geometry.MeshDomain (geometry.py:400-580).
+
+    Same constructor as the reference. Distances, closest points and the inside test
+    (angle-weighted pseudo-normal of the closest feature) run on the GPU over a BVH the
+    library builds (WOS_DOM_MESH); start points are validated there by ``estimate``.
+    """
+
+    dim = 3
+
+    def __init__(self, vertices, faces):
+        v = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64))
+        f = np.ascontiguousarray(np.asarray(faces, dtype=np.int64))
+        if v.ndim != 2 or v.shape[1] != 3:
+            raise ValueError("vertices must be (n, 3)")
+        if f.ndim != 2 or f.shape[1] != 3:
+            raise ValueError("faces must be (m, 3) triangles")
+        if f.min() < 0 or f.max() >= v.shape[0]:
+            raise ValueError("face index out of range")
+        tri = v[f]
+        if np.any(np.linalg.norm(np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]), axis=1) == 0.0):
+            raise ValueError("degenerate triangle in mesh")
+        self.vertices = v
+        self.faces = f
+        self._lo = v.min(axis=0)
+        self._hi = v.max(axis=0)
+
+    def bounding_box(self):
+        return self._lo.copy(), self._hi.copy()
+
+    def bounding_radius(self):
+        center = 0.5 * (self._lo + self._hi)
+        return float(np.linalg.norm(self.vertices - center, axis=1).max())
+
+    def spec(self):
+        return specs.DOM_MESH, mesh_params(self)
+
+    def __repr__(self):
+        return f"MeshDomain({self.vertices.shape[0]} vertices, {self.faces.shape[0]} faces)"
+
+
+def mesh_params(dom):
+    """[nv, nf, vertices..., faces...] of a MeshDomain (ours or the reference's)."""
+    v = np.asarray(dom.vertices, dtype=np.float64)
+    f = np.asarray(dom.faces, dtype=np.int64)
+    return (float(v.shape[0]), float(f.shape[0])) + tuple(v.ravel().tolist()) + tuple(
+        f.astype(np.float64).ravel().tolist())
+
+
 def polar_params(dom):
     """[r0, c1, c2, stride, n, bx..., by...] of a PolarDomain (ours or the reference's)."""
     return ((float(dom.r0), float(dom.c1), float(dom.c2), float(dom._stride), float(dom._bx.size))
@@ -244,6 +295,9 @@ def domain_spec(dom):
         return specs.DOM_BALL, tuple(c.tolist()) + (float(dom.radius),), int(c.shape[0])
     if name == "PolarDomain" and hasattr(dom, "_bx") and hasattr(dom, "r0"):
         return specs.DOM_POLAR, polar_params(dom), 2
+    if name == "MeshDomain" and hasattr(dom, "vertices") and hasattr(dom, "faces"):
+        return specs.DOM_MESH, mesh_params(dom), 3
     raise UnsupportedDomainError(
-        f"{name} has no GPU encoding (supported: BallDomain, BoxDomain, PolygonDomain, PolarDomain)"
+        f"{name} has no GPU encoding (supported: BallDomain, BoxDomain, PolygonDomain, PolarDomain, "
+        "MeshDomain)"
     )

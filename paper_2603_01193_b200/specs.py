@@ -41,6 +41,7 @@ DOM_BALL = 0
 DOM_POLAR = 1
 DOM_BOX = 2
 DOM_POLYGON = 3
+DOM_MESH = 4
 
 SRC_NAMES = {SRC_NONE: "none", SRC_CONST: "const", SRC_RBF2: "rbf2", SRC_SINE: "sine", SRC_GAUSS: "gauss",
              SRC_SCREENED_CONST: "screened_const", SRC_SCREENED_VC: "screened_vc"}
