@@ -111,23 +111,35 @@ static double polar_curve_d2(const double* P, double t, double px, double py) {
   const double dx = r * cos(t) - px, dy = r * sin(t) - py;
   return dx * dx + dy * dy;
 }
+/* the product's NATIVE form scans coarse to fine (wos_walk.cuh polar_query); the
+ * drivers set this for native walks */
+static int g_polar_native = 0;
+static void polar_probe(const double* bx, const double* by, int n, int jj, double px, double py,
+                        double* best, int* bj) {
+  jj = jj < 0 ? jj + n : (jj >= n ? jj - n : jj);
+  const double dx = bx[jj] - px, dy = by[jj] - py, d2 = dx * dx + dy * dy;
+  if (d2 < *best) { *best = d2; *bj = jj; }
+}
 /* _kernels.polar_query_fast (_kernels.py:121-148, 185-219) */
 static double polar_query(const double* P, double px, double py, double* qx, double* qy) {
   const int stride = (int)P[3], n = (int)P[4];
   const double *bx = P + 5, *by = P + 5 + n;
   double best = 1.0e300;
   int bj = 0;
-  for (int j = 0; j < n; j += stride) {
-    const double dx = bx[j] - px, dy = by[j] - py, d2 = dx * dx + dy * dy;
-    if (d2 < best) { best = d2; bj = j; }
-  }
-  if (stride > 1) {
-    const int lo = bj - stride;
-    for (int off = 0; off <= 2 * stride; ++off) {
-      int jj = (lo + off) % n;
-      if (jj < 0) jj += n;
-      const double dx = bx[jj] - px, dy = by[jj] - py, d2 = dx * dx + dy * dy;
-      if (d2 < best) { best = d2; bj = jj; }
+  if (g_polar_native) {
+    int st = stride > 1 ? stride : 8;
+    for (int j = 0; j < n; j += st) polar_probe(bx, by, n, j, px, py, &best, &bj);
+    while (st > 1) {
+      const int f = st >= 8 ? st / 8 : 1, c = bj;
+      for (int off = -st; off <= st; off += f)
+        if (off != 0) polar_probe(bx, by, n, c + off, px, py, &best, &bj);
+      st = f;
+    }
+  } else {
+    for (int j = 0; j < n; j += stride) polar_probe(bx, by, n, j, px, py, &best, &bj);
+    if (stride > 1) {
+      const int lo = bj - stride;
+      for (int off = 0; off <= 2 * stride; ++off) polar_probe(bx, by, n, lo + off, px, py, &best, &bj);
     }
   }
   const double h = TWO_PI / n, t0 = bj * h;
@@ -779,6 +791,7 @@ static int run_rows(const wos_problem* pb, int native, int64_t n, const double* 
                     const uint64_t* pid, const uint64_t* tid, const double* sgn, uint64_t seed,
                     double eps, int64_t max_steps, double* values, int64_t* steps, uint8_t* hits,
                     int nthreads) {
+  g_polar_native = native;
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   pthread_t th[256];
@@ -871,6 +884,7 @@ int oracle_estimate(const wos_problem* pbs, int native, int64_t P, const double*
                     const int64_t* pid, const int32_t* inst, int64_t L, uint64_t traj_start,
                     int antithetic, uint64_t seed, double eps, int64_t max_steps, double* mean,
                     double* m2, uint64_t* total_steps, int nthreads) {
+  g_polar_native = native;
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   pthread_t th[256];
