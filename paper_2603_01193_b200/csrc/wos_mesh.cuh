@@ -109,16 +109,27 @@ __device__ __forceinline__ Real box_d2(const MeshNode<Real>& n, const Real* p) {
 // Nearest triangle to p: squared distance, closest point, region and triangle (leaf
 // order). Depth-first, nearer child first, pruned by the node boxes; a triangle
 // replaces the best only when strictly closer.
+// `hint` (or -1): a triangle to test first — a walk's previous nearest triangle is
+// within 2d of the new position, so it bounds the search from the start and the
+// traversal prunes almost every box.
 template <class Real>
 __device__ __forceinline__ Real mesh_nearest(const MeshNode<Real>* __restrict__ nodes,
                                              const Real* __restrict__ tris, const Real* p,
-                                             Real* q_best, int* reg_best, int* tri_best) {
+                                             Real* q_best, int* reg_best, int* tri_best,
+                                             int hint = -1) {
   constexpr int kStack = 48;
   int stack[kStack];
   int sp = 0;
   int node = 0;
   Real best = Real(3.0e38);
   int breg = MREG_FACE, btri = 0;
+  if (hint >= 0) {
+    const Real* t = tris + 9 * (size_t)hint;
+    breg = closest_on_triangle(p, t, t + 3, t + 6, q_best);
+    Real df[3] = {q_best[0] - p[0], q_best[1] - p[1], q_best[2] - p[2]};
+    best = mdot3(df, df);
+    btri = hint;
+  }
   while (true) {
     const MeshNode<Real> n = nodes[node];
     if (n.right < 0) {
@@ -128,7 +139,9 @@ __device__ __forceinline__ Real mesh_nearest(const MeshNode<Real>* __restrict__ 
         const int reg = closest_on_triangle(p, t, t + 3, t + 6, q);
         Real df[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
         const Real d2 = mdot3(df, df);
-        if (d2 < best) {
+        // strictly closer replaces; at a tie the lower leaf index wins, so the answer
+        // does not depend on the hint
+        if (d2 < best || (d2 == best && n.first + k < btri)) {
           best = d2;
           breg = reg;
           btri = n.first + k;
@@ -142,8 +155,9 @@ __device__ __forceinline__ Real mesh_nearest(const MeshNode<Real>* __restrict__ 
       const Real dl = box_d2(nodes[l], p), dr = box_d2(nodes[r], p);
       const int nf = dl <= dr ? l : r, ff = dl <= dr ? r : l;
       const Real dn = dl <= dr ? dl : dr, dfar = dl <= dr ? dr : dl;
-      if (dfar < best && sp < kStack) stack[sp++] = ff;
-      if (dn < best) {
+      // boxes at exactly the best distance are still visited (ties resolve by index)
+      if (dfar <= best && sp < kStack) stack[sp++] = ff;
+      if (dn <= best) {
         node = nf;
         continue;
       }
@@ -152,7 +166,7 @@ __device__ __forceinline__ Real mesh_nearest(const MeshNode<Real>* __restrict__ 
     bool found = false;
     while (sp > 0) {
       const int c = stack[--sp];
-      if (box_d2(nodes[c], p) < best) {
+      if (box_d2(nodes[c], p) <= best) {
         node = c;
         found = true;
         break;

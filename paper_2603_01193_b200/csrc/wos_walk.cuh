@@ -373,18 +373,21 @@ struct Walker {
     } else if constexpr (S::DOM == DOM_POLAR) {
       polar_query(l, a, nullptr, l.x[0], l.x[1], &q[0], &q[1]);
     } else if constexpr (S::DOM == DOM_MESH) {
-      mesh_d2(l, a, q);
+      Lane c = l;
+      mesh_d2(c, a, q);
     } else {
       poly_project(l, a, q);
     }
   }
 
   // ---------------- closed triangle meshes (geometry.MeshDomain) ----------------
-  __device__ static __forceinline__ Real mesh_d2(const Lane& l, const KArgs& a, Real* q) {
+  __device__ static __forceinline__ Real mesh_d2(Lane& l, const KArgs& a, Real* q) {
     int reg, tri;
-    return mesh_nearest<Real>(reinterpret_cast<const MeshNode<Real>*>(a.nodes) + l.seg_off,
-                              reinterpret_cast<const Real*>(a.segs) + 9 * (size_t)l.rec_off, l.x, q,
-                              &reg, &tri);
+    const Real d2 = mesh_nearest<Real>(reinterpret_cast<const MeshNode<Real>*>(a.nodes) + l.seg_off,
+                                       reinterpret_cast<const Real*>(a.segs) + 9 * (size_t)l.rec_off,
+                                       l.x, q, &reg, &tri, l.seg_i);
+    l.seg_i = tri;  // next query starts from this triangle
+    return d2;
   }
 
   // ---------------- polar star curves (geometry.PolarDomain) ----------------
@@ -1144,6 +1147,7 @@ struct Walker {
       l.n_seg = h.n_seg;
       l.rec_off = h.rec_off;
     }
+    if constexpr (S::DOM == DOM_MESH) l.seg_i = -1;
     if constexpr (kScr) {
       l.thr = Real(1);
       const Real* P = prow(l, a) + kSrcOff;
