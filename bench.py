@@ -305,13 +305,21 @@ def main():
     peaks = ctx.probe_peaks() if rank == 0 else None
 
     # ---- e2e through the C-ABI with host buffers (H2D + kernel + D2H per step) ----
-    host_pts = np.ascontiguousarray(shard.points)
+    def pinned(a):
+        # page-locked host buffers (the contract's pinned host memory): the library's
+        # chunked pipeline overlaps their copies with the walks
+        t = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, a.dtype)).dtype).pin_memory()
+        out = t.numpy()
+        out[...] = a
+        return out, t
+
+    host_pts, _keep_pts = pinned(np.ascontiguousarray(shard.points))
     # default ids (0..P-1, the reference's estimate() default) are generated on the device
-    host_ids = None if world == 1 and args.replicas == 1 and np.array_equal(shard.point_ids, np.arange(shard.n_points)) \
-        else np.ascontiguousarray(shard.point_ids)
-    host_inst = np.ascontiguousarray(shard.inst_index) if inst is not None else None
-    out_mean = np.empty(shard.n_points)
-    out_m2 = np.empty(shard.n_points)
+    host_ids, _keep_ids = (None, None) if world == 1 and args.replicas == 1 and np.array_equal(
+        shard.point_ids, np.arange(shard.n_points)) else pinned(np.ascontiguousarray(shard.point_ids))
+    host_inst, _keep_inst = pinned(np.ascontiguousarray(shard.inst_index)) if inst is not None else (None, None)
+    out_mean, _keep_mean = pinned(np.empty(shard.n_points))
+    out_m2, _keep_m2 = pinned(np.empty(shard.n_points))
     from ctypes import byref, c_uint64
 
     wc = engine.walk_config_struct(eps, w.cfg.max_steps, w.cfg.antithetic, w.cfg.mode, w.cfg.rng_seed)
@@ -399,7 +407,7 @@ def main():
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "walk-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "path": "wos_estimate_host (C ABI, host buffers; copies inside, pipelined in point chunks)"},
+                    "path": "wos_estimate_host (C ABI, pinned host buffers; copies inside, pipelined in point chunks)"},
             "gpu_launches": 2 * args.steps,
         }
         if cpu is not None:

@@ -56,8 +56,10 @@ struct wos_context {
   int num_sms = 148;
   cudaStream_t stream = nullptr;          // private stream of the *_host entry points
   cudaStream_t copy_stream = nullptr;     // host pipeline copies
+  cudaStream_t stream2 = nullptr;         // host pipeline: odd chunks' walks (tails overlap)
   cudaEvent_t ev_copy[kPipeChunks] = {};
   cudaEvent_t ev_kernel[kPipeChunks] = {};
+  cudaEvent_t ev_start = nullptr;
   unsigned int* d_counters = nullptr;     // work counters, one per launch slot
   std::atomic<unsigned> next_counter{0};
   unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
@@ -136,10 +138,12 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   c->num_sms = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
   for (int i = 0; i < kPipeChunks && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_kernel[i], cudaEventDisableTiming);
   }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, sizeof(unsigned) * kCounterRing);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_exterior, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
@@ -167,10 +171,12 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   for (int i = 0; i < kPipeChunks; ++i) {
     if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
     if (c->ev_kernel[i]) cudaEventDestroy(c->ev_kernel[i]);
   }
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
   delete c;
 }
 
@@ -1382,10 +1388,13 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   double* d_mean = (double*)(base + bp + b8);
   double* d_m2 = (double*)(base + bp + 2 * b8);
   int32_t* d_inst = inst_index ? (int32_t*)(base + bp + 3 * b8) : nullptr;
-  const cudaStream_t cs = c->stream, xs = c->copy_stream;
+  const cudaStream_t cs = c->stream, xs = c->copy_stream, cs2 = c->stream2;
   CUDA_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(unsigned long long), cs));
-  // Software pipeline over point chunks: copies on `xs`, walks on `cs`, so the
-  // copies of chunk i+1 and the results of chunk i-1 overlap the walks of chunk i.
+  CUDA_TRY(cudaEventRecord(c->ev_start, cs));
+  CUDA_TRY(cudaStreamWaitEvent(cs2, c->ev_start, 0));
+  // Software pipeline over point chunks: copies on `xs`, walks alternately on `cs` and
+  // `cs2`, so the copies of chunk i+1 and the results of chunk i-1 overlap the walks
+  // of chunk i, and chunk i+1's persistent grid fills the SMs chunk i's tail frees.
   const int64_t work = P * L;
   const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kPipeChunks, work / kPipeMinWork));
   int64_t lo[kPipeChunks + 1];
@@ -1399,20 +1408,24 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   };
   for (int i = 0; i < nch; ++i) {
     const int64_t o = lo[i], m = lo[i + 1] - lo[i];
+    const cudaStream_t ks = (i & 1) ? cs2 : cs;
     CUDA_TRY(cudaMemcpyAsync(d_pts + o * s->dim, points + o * s->dim, m * s->dim * 8,
                              cudaMemcpyHostToDevice, xs));
     if (d_ids) CUDA_TRY(cudaMemcpyAsync(d_ids + o, point_ids + o, m * 8, cudaMemcpyHostToDevice, xs));
     if (d_inst) CUDA_TRY(cudaMemcpyAsync(d_inst + o, inst_index + o, m * 4, cudaMemcpyHostToDevice, xs));
     CUDA_TRY(cudaEventRecord(c->ev_copy[i], xs));
-    CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_copy[i], 0));
+    CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_copy[i], 0));
     r = estimate_impl(c, s, cfg, m, d_pts + o * s->dim, d_ids ? d_ids + o : nullptr,
                       d_inst ? d_inst + o : nullptr, L, traj_start, d_mean + o, d_m2 + o,
-                      reinterpret_cast<uint64_t*>(c->d_steps), cs, o);
+                      reinterpret_cast<uint64_t*>(c->d_steps), ks, o);
     if (r) return r;
-    CUDA_TRY(cudaEventRecord(c->ev_kernel[i], cs));
+    CUDA_TRY(cudaEventRecord(c->ev_kernel[i], ks));
     if (i > 0 && (r = d2h(i - 1))) return r;
   }
   if ((r = d2h(nch - 1))) return r;
+  // join the second walk stream before reading the counters
+  CUDA_TRY(cudaEventRecord(c->ev_start, cs2));
+  CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_start, 0));
   unsigned long long steps = 0, ext = 0;
   CUDA_TRY(cudaMemcpyAsync(&steps, c->d_steps, 8, cudaMemcpyDeviceToHost, cs));
   CUDA_TRY(cudaMemcpyAsync(&ext, c->d_exterior, 8, cudaMemcpyDeviceToHost, cs));
