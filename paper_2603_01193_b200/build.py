@@ -36,7 +36,8 @@ UNITS = {
     "wos_kernels_replay_f32.cu": ["--fmad=false"],
     "wos_cache.cu": ["--fmad=false"],
 }
-HEADERS = ["wos_types.h", "wos_rng.cuh", "wos_walk.cuh", "wos_kernels.h", "wos_kernels_native.inc"]
+HEADERS = ["wos_types.h", "wos_rng.cuh", "wos_walk.cuh", "wos_mesh.cuh", "wos_kernels.h",
+           "wos_kernels_native.inc"]
 
 
 def _stale(obj, deps):
