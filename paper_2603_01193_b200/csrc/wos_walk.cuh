@@ -857,28 +857,86 @@ struct Walker {
     }
     return 0.5 * (lo + hi);
   }
-  // NATIVE: safeguarded Newton on the same CDF (pdf = q^2 t sinh(q (1-t)) / (sinh q - q)),
-  // started from the harmonic (q -> 0) inverse t = 1/2 - sin(asin(1 - 2u) / 3); every
-  // iterate stays inside the bracket [lo, hi] that the CDF values maintain
-  __device__ static __forceinline__ double invert_radial_newton(double q, double u) {
-    double t = 0.5 - sin(asin(1.0 - 2.0 * u) * (1.0 / 3.0));
-    if (q < 1.0e-4) return t;
-    const double sq = sinh(q), den = sq - q;
-    double lo = 0.0, hi = 1.0;
-    for (int it = 0; it < 40; ++it) {
-      const double e = exp(q * (1.0 - t)), ei = 1.0 / e;
-      const double sh = 0.5 * (e - ei), ch = 0.5 * (e + ei);
-      const double F = (sq - q * t * ch - sh) / den - u;
-      if (F < 0.0) lo = t;
+  // NATIVE fp32 inversion of the same CDF, stable over the whole q range:
+  //  q < 1 : F = t^2 sum_k w_k p_k(t) / sum_k w_k, w_k = q^(2k-2) / (2k+1)!, the q-series of
+  //          the hyperbolic form (p_k from expanding sinh/cosh; p_k(1) = 1), k <= 4;
+  //  q >= 1: F = N / D scaled by 2 e^-q: D = 1 - e^-2q - 2q e^-q,
+  //          N = A(x) - e^-2q + (1 - x) e^-(2q - x), x = q t, A(x) = 1 - (1 + x) e^-x
+  //          (series for small x), pdf = q x (e^-x - e^-(2q - x)) / D.
+  // Safeguarded Newton from the harmonic (q < 1) or Gamma(2) (q >= 1) quantile.
+  __device__ static __forceinline__ float invert_radial_f32(float q, float u) {
+    float lo = 0.0f, hi = 1.0f, t;
+    // start: the harmonic quantile t = 1/2 - sin(asin(1 - 2u) / 3) for q < 3.5, else the
+    // Gamma(2) quantile of x = q t (x = -ln(1 - u) + ln(1 + x), two fixed-point steps)
+    if (q < 3.5f) {
+      t = 0.5f - __sinf(asinf(1.0f - 2.0f * u) * (1.0f / 3.0f));
+    } else {
+      const float l1 = -__logf(1.0f - u);
+      float x = l1 + __logf(1.0f + l1);
+      x = l1 + __logf(1.0f + x);
+      t = fminf(x / q, 0.999f);
+    }
+    // Newton until |F(t) - u| <= 1e-6 (fp32 resolution of u) or the step stalls
+    if (q < 1.0f) {
+      const float q2 = q * q;
+      const float w1 = 1.0f / 6.0f, w2 = q2 * (1.0f / 120.0f), w3 = q2 * q2 * (1.0f / 5040.0f),
+                  w4 = q2 * q2 * q2 * (1.0f / 362880.0f);
+      const float iw = 1.0f / (w1 + w2 + w3 + w4);
+      // combined polynomial P(t) = sum_j c_j t^j (degree 7), F = t^2 P(t)
+      float c[8];
+      c[0] = (3.0f * w1 + 10.0f * w2 + 21.0f * w3 + 36.0f * w4) * iw;
+      c[1] = (-2.0f * w1 - 20.0f * w2 - 70.0f * w3 - 168.0f * w4) * iw;
+      c[2] = (15.0f * w2 + 105.0f * w3 + 378.0f * w4) * iw;
+      c[3] = (-4.0f * w2 - 84.0f * w3 - 504.0f * w4) * iw;
+      c[4] = (35.0f * w3 + 420.0f * w4) * iw;
+      c[5] = (-6.0f * w3 - 216.0f * w4) * iw;
+      c[6] = (63.0f * w4) * iw;
+      c[7] = (-8.0f * w4) * iw;
+      for (int it = 0; it < 16; ++it) {
+        float P = c[7], dP = 7.0f * c[7];
+#pragma unroll
+        for (int j = 6; j >= 0; --j) {
+          P = fmaf(P, t, c[j]);
+          if (j >= 1) dP = fmaf(dP, t, (float)j * c[j]);
+        }
+        const float F = t * t * P - u;
+        if (fabsf(F) <= 1e-6f) break;
+        if (F < 0.0f) lo = t;
+        else hi = t;
+        const float pdf = t * fmaf(t, dP, 2.0f * P);
+        float tn = pdf > 0.0f ? t - F / pdf : 0.5f * (lo + hi);
+        if (!(tn >= lo && tn <= hi)) tn = 0.5f * (lo + hi);
+        const bool done = fabsf(tn - t) <= 2e-7f * fmaxf(t, 1e-3f);
+        t = tn;
+        if (done) break;
+      }
+      return t;
+    }
+    const float e2q = __expf(-2.0f * q);
+    const float D = 1.0f - e2q - 2.0f * q * __expf(-q);
+    for (int it = 0; it < 16; ++it) {
+      const float x = q * t;
+      const float ex = __expf(-x), e2 = __expf(x - 2.0f * q);
+      float A;
+      if (x < 0.25f) {  // 1 - (1 + x) e^-x = e^-x (x^2/2 + x^3/6 + x^4/24 + x^5/120 + x^6/720)
+        A = ex * x * x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720.0f, 1.0f / 120.0f), 1.0f / 24.0f), 1.0f / 6.0f), 0.5f);
+      } else {
+        A = fmaf(-(1.0f + x), ex, 1.0f);
+      }
+      const float F = (A - e2q + (1.0f - x) * e2) / D - u;
+      if (fabsf(F) <= 1e-6f) break;
+      if (F < 0.0f) lo = t;
       else hi = t;
-      const double pdf = q * q * t * sh / den;
-      double tn = (pdf > 0.0) ? t - F / pdf : 0.5 * (lo + hi);
-      if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
-      if (fabs(tn - t) < 1.0e-13) return tn;
+      const float pdf = q * x * (ex - e2) / D;
+      float tn = pdf > 0.0f ? t - F / pdf : 0.5f * (lo + hi);
+      if (!(tn >= lo && tn <= hi)) tn = 0.5f * (lo + hi);
+      const bool done = fabsf(tn - t) <= 2e-7f * fmaxf(t, 1e-3f);
       t = tn;
+      if (done) break;
     }
     return t;
   }
+
   __device__ static __forceinline__ void note_majorant(const KArgs& a, double sp) {
     atomicMax(a.majorant, (unsigned long long)__double_as_longlong(sp));
   }
@@ -948,7 +1006,7 @@ struct Walker {
     __sincosf(fmaf(f12(A.z), kTwoPiF, -kTwoPiF), &sph, &cph);
     const bool vol = (f12(A.x) - 1.0f) >= surf;
     float rad = d;
-    if (vol) rad = d * (float)invert_radial_newton(q, (double)(f12(A.w) - 1.0f) + 0x1p-24);
+    if (vol) rad = d * invert_radial_f32(qf, (f12(A.w) - 1.0f) + 0x1p-24f);
     const float sr = l.sgn * rad, srxy = sr * sxy;
     l.x[0] = fmaf(srxy, cph, l.x[0]);
     l.x[1] = fmaf(srxy, sph, l.x[1]);
