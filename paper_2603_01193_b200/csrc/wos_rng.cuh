@@ -68,6 +68,66 @@ __device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const uint32_t* rk0, con
   return c;
 }
 
+// A walk draws blocks at counters (2 step, c1, c2, c3) with c1..c3 fixed for the walk.
+// Round 0 multiplies only c0 (varies) and c2 (fixed); its outputs x0 = hi(M1 c2) ^ c1
+// ^ k0 and x1 = lo(M1 c2) are fixed, so round 1's product M0 x0 is fixed as well.
+// Precomputing those words once per walk leaves two of the first four IMAD.WIDE and
+// one XOR per block; the output is bit-identical to philox4x32.
+struct PhiloxPre {
+  uint32_t e;   // c3 ^ k1(0)
+  uint32_t bk;  // lo(M1 c2) ^ k0(1)
+  uint32_t hk;  // hi(M0 x0) ^ k1(1)
+  uint32_t lw;  // lo(M0 x0)
+};
+
+__device__ __forceinline__ PhiloxPre philox_pre(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k00,
+                                                uint32_t k10, uint32_t k01, uint32_t k11) {
+  const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+  const uint32_t x0 = (uint32_t)(p1 >> 32) ^ c1 ^ k00;
+  const uint64_t p0 = (uint64_t)0xD2511F53u * x0;
+  return PhiloxPre{c3 ^ k10, (uint32_t)p1 ^ k01, (uint32_t)(p0 >> 32) ^ k11, (uint32_t)p0};
+}
+
+// rounds 0 and 1 from the precomputed words: the state entering round 2
+__device__ __forceinline__ uint4 philox_pre_r01(uint32_t c0, const PhiloxPre& p) {
+  const uint64_t q0 = (uint64_t)0xD2511F53u * c0;                   // round 0, word 0
+  const uint64_t q1 = (uint64_t)0xCD9E8D57u * ((uint32_t)(q0 >> 32) ^ p.e);  // round 1, word 2
+  return make_uint4((uint32_t)(q1 >> 32) ^ p.bk, (uint32_t)q1, p.hk ^ (uint32_t)q0, p.lw);
+}
+
+__device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t c0, const PhiloxPre& p, const uint32_t* rk0,
+                                                   const uint32_t* rk1) {
+  uint4 c = philox_pre_r01(c0, p);
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint64_t p0 = (uint64_t)M0 * c.x;
+    uint64_t p1 = (uint64_t)M1 * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c = make_uint4(hi1 ^ c.y ^ rk0[r], lo1, hi0 ^ c.w ^ rk1[r], lo0);
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 philox4x32_pre(uint32_t c0, const PhiloxPre& p, uint32_t k0, uint32_t k1) {
+  uint4 c = philox_pre_r01(c0, p);
+  k0 += 2u * 0x9E3779B9u;
+  k1 += 2u * 0xBB67AE85u;
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint64_t p0 = (uint64_t)M0 * c.x;
+    uint64_t p1 = (uint64_t)M1 * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
 // NATIVE uniform: (w >> 9) * 2^-23 in [0, 1), exact in fp32 (one LOP3 + one FADD).
 __device__ __forceinline__ float u01_23(uint32_t w) {
   return __uint_as_float(0x3f800000u | (w >> 9)) - 1.0f;

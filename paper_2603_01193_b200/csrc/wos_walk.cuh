@@ -158,7 +158,9 @@ struct Walker {
     int step;
     uint32_t seq;  // ESTIMATE: byte offset of the walk's ring slot; ROWS: row index
     uint64_t pid, tid, ikey;   // REPLAY counters / key
-    uint32_t c1, c2, c3, k1;   // NATIVE counters / key
+    uint32_t c1, c2, c3;       // NATIVE kHot: counter words
+    PhiloxPre pc;              // other NATIVE: the counter words folded through rounds 0-1
+    uint32_t k1;               // NATIVE multi-instance: the instance key
     int32_t seg_off, n_seg, rec_off;
     int32_t seg_i;  // polygon: nearest segment found by the last distance query
     Real thr;       // delta tracking: throughput (walker.py:365, _kernels.py:539)
@@ -1101,10 +1103,25 @@ struct Walker {
   }
 
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
-    const uint4 c = make_uint4(2u * (uint32_t)l.step, l.c1, l.c2, l.c3);
-    if constexpr (kHot) return philox4x32_rk(c, l.hk0, l.hk1);
-    else if constexpr (ONE) return philox4x32_rk(c, a.rk0, a.rk1);
-    else return philox4x32(c, a.nkey0, l.k1);
+    const uint32_t c0 = 2u * (uint32_t)l.step;
+    if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1);
+    else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1);
+    else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1);
+  }
+
+  // the walk's Philox counter words (c1, c2, c3) folded through rounds 0-1 (wos_rng.cuh)
+  __device__ static __forceinline__ void set_counter(Lane& l, const KArgs& a, uint32_t c1, uint32_t c2,
+                                                     uint32_t c3) {
+    // kHot walks are short against the refill cadence: the per-walk fold would cost a
+    // warp more at each refill than it saves per step (measured on cfg4)
+    if constexpr (kHot) {
+      l.c1 = c1;
+      l.c2 = c2;
+      l.c3 = c3;
+    }
+    else if constexpr (ONE) l.pc = philox_pre(c1, c2, c3, a.rk0[0], a.rk1[0], a.rk0[1], a.rk1[1]);
+    else
+      l.pc = philox_pre(c1, c2, c3, a.nkey0, l.k1, a.nkey0 + 0x9E3779B9u, l.k1 + 0xBB67AE85u);
   }
 
   // NATIVE: Green's-function importance sampling, fp32 fast math, one Philox block
@@ -1160,16 +1177,14 @@ struct Walker {
 
   // ---------------- walk start ----------------
   // single-instance NATIVE start from precomputed counter words (same state as start)
-  __device__ static __forceinline__ void start_native(Lane& l, const float* x0, float sgn,
+  __device__ static __forceinline__ void start_native(Lane& l, const KArgs& a, const float* x0, float sgn,
                                                       uint32_t c1, uint32_t c2, uint32_t c3) {
 #pragma unroll
     for (int i = 0; i < DIM; ++i) l.x[i] = x0[i];
     l.acc = 0.0f;
     l.sgn = sgn;
     l.step = 0;
-    l.c1 = c1;
-    l.c2 = c2;
-    l.c3 = c3;
+    set_counter(l, a, c1, c2, c3);
   }
 
   template <class X>
@@ -1181,11 +1196,7 @@ struct Walker {
     l.acc = Real(0);
     l.sgn = (Real)sgn;
     l.step = 0;
-    if constexpr (S::NATIVE) {
-      l.c1 = (uint32_t)pid;
-      l.c2 = (uint32_t)tid;
-      l.c3 = (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu);
-    } else {
+    if constexpr (!S::NATIVE) {
       l.pid = pid;
       l.tid = tid;
     }
@@ -1205,6 +1216,9 @@ struct Walker {
       l.n_seg = h.n_seg;
       l.rec_off = h.rec_off;
     }
+    if constexpr (S::NATIVE)
+      set_counter(l, a, (uint32_t)pid, (uint32_t)tid,
+                  (uint32_t)(tid >> 32) ^ ((uint32_t)(pid >> 32) * 0x85EBCA6Bu));
     if constexpr (S::DOM == DOM_MESH) l.seg_i = -1;
     if constexpr (kScr) {
       l.thr = Real(1);
@@ -1593,7 +1607,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               if constexpr (S::NATIVE && S::ONE && !W::kScr && S::DOM != DOM_POLY &&
                             S::DOM != DOM_POLAR && S::DOM != DOM_MESH) {
                 if (cu_fastc) {
-                  W::start_native(l, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
+                  W::start_native(l, a, cu_x, (anti && (jr & 1u)) ? -1.0f : 1.0f, cu_c1,
                                   cu_c2b + (anti ? (jr & ~1u) : jr), cu_c3);
                   started = true;
                 }
