@@ -517,30 +517,75 @@ struct Walker {
       float s[DIM], c[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) __sincosf(kPiF * y[i], &s[i], &c[i]);
+      // Independent Horner chains run two at a time as packed FFMA2 (fma.rn.f32x2,
+      // elementwise fma.rn): the same operations in the same order as scalar fmaf, so
+      // bit-identical to it, at half the issue slots.
+      auto f2 = [](float x, float y) { return make_float2(x, y); };
       if constexpr (DIM == 2) {
-        float q = 0.f;
+        float hp[K];  // hp[p] = sum_r a[p][r] c1^r
 #pragma unroll
-        for (int p = K - 1; p >= 0; --p) {
-          float h = a[p * K + (K - 1)];
+        for (int p = 0; p + 1 < K; p += 2) {
+          float2 h = f2(a[p * K + (K - 1)], a[(p + 1) * K + (K - 1)]);
 #pragma unroll
-          for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[1], a[p * K + r]);
-          q = (p == K - 1) ? h : fmaf(q, c[0], h);
+          for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[1], c[1]), f2(a[p * K + r], a[(p + 1) * K + r]));
+          hp[p] = h.x;
+          hp[p + 1] = h.y;
         }
+        if constexpr (K % 2) {
+          float h = a[(K - 1) * K + (K - 1)];
+#pragma unroll
+          for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[1], a[(K - 1) * K + r]);
+          hp[K - 1] = h;
+        }
+        float q = hp[K - 1];
+#pragma unroll
+        for (int p = K - 2; p >= 0; --p) q = fmaf(q, c[0], hp[p]);
         return (s[0] * s[1]) * q;
       } else {
-        float q = 0.f;
+        auto A = [&](int p, int qd, int r) { return a[(p * K + qd) * K + r]; };
+        float mp[K];  // mp[p] = sum_qd c1^qd sum_r a[p][qd][r] c2^r
+        // pairs of p: both chains of every level share the broadcast c2 / c1
 #pragma unroll
-        for (int p = K - 1; p >= 0; --p) {
-          float m = 0.f;
+        for (int p = 0; p + 1 < K; p += 2) {
+          float2 hq[K];
 #pragma unroll
-          for (int qd = K - 1; qd >= 0; --qd) {
-            float h = a[(p * K + qd) * K + (K - 1)];
+          for (int qd = 0; qd < K; ++qd) {
+            float2 h = f2(A(p, qd, K - 1), A(p + 1, qd, K - 1));
 #pragma unroll
-            for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[2], a[(p * K + qd) * K + r]);
-            m = (qd == K - 1) ? h : fmaf(m, c[1], h);
+            for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p + 1, qd, r)));
+            hq[qd] = h;
           }
-          q = (p == K - 1) ? m : fmaf(q, c[0], m);
+          float2 m = hq[K - 1];
+#pragma unroll
+          for (int qd = K - 2; qd >= 0; --qd) m = __ffma2_rn(m, f2(c[1], c[1]), hq[qd]);
+          mp[p] = m.x;
+          mp[p + 1] = m.y;
         }
+        if constexpr (K % 2) {  // the unpaired p: pairs of qd
+          constexpr int p = K - 1;
+          float hq[K];
+#pragma unroll
+          for (int qd = 0; qd + 1 < K; qd += 2) {
+            float2 h = f2(A(p, qd, K - 1), A(p, qd + 1, K - 1));
+#pragma unroll
+            for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p, qd + 1, r)));
+            hq[qd] = h.x;
+            hq[qd + 1] = h.y;
+          }
+          {
+            float h = A(p, K - 1, K - 1);
+#pragma unroll
+            for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[2], A(p, K - 1, r));
+            hq[K - 1] = h;
+          }
+          float m = hq[K - 1];
+#pragma unroll
+          for (int qd = K - 2; qd >= 0; --qd) m = fmaf(m, c[1], hq[qd]);
+          mp[p] = m;
+        }
+        float q = mp[K - 1];
+#pragma unroll
+        for (int p = K - 2; p >= 0; --p) q = fmaf(q, c[0], mp[p]);
         return (s[0] * s[1] * s[2]) * q;
       }
     } else {
@@ -1166,11 +1211,15 @@ struct Walker {
       const float med = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6]));
       const float sr = l.sgn * fmaf(d, med, -d);
       const float srv = sr * vs;
-      const float g[3] = {fmaf(srv, vcp, l.x[0]), fmaf(srv, vsp, l.x[1]), fmaf(sr, vz, l.x[2])};
+      // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
+      const float2 xy = make_float2(l.x[0], l.x[1]);
+      const float2 gxy = __ffma2_rn(make_float2(srv, srv), make_float2(vcp, vsp), xy);
+      const float g[3] = {gxy.x, gxy.y, fmaf(sr, vz, l.x[2])};
       l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
       const float sdxy = sd * sxy;
-      l.x[0] = fmaf(sdxy, cph, l.x[0]);
-      l.x[1] = fmaf(sdxy, sph, l.x[1]);
+      const float2 nxy = __ffma2_rn(make_float2(sdxy, sdxy), make_float2(cph, sph), xy);
+      l.x[0] = nxy.x;
+      l.x[1] = nxy.y;
       l.x[2] = fmaf(sd, z, l.x[2]);
     }
   }
