@@ -596,21 +596,22 @@ struct Walker {
         Real f = Real(0);
         if constexpr (S::NATIVE && (K % 4) == 0) {
           // rows are 16-byte aligned (kSrcOff and the row stride are multiples of 4)
+          // packed FFMA2: even / odd l accumulate in the two halves of a pair, and the
+          // x factor scales both halves, so one horizontal add finishes the series
           const float4* a4 = reinterpret_cast<const float4*>(a);
+          float2 fp = make_float2(0.f, 0.f);
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            float t = 0.f;
+            float2 t = make_float2(0.f, 0.f);
 #pragma unroll
             for (int l4 = 0; l4 < K / 4; ++l4) {
               const float4 c = a4[(k * K) / 4 + l4];
-              t = fmaf(c.x, sy[4 * l4], t);
-              t = fmaf(c.y, sy[4 * l4 + 1], t);
-              t = fmaf(c.z, sy[4 * l4 + 2], t);
-              t = fmaf(c.w, sy[4 * l4 + 3], t);
+              t = __ffma2_rn(make_float2(c.x, c.y), make_float2(sy[4 * l4], sy[4 * l4 + 1]), t);
+              t = __ffma2_rn(make_float2(c.z, c.w), make_float2(sy[4 * l4 + 2], sy[4 * l4 + 3]), t);
             }
-            f = fmaf(sx[k], t, f);
+            fp = __ffma2_rn(make_float2(sx[k], sx[k]), t, fp);
           }
-          return f;
+          return fp.x + fp.y;
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
