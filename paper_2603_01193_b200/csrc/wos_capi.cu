@@ -88,7 +88,7 @@ struct wos_problem_set {
   InstHdr* d_hdr = nullptr;
   double* d_segs_d = nullptr;             // [nseg][ax, ay, ex, ey]
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
-  float4* d_segs_n = nullptr;             // NATIVE: per polygon n + 1 records {v_k, e_k/|e_k|^2}
+  float4* d_segs_n = nullptr;             // NATIVE: per polygon segment-pair records (poly_scan)
   size_t bytes_segs_n = 0;
   MeshNode<double>* d_mesh_nodes_d = nullptr;  // MESH: BVH nodes and leaf-ordered triangles
   MeshNode<float>* d_mesh_nodes_f = nullptr;
@@ -632,6 +632,7 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       hd[i].seg_off = (int)(segd.size() / 4);
       hd[i].rec_off = (int)segn.size();
       hd[i].n_seg = nv;
+      std::vector<float> vx, vy, ux, uy;
       for (int k = 0; k < nv; ++k) {
         const int j = (k + 1 == nv) ? 0 : k + 1;
         const double ax = V[2 * k], ay = V[2 * k + 1];
@@ -641,10 +642,25 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
         segd.push_back(ex);
         segd.push_back(ey);
         const double l2 = ex * ex + ey * ey;
-        // NATIVE record: vertex k and e_k / |e_k|^2; the next record holds vertex k+1
-        segn.push_back(make_float4((float)ax, (float)ay, (float)(ex / l2), (float)(ey / l2)));
+        vx.push_back((float)ax);
+        vy.push_back((float)ay);
+        ux.push_back((float)(ex / l2));
+        uy.push_back((float)(ey / l2));
       }
-      segn.push_back(make_float4((float)V[0], (float)V[1], 0.f, 0.f));  // closing vertex
+      // NATIVE records in segment pairs (wos_walk.cuh poly_scan): A_j = (x_2j, x_2j+1,
+      // y_2j, y_2j+1), U_j = (u_2j, u_2j+1 by component), then a closing A at vertex 0.
+      // An odd polygon gets a zero-length segment at vertex 0 (u = 0) as its pad.
+      if (nv & 1) {
+        vx.push_back((float)V[0]);
+        vy.push_back((float)V[1]);
+        ux.push_back(0.f);
+        uy.push_back(0.f);
+      }
+      for (size_t k = 0; k < vx.size(); k += 2) {
+        segn.push_back(make_float4(vx[k], vx[k + 1], vy[k], vy[k + 1]));
+        segn.push_back(make_float4(ux[k], ux[k + 1], uy[k], uy[k + 1]));
+      }
+      segn.push_back(make_float4((float)V[0], 0.f, (float)V[1], 0.f));  // closing vertex
     }
     for (int k = 0; k < 8; ++k) rn[k] = (float)rd[k];
     if (p.dom_kind == WOS_DOM_BOX)  // NATIVE box distance: centre and half extent

@@ -228,41 +228,76 @@ struct Walker {
 
   // polygon: min distance over segments; records the first nearest segment in l.seg_i
   // (the closest point is rebuilt from that one segment only at termination)
-  // NATIVE scan over vertex records {v_k, e_k/|e_k|^2} (record k+1 supplies v_{k+1}).
-  // Segments go in blocks of 4: the running minimum takes one FMNMX3 + FMNMX per
-  // block and only the first block attaining the minimum is remembered (*bi_out =
-  // its first segment); poly_project resolves the first nearest segment inside it,
-  // which is the global first nearest segment.
-  __device__ static __forceinline__ float seg_d2(float4 R, float4 Rn, float px, float py) {
-    const float ex = Rn.x - R.x, ey = Rn.y - R.y;
-    const float wx = px - R.x, wy = py - R.y;
-    const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
+  // NATIVE records come in segment pairs (wos_capi.cu build): A_j = (x_2j, x_2j+1,
+  // y_2j, y_2j+1), U_j = the same pairs of e_k/|e_k|^2, then A_j+1; one closing A
+  // holds vertex 0 again. An odd polygon gets a zero-length last segment at vertex 0,
+  // which never beats segment 0 (same end point). Both segments of a pair go through
+  // packed FADD2/FMUL2/FFMA2 with the scalar seg_d2 operation order, so every
+  // distance is bit-identical to seg_d2. The running minimum moves in blocks of 4
+  // segments and remembers the first block attaining it (*bi_out = its first
+  // segment); poly_project resolves the first nearest segment inside it.
+  __device__ static __forceinline__ float seg_d2(float ax, float ay, float nx, float ny, float ux, float uy,
+                                                 float px, float py) {
+    const float ex = nx - ax, ey = ny - ay;
+    const float wx = px - ax, wy = py - ay;
+    const float t = __saturatef(fmaf(wx, ux, wy * uy));
     const float dx = fmaf(-t, ex, wx), dy = fmaf(-t, ey, wy);
     return fmaf(dx, dx, dy * dy);
+  }
+
+  __device__ static __forceinline__ float2 pair_d2(float4 A, float4 U, float4 An, float px, float py) {
+    const float2 ex = make_float2(A.y - A.x, An.x - A.y), ey = make_float2(A.w - A.z, An.z - A.w);
+    const float2 wx = __fadd2_rn(make_float2(px, px), make_float2(-A.x, -A.y));
+    const float2 wy = __fadd2_rn(make_float2(py, py), make_float2(-A.z, -A.w));
+    const float2 sy = __fmul2_rn(wy, make_float2(U.z, U.w));
+    const float2 t = make_float2(__saturatef(fmaf(wx.x, U.x, sy.x)), __saturatef(fmaf(wx.y, U.y, sy.y)));
+    const float2 nt = make_float2(-t.x, -t.y);
+    const float2 dx = __ffma2_rn(nt, ex, wx), dy = __ffma2_rn(nt, ey, wy);
+    return __ffma2_rn(dx, dx, __fmul2_rn(dy, dy));
+  }
+
+  // segment s of a paired record block: its distance (seg_d2 order) and, optionally,
+  // the closest point
+  __device__ static __forceinline__ float seg_at(const float4* rec, int s, float px, float py,
+                                                 float* qx = nullptr, float* qy = nullptr) {
+    const int j = s >> 1;
+    const float4 A = __ldg(rec + 2 * j), U = __ldg(rec + 2 * j + 1), An = __ldg(rec + 2 * j + 2);
+    const bool odd = s & 1;
+    const float ax = odd ? A.y : A.x, ay = odd ? A.w : A.z;
+    const float nx = odd ? An.x : A.y, ny = odd ? An.z : A.w;
+    const float ux = odd ? U.y : U.x, uy = odd ? U.w : U.z;
+    if (qx != nullptr) {
+      const float ex = nx - ax, ey = ny - ay;
+      const float wx = px - ax, wy = py - ay;
+      const float t = __saturatef(fmaf(wx, ux, wy * uy));
+      *qx = fmaf(t, ex, ax);
+      *qy = fmaf(t, ey, ay);
+    }
+    return seg_d2(ax, ay, nx, ny, ux, uy, px, py);
   }
 
   template <class P>
   __device__ static __forceinline__ float poly_scan(const P rec, int n, float px, float py, int* bi_out) {
     float best = 3.0e38f;
     int bi = 0;
-    float4 R = rec[0];
-    const int n4 = n & ~3;
+    float4 A = rec[0];
+    const int m = (n + 1) >> 1;  // segment pairs
+    const int m2 = m & ~1;
 #pragma unroll 2
-    for (int i = 0; i < n4; i += 4) {
-      const float4 R1 = rec[i + 1], R2 = rec[i + 2], R3 = rec[i + 3], R4 = rec[i + 4];
-      const float d0 = seg_d2(R, R1, px, py), d1 = seg_d2(R1, R2, px, py);
-      const float d2 = seg_d2(R2, R3, px, py), d3 = seg_d2(R3, R4, px, py);
-      const float m = fminf(fminf(fminf(d0, d1), d2), d3);
-      bi = m < best ? i : bi;
-      best = fminf(best, m);
-      R = R4;
+    for (int j = 0; j < m2; j += 2) {
+      const float4 U0 = rec[2 * j + 1], A1 = rec[2 * j + 2], U1 = rec[2 * j + 3], A2 = rec[2 * j + 4];
+      const float2 d01 = pair_d2(A, U0, A1, px, py), d23 = pair_d2(A1, U1, A2, px, py);
+      const float mn = fminf(fminf(fminf(d01.x, d01.y), d23.x), d23.y);
+      bi = mn < best ? 2 * j : bi;
+      best = fminf(best, mn);
+      A = A2;
     }
-    for (int i = n4; i < n; ++i) {  // tail (n not a multiple of 4): exact per segment
-      const float4 Rn = rec[i + 1];
-      const float d = seg_d2(R, Rn, px, py);
-      bi = d < best ? i : bi;
-      best = fminf(best, d);
-      R = Rn;
+    if (m & 1) {  // last pair
+      const int j = m - 1;
+      const float2 d = pair_d2(A, rec[2 * j + 1], rec[2 * j + 2], px, py);
+      const float mn = fminf(d.x, d.y);
+      bi = mn < best ? 2 * j : bi;
+      best = fminf(best, mn);
     }
     *bi_out = bi;
     return best;
@@ -304,27 +339,26 @@ struct Walker {
   }
 
   // closest point on the segment recorded by the last distance query (NATIVE: the
-  // first nearest segment of the recorded 4-segment block)
+  // first nearest segment of the recorded block of 4, or of the last pair)
   __device__ static __forceinline__ void poly_project(const Lane& l, const KArgs& a, Real* q) {
     const int i0 = l.seg_i;
     if constexpr (S::NATIVE) {
       const float4* rec = reinterpret_cast<const float4*>(a.segs) + l.rec_off;
-      const int i1 = (i0 + 4 <= (l.n_seg & ~3)) ? i0 + 4 : i0 + 1;  // block or tail segment
+      const int np = ((l.n_seg + 1) >> 1) << 1;  // segments incl. the odd polygon's pad
+      const int i1 = min(i0 + 4, np);
       float best = 3.0e38f;
       int bi = i0;
       for (int i = i0; i < i1; ++i) {
-        const float d = seg_d2(__ldg(rec + i), __ldg(rec + i + 1), l.x[0], l.x[1]);
+        const float d = seg_at(rec, i, l.x[0], l.x[1]);
         if (d < best) {
           best = d;
           bi = i;
         }
       }
-      const float4 R = __ldg(rec + bi), Rn = __ldg(rec + bi + 1);
-      const float ex = Rn.x - R.x, ey = Rn.y - R.y;
-      const float wx = l.x[0] - R.x, wy = l.x[1] - R.y;
-      const float t = __saturatef(fmaf(wx, R.z, wy * R.w));
-      q[0] = fmaf(t, ex, R.x);
-      q[1] = fmaf(t, ey, R.y);
+      float qx, qy;
+      seg_at(rec, bi, l.x[0], l.x[1], &qx, &qy);
+      q[0] = qx;
+      q[1] = qy;
     } else {
       const int i = i0;
       const Real* seg = reinterpret_cast<const Real*>(a.segs) + 4 * (size_t)l.seg_off;
@@ -612,15 +646,16 @@ struct Walker {
             fp = __ffma2_rn(make_float2(sx[k], sx[k]), t, fp);
           }
           return fp.x + fp.y;
-        }
+        } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          Real t = Real(0);
+          for (int k = 0; k < K; ++k) {
+            Real t = Real(0);
 #pragma unroll
-          for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sy[l];
-          f = f + sx[k] * t;
+            for (int l = 0; l < K; ++l) t = t + a[k * K + l] * sy[l];
+            f = f + sx[k] * t;
+          }
+          return f;
         }
-        return f;
       } else {
         Real sz[K];
         sine_row<K>(y[2], sz);
