@@ -11,6 +11,7 @@
 #include <array>
 #include <atomic>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/wos_b200.h"
@@ -90,6 +91,8 @@ struct wos_problem_set {
   float* d_segs_f = nullptr;              // REPLAY_F32: same, float
   float4* d_segs_n = nullptr;             // NATIVE: per polygon segment-pair records (poly_scan)
   size_t bytes_segs_n = 0;
+  uint32_t* d_poly_grid = nullptr;        // NATIVE: polygon candidate grids (build_poly_grid)
+  bool poly_grid = false;                 // some polygon of the set has a grid
   MeshNode<double>* d_mesh_nodes_d = nullptr;  // MESH: BVH nodes and leaf-ordered triangles
   MeshNode<float>* d_mesh_nodes_f = nullptr;
   double* d_mesh_tris_d = nullptr;
@@ -334,6 +337,168 @@ static int validate(const wos_problem& p) {
 // normals, angle-weighted vertex normals, edge normals from the two adjacent faces;
 // a median-split BVH (largest box extent, leaves of <= 8 triangles, geometry.py:326-358)
 // laid out depth first with the left child next to its parent.
+// ---------------------------------------------------------------------------
+// NATIVE polygon candidate grid. The polygon's bounding box is cut into G x G cells;
+// each cell lists (ascending) the segment pairs that can hold the nearest segment of
+// some point in the cell: pair j is listed when one of its segments comes within
+// U + margin of the cell, U = min over segments of the largest corner distance (an
+// upper bound of the boundary distance anywhere in the cell, the distance to a
+// segment being convex). Unlisted segments are farther than the nearest one by more
+// than the fp32 rounding of the query, so the listed minimum (and its first segment)
+// is the full scan's. Walks spend most steps near the boundary, where lists are short.
+// ---------------------------------------------------------------------------
+static float bits_f32(int v) {
+  float f;
+  memcpy(&f, &v, sizeof(f));
+  return f;
+}
+
+struct PolyGrid {
+  int G = 0;
+  double lo[2] = {0, 0}, ih[2] = {0, 0};
+  std::vector<uint32_t> cells;  // G*G + 1 offsets into idx
+  std::vector<uint16_t> idx;    // pair indices
+};
+
+static double seg_dist(double px, double py, double ax, double ay, double bx, double by) {
+  const double ex = bx - ax, ey = by - ay, wx = px - ax, wy = py - ay;
+  const double l2 = ex * ex + ey * ey;
+  double t = l2 > 0 ? (wx * ex + wy * ey) / l2 : 0.0;
+  t = t < 0 ? 0 : (t > 1 ? 1 : t);
+  const double dx = wx - t * ex, dy = wy - t * ey;
+  return sqrt(dx * dx + dy * dy);
+}
+
+// distance between segment ab and the box [x0, x1] x [y0, y1]
+static double seg_box_dist(double ax, double ay, double bx, double by, double x0, double y0, double x1,
+                           double y1) {
+  // Liang-Barsky: does the segment meet the box?
+  double t0 = 0.0, t1 = 1.0;
+  const double dx = bx - ax, dy = by - ay;
+  const double pp[4] = {-dx, dx, -dy, dy}, qq[4] = {ax - x0, x1 - ax, ay - y0, y1 - ay};
+  bool hit = true;
+  for (int k = 0; k < 4 && hit; ++k) {
+    if (pp[k] == 0.0) {
+      if (qq[k] < 0.0) hit = false;
+    } else {
+      const double r = qq[k] / pp[k];
+      if (pp[k] < 0.0) t0 = std::max(t0, r);
+      else t1 = std::min(t1, r);
+      if (t0 > t1) hit = false;
+    }
+  }
+  if (hit) return 0.0;
+  auto pbox = [&](double px, double py) {
+    const double ux = px < x0 ? x0 - px : (px > x1 ? px - x1 : 0.0);
+    const double uy = py < y0 ? y0 - py : (py > y1 ? py - y1 : 0.0);
+    return sqrt(ux * ux + uy * uy);
+  };
+  double d = std::min(pbox(ax, ay), pbox(bx, by));
+  const double cx[4] = {x0, x1, x0, x1}, cy[4] = {y0, y0, y1, y1};
+  for (int k = 0; k < 4; ++k) d = std::min(d, seg_dist(cx[k], cy[k], ax, ay, bx, by));
+  return d;
+}
+
+// V: nv vertices; segments 0..np-1 with np = nv rounded up to even (the pad is the
+// zero-length segment at vertex 0). The lists are refined down a quadtree: a child
+// cell's candidates are a subset of its parent's (its U is no larger, its box
+// distances no smaller), so each level only tests the parent's list.
+static void build_poly_grid(const double* V, int nv, PolyGrid* g) {
+  const int np = nv + (nv & 1);
+  g->G = 0;
+  if (nv < 24) return;  // short polygons: the full scan is as cheap
+#ifndef WOS_POLY_GRID_SCALE
+#define WOS_POLY_GRID_SCALE 11.4
+#endif
+#ifndef WOS_POLY_GRID_MAX
+#define WOS_POLY_GRID_MAX 128
+#endif
+  const double want = WOS_POLY_GRID_SCALE * sqrt((double)nv);
+  int levels = 2;
+  while ((1 << levels) < want && (1 << levels) < WOS_POLY_GRID_MAX) ++levels;
+  const int G = 1 << levels;
+  double lo[2] = {V[0], V[1]}, hi[2] = {V[0], V[1]};
+  for (int k = 1; k < nv; ++k)
+    for (int c = 0; c < 2; ++c) {
+      lo[c] = std::min(lo[c], V[2 * k + c]);
+      hi[c] = std::max(hi[c], V[2 * k + c]);
+    }
+  const double diag = hypot(hi[0] - lo[0], hi[1] - lo[1]);
+  const double margin = 1e-5 * diag;
+  for (int c = 0; c < 2; ++c) {
+    const double pad = 1e-9 * diag;
+    lo[c] -= pad;
+    hi[c] += pad;
+    g->lo[c] = lo[c];
+    g->ih[c] = G / (hi[c] - lo[c]);
+  }
+  std::vector<double> SA(2 * np), SB(2 * np);
+  for (int s = 0; s < np; ++s) {
+    const int i = s < nv ? s : 0, j = s < nv ? (s + 1 == nv ? 0 : s + 1) : 0;
+    SA[2 * s] = V[2 * i];
+    SA[2 * s + 1] = V[2 * i + 1];
+    SB[2 * s] = V[2 * j];
+    SB[2 * s + 1] = V[2 * j + 1];
+  }
+  auto sd = [&](double px, double py, int s) {
+    return seg_dist(px, py, SA[2 * s], SA[2 * s + 1], SB[2 * s], SB[2 * s + 1]);
+  };
+  // level l: (1 << l)^2 cells, row-major; cell c's candidate segments (ascending) are
+  // data[off[c] .. off[c + 1])
+  std::vector<uint32_t> off = {0u, (uint32_t)np}, noff;
+  std::vector<int> data(np), ndata;
+  for (int s = 0; s < np; ++s) data[s] = s;
+  std::vector<double> dc;
+  for (int l = 1; l <= levels; ++l) {
+    const int n = 1 << l, pn = n >> 1;
+    const double hx = (hi[0] - lo[0]) / n, hy = (hi[1] - lo[1]) / n;
+    const double r = 0.5 * sqrt(hx * hx + hy * hy);
+    noff.assign((size_t)n * n + 1, 0u);
+    ndata.clear();
+    for (int cy = 0; cy < n; ++cy)
+      for (int cx = 0; cx < n; ++cx) {
+        const size_t pc = (size_t)(cy >> 1) * pn + (cx >> 1);
+        const int* C = data.data() + off[pc];
+        const int nc = (int)(off[pc + 1] - off[pc]);
+        const double x0 = lo[0] + cx * hx, y0 = lo[1] + cy * hy, x1 = x0 + hx, y1 = y0 + hy;
+        const double qx[4] = {x0, x1, x0, x1}, qy[4] = {y0, y0, y1, y1};
+        const double mx = 0.5 * (x0 + x1), my = 0.5 * (y0 + y1);
+        double U = 1e300;
+        dc.resize(nc);
+        for (int k = 0; k < nc; ++k) {
+          dc[k] = sd(mx, my, C[k]);
+          if (dc[k] >= U) continue;  // convexity: its farthest corner cannot beat U
+          double m = 0.0;
+          for (int q = 0; q < 4; ++q) m = std::max(m, sd(qx[q], qy[q], C[k]));
+          U = std::min(U, m);
+        }
+        for (int k = 0; k < nc; ++k) {
+          if (dc[k] - r > U + margin) continue;  // box distance >= centre distance - r
+          const int sg = C[k];
+          if (seg_box_dist(SA[2 * sg], SA[2 * sg + 1], SB[2 * sg], SB[2 * sg + 1], x0, y0, x1, y1) <= U + margin)
+            ndata.push_back(sg);
+        }
+        noff[(size_t)cy * n + cx + 1] = (uint32_t)ndata.size();
+      }
+    off.swap(noff);
+    data.swap(ndata);
+  }
+  g->G = G;
+  g->cells.assign((size_t)G * G + 1, 0);
+  g->idx.clear();
+  for (size_t c = 0; c < (size_t)G * G; ++c) {
+    g->cells[c] = (uint32_t)g->idx.size();
+    int last = -1;
+    for (uint32_t k = off[c]; k < off[c + 1]; ++k) {
+      const int sg = data[k];
+      const int j = sg >> 1;
+      if (j != last) g->idx.push_back((uint16_t)j);
+      last = j;
+    }
+  }
+  g->cells[(size_t)G * G] = (uint32_t)g->idx.size();
+}
+
 struct MeshBuild {
   std::vector<MeshNode<double>> nodes;
   std::vector<double> tris;   // leaf order, 9 per triangle
@@ -569,6 +734,25 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   std::vector<InstHdr> hd(n);
   std::vector<double> segd;
   std::vector<float4> segn;
+  std::vector<uint32_t> pcells;  // NATIVE polygon candidate grids: cell offsets, pair lists
+  std::vector<uint16_t> pidx;
+  struct GridFix {
+    size_t rec, cells, idx;
+  };
+  std::vector<GridFix> grid_fix;
+  std::vector<PolyGrid> grids;  // NATIVE polygon candidate grids, built in parallel
+  if (s->dom_kind == WOS_DOM_POLYGON) {
+    grids.resize(n);
+    const int nt = std::max(1, std::min(n, std::min(16, (int)std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
+    auto work = [&]() {
+      for (int i = next++; i < n; i = next++) build_poly_grid(probs[i].dom + 1, (int)probs[i].dom[0], &grids[i]);
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+  }
   std::vector<double> polard;  // POLAR tables, (bx, by) pairs
   std::vector<MeshNode<double>> mnodes;  // MESH: all instances' BVHs, triangles, normals
   std::vector<double> mtris, mfnorm;
@@ -630,7 +814,6 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       const int nv = (int)p.dom[0];
       const double* V = p.dom + 1;
       hd[i].seg_off = (int)(segd.size() / 4);
-      hd[i].rec_off = (int)segn.size();
       hd[i].n_seg = nv;
       std::vector<float> vx, vy, ux, uy;
       for (int k = 0; k < nv; ++k) {
@@ -647,9 +830,17 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
         ux.push_back((float)(ex / l2));
         uy.push_back((float)(ey / l2));
       }
-      // NATIVE records in segment pairs (wos_walk.cuh poly_scan): A_j = (x_2j, x_2j+1,
-      // y_2j, y_2j+1), U_j = (u_2j, u_2j+1 by component), then a closing A at vertex 0.
-      // An odd polygon gets a zero-length segment at vertex 0 (u = 0) as its pad.
+      // NATIVE records in segment pairs (wos_walk.cuh poly_scan): two header records
+      // (the candidate grid's box and offsets), then A_j = (x_2j, x_2j+1, y_2j, y_2j+1),
+      // U_j = (u_2j, u_2j+1 by component), then a closing A at vertex 0. An odd
+      // polygon gets a zero-length segment at vertex 0 (u = 0) as its pad.
+      const PolyGrid& g = grids[i];
+      segn.push_back(make_float4((float)g.lo[0], (float)g.lo[1], (float)g.ih[0], (float)g.ih[1]));
+      grid_fix.push_back({segn.size(), pcells.size(), pidx.size()});
+      segn.push_back(make_float4(bits_f32(g.G), 0.f, 0.f, 0.f));  // offsets patched below
+      pcells.insert(pcells.end(), g.cells.begin(), g.cells.end());
+      pidx.insert(pidx.end(), g.idx.begin(), g.idx.end());
+      hd[i].rec_off = (int)segn.size();
       if (nv & 1) {
         vx.push_back((float)V[0]);
         vy.push_back((float)V[1]);
@@ -822,6 +1013,20 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     if (e == cudaSuccess) e = cudaMemcpy(s->d_polar_f, polarf.data(), s->bytes_polar_f, cudaMemcpyHostToDevice);
   }
   if (!segd.empty()) {
+    // candidate grids: one buffer of 32-bit words, the cell offsets (rebased to the
+    // polygon's list) then the uint16 pair lists; header record 1 = (G, cells, idx16)
+    const size_t nw = pcells.size() + (pidx.size() + 1) / 2;
+    std::vector<uint32_t> gbuf(std::max<size_t>(nw, 1), 0u);
+    for (const PolyGrid& g : grids) s->poly_grid = s->poly_grid || g.G > 0;
+    for (const GridFix& f : grid_fix) {
+      float4& h1 = segn[f.rec];
+      h1.y = bits_f32((int)f.cells);
+      h1.z = bits_f32((int)(2 * pcells.size() + f.idx));
+    }
+    std::copy(pcells.begin(), pcells.end(), gbuf.begin());
+    if (!pidx.empty()) memcpy(gbuf.data() + pcells.size(), pidx.data(), pidx.size() * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_poly_grid, gbuf.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_poly_grid, gbuf.data(), gbuf.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_d, segd.size() * 8);
     if (e == cudaSuccess) e = cudaMalloc(&s->d_segs_f, segf.size() * 4);
     s->bytes_segs_n = segn.size() * sizeof(float4);
@@ -849,6 +1054,7 @@ extern "C" void wos_problem_set_destroy(wos_problem_set* s) {
   cudaFree(s->d_segs_d);
   cudaFree(s->d_segs_f);
   cudaFree(s->d_segs_n);
+  cudaFree(s->d_poly_grid);
   cudaFree(s->d_polar_d);
   cudaFree(s->d_polar_f);
   cudaFree(s->d_mesh_nodes_d);
@@ -1026,7 +1232,10 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
   return k;
 }
 
-static const size_t kSegStageMax = 96 * 1024;  // polygon records staged per CTA at most
+#ifndef WOS_SEG_STAGE_MAX
+#define WOS_SEG_STAGE_MAX (96 * 1024)
+#endif
+static const size_t kSegStageMax = WOS_SEG_STAGE_MAX;  // polygon records staged per CTA at most
 
 static size_t smem_bytes(size_t stage, size_t elem) {
   return stage + (size_t)kWarps * (kRing * elem + kSlots * 4 + kUQ * 4);
@@ -1051,10 +1260,14 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   } else {
     a.table = s->d_table_n;
     a.segs = s->d_segs_n;
+    a.nodes = s->d_poly_grid;
     a.stage_bytes = (int)s->bytes_f;
     a.sine_K = s->sine_K_native;
-    // polygon records go to shared memory when they fit (else read through L1)
-    if (s->bytes_segs_n > 0 && s->bytes_segs_n <= kSegStageMax) a.seg_stage_bytes = (int)s->bytes_segs_n;
+    // polygon records go to shared memory when they fit and the set has no candidate
+    // grids (grid queries touch a few records each: L1 serves them, and the freed
+    // shared memory buys occupancy)
+    if (s->bytes_segs_n > 0 && s->bytes_segs_n <= kSegStageMax && !s->poly_grid)
+      a.seg_stage_bytes = (int)s->bytes_segs_n;
     if (k.one) {
       // instance row and Philox4x32 round keys ride in the kernel parameters
       a.stage_bytes = 0;

@@ -303,14 +303,47 @@ struct Walker {
     return best;
   }
 
+  // candidate-grid query (wos_capi.cu build_poly_grid): the cell's ascending list of
+  // segment pairs; records the exact first nearest segment
+  __device__ static __forceinline__ float poly_grid_scan(const float4* __restrict__ R, float4 H0, int G, int cells_off,
+                                                         int idx_off, const uint32_t* __restrict__ gw,
+                                                         float px, float py, int* bi_out) {
+    const int cx = min(max((int)((px - H0.x) * H0.z), 0), G - 1);
+    const int cy = min(max((int)((py - H0.y) * H0.w), 0), G - 1);
+    const uint32_t* cell = gw + cells_off + cy * G + cx;
+    const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
+    const uint16_t* idx = reinterpret_cast<const uint16_t*>(gw) + idx_off;
+    float best = 3.0e38f;
+    int bi = 0;
+    for (uint32_t k = b; k < e; ++k) {
+      const int j = __ldg(idx + k);
+      const float2 d = pair_d2(__ldg(R + 2 * j), __ldg(R + 2 * j + 1), __ldg(R + 2 * j + 2), px, py);
+      if (d.x < best) {
+        best = d.x;
+        bi = 2 * j;
+      }
+      if (d.y < best) {
+        best = d.y;
+        bi = 2 * j + 1;
+      }
+    }
+    *bi_out = bi;
+    return best;
+  }
+
   __device__ static __forceinline__ Real poly_dist(Lane& l, const KArgs& a, const float4* srec) {
     if constexpr (S::NATIVE) {
       int bi;
       float best;
-      if (srec != nullptr)  // staged in shared memory
-        best = poly_scan(srec + l.rec_off, l.n_seg, l.x[0], l.x[1], &bi);
-      else
-        best = poly_scan(reinterpret_cast<const float4*>(a.segs) + l.rec_off, l.n_seg, l.x[0], l.x[1], &bi);
+      const float4* R = (srec != nullptr ? srec : reinterpret_cast<const float4*>(a.segs)) + l.rec_off;
+      const float4 H1 = R[-1];
+      const int G = __float_as_int(H1.x);
+      if (G > 0) {  // (sets with grids are never staged: R is global)
+        best = poly_grid_scan(R, R[-2], G, __float_as_int(H1.y), __float_as_int(H1.z),
+                              reinterpret_cast<const uint32_t*>(a.nodes), l.x[0], l.x[1], &bi);
+      } else {  // R: shared memory when staged, else global
+        best = poly_scan(R, l.n_seg, l.x[0], l.x[1], &bi);
+      }
       l.seg_i = bi;
       return fast_sqrt(best);
     } else {

@@ -143,3 +143,61 @@ def test_mesh_walk_harmonic_linear(gpu, mode):
     prob = Problem(MeshDomain(corners, faces), boundary_spec=(2, (1.0, 0.0, 0.0, 0.0)))
     (e,) = estimate(prob, [[0.25, 0.1, -0.4]], 20_000, WalkConfig(rng_seed=6, mode=mode))
     assert abs(e.mean - 0.25) < 4.0 * e.std_error
+
+
+def _brute_polygon(V, p):
+    """fp64 full scan: distance, closest point and FIRST nearest segment (the reference's
+    min over segments, geometry.py polygon adapter / oracle query())."""
+    A = V
+    B = np.roll(V, -1, axis=0)
+    E = B - A
+    W = p[None, :] - A
+    t = np.clip((W * E).sum(1) / (E * E).sum(1), 0.0, 1.0)
+    C = A + t[:, None] * E
+    d = np.hypot(*(p[None, :] - C).T)
+    k = int(np.argmin(d))
+    return d[k], C[k]
+
+
+def _comb_polygon(n=20):
+    """A concave comb: the unit square with n deep notches cut from the top edge, so
+    cell candidate lists mix near and far teeth."""
+    v = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0)]
+    for k in range(n - 1, -1, -1):
+        xa, xb = (k + 0.7) / n, (k + 0.3) / n
+        v += [(xa, 1.0), (xa, 0.35), (xb, 0.35), (xb, 1.0)]
+    v.append((0.0, 1.0))
+    return np.array(v)
+
+
+@pytest.mark.parametrize("mode,tol", [("replay", 1e-12), ("native", 3e-6)])
+@pytest.mark.parametrize("shape", ["star128", "star97", "comb"])
+def test_polygon_distance_candidate_grid(gpu, mode, tol, shape):
+    """Polygons with >= 24 vertices answer NATIVE queries through the candidate grid
+    (wos_capi.cu build_poly_grid): distance and closest point equal the full fp64 scan
+    (odd vertex counts add a zero-length pad segment; the comb is strongly concave)."""
+    from paper_2603_01193_b200 import PolygonDomain, star_polygon
+
+    if shape == "star128":
+        dom = star_polygon([0.07, -0.05, 0.04, 0.03], [0.02, 0.06, -0.04, 0.02], 128)
+    elif shape == "star97":
+        dom = star_polygon([0.3, -0.2, 0.1, 0.05], [0.1, 0.2, -0.1, 0.05], 97)
+    else:
+        dom = PolygonDomain(_comb_polygon())
+    V = np.asarray(dom.vertices, float)
+    assert len(V) >= 24
+    rng = np.random.default_rng(5)
+    lo, hi = V.min(0), V.max(0)
+    cand = lo + (hi - lo) * rng.random((6000, 2))
+    pts = cand[dom.contains(cand)][:300]
+    # and points hugging the boundary (where walks spend their steps)
+    mid = 0.5 * (V + np.roll(V, -1, axis=0))
+    cen = V.mean(0)
+    near = mid + 1e-3 * (cen - mid) / np.linalg.norm(cen - mid, axis=1)[:, None]
+    pts = np.vstack([pts, near[dom.contains(near)][:100]])
+    q, d = projections(dom, pts, mode)
+    for p, qi, di in zip(pts, q, d):
+        want_d, want_q = _brute_polygon(V, p)
+        assert abs(di - want_d) <= tol * max(1.0, want_d), (p, di, want_d)
+        # the closest point is on the boundary at the minimum distance
+        assert abs(np.hypot(*(p - qi)) - want_d) <= 10 * tol
