@@ -1550,11 +1550,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // are recorded and their lanes re-issued in the same divergent block right after
   // the step; unit grabs, retirement and the exit test run only when the unit or
   // the ring runs short. Re-issuing every iteration costs a divergent start per
-  // iteration, which pays off only when a jump is expensive (a 128-segment scan);
-  // cheap jumps use the batched refill of the general loop below (measured, cfg3
-  // vs cfg4: DESIGN.md section 3).
+  // iteration, which paid off (7 %) while a polygon jump was a full 128-segment
+  // scan; with the candidate grid the jump is cheap and the batched refill of the
+  // general loop below is as fast, so it is off by default (-D WOS_POLY_EAGER=1).
   // ======================================================================
-  constexpr bool kEager = (S::DOM == DOM_POLY);
+#ifndef WOS_POLY_EAGER
+#define WOS_POLY_EAGER 0
+#endif
+  constexpr bool kEager = WOS_POLY_EAGER && (S::DOM == DOM_POLY);
   if (kEager && fast) {
     while (true) {
       bool fin = false;
