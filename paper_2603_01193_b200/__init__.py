@@ -5,9 +5,11 @@ Drop-in for the reference package ``spherewalk``'s estimator path:
 ``walk_poisson_antithetic``, ``estimate``, ``PointEstimate``, and the
 epoch-averaged ``EstimateCache`` of the training-label loop — backed by
 hand-written sm_100a CUDA kernels in ``libwos_b200.so`` behind the C ABI of
-``include/wos_b200.h``. There is no CPU fallback.
+``include/wos_b200.h``. There is no CPU fallback. ``artifacts`` writes the
+reference CLI's solve / bench files (run stamp, CSV, summary) from GPU estimates.
 """
 
+from . import artifacts
 from .cache import CacheShapeError, EstimateCache, cache_update, export_csv
 from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, estimate_tensors
 from .engine import UnsupportedProblemError
