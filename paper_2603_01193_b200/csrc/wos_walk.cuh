@@ -156,6 +156,7 @@ struct Walker {
     Real sgn;
     const Real* row;  // this walk's instance row in the staged table (shared memory)
     int step;
+    Real d;        // distance to the boundary at x (jump-first loop: carried to the next jump)
     uint32_t seq;  // ESTIMATE: byte offset of the walk's ring slot; ROWS: row index
     uint64_t pid, tid, ikey;   // REPLAY counters / key
     uint32_t c1, c2, c3;       // NATIVE kHot: counter words
@@ -186,35 +187,8 @@ struct Walker {
   // ---------------- domains ----------------
   // distance to the boundary (positive inside)
   __device__ static __forceinline__ Real dist(Lane& l, const KArgs& a, const float4* srec) {
-    if constexpr (S::DOM == DOM_BALL) {
-      // geometry.py:196-206 / _kernels.py:329-339
-      Real s = Real(0);
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        Real u = l.x[i] - domp(l, a, i);
-        if constexpr (S::NATIVE) s = fmaf(u, u, s);
-        else s = s + u * u;
-      }
-      if constexpr (S::NATIVE) return domp(l, a, 3) - fast_sqrt(s);
-      else return pabs(domp(l, a, 3) - psqrt(s));
-    } else if constexpr (S::DOM == DOM_BOX) {
-      if constexpr (S::NATIVE) {
-        // min over axes of h_i - |x_i - c_i| (centre at [8, 11), half extent at [12, 15))
-        Real d = domp(l, a, 12) - fabsf(l.x[0] - domp(l, a, 8));
-#pragma unroll
-        for (int i = 1; i < DIM; ++i) d = fminf(d, domp(l, a, 12 + i) - fabsf(l.x[i] - domp(l, a, 8 + i)));
-        return d;
-      } else {
-        Real d = l.x[0] - domp(l, a, 0);
-        d = pmin(d, domp(l, a, 4) - l.x[0]);
-#pragma unroll
-        for (int i = 1; i < DIM; ++i) {
-          d = pmin(d, l.x[i] - domp(l, a, i));
-          d = pmin(d, domp(l, a, 4 + i) - l.x[i]);
-        }
-        return d;
-      }
-    } else if constexpr (S::DOM == DOM_POLAR) {
+    if constexpr (S::DOM == DOM_BALL || S::DOM == DOM_BOX) return dist_at(l, a, l.x);
+    else if constexpr (S::DOM == DOM_POLAR) {
       Real qx, qy;
       return polar_query(l, a, srec, l.x[0], l.x[1], &qx, &qy);
     } else if constexpr (S::DOM == DOM_MESH) {
@@ -223,6 +197,40 @@ struct Walker {
       return psqrt(mesh_d2(l, a, q));
     } else {
       return poly_dist(l, a, srec);
+    }
+  }
+
+  // closed-form domains: distance at any point x (the walk's, or a unit's start point)
+  __device__ static __forceinline__ Real dist_at(const Lane& l, const KArgs& a, const Real* x) {
+    if constexpr (S::DOM == DOM_BALL) {
+      // geometry.py:196-206 / _kernels.py:329-339
+      Real s = Real(0);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        Real u = x[i] - domp(l, a, i);
+        if constexpr (S::NATIVE) s = fmaf(u, u, s);
+        else s = s + u * u;
+      }
+      if constexpr (S::NATIVE) return domp(l, a, 3) - fast_sqrt(s);
+      else return pabs(domp(l, a, 3) - psqrt(s));
+    } else {
+      static_assert(S::DOM == DOM_BOX, "dist_at: closed-form domains only");
+      if constexpr (S::NATIVE) {
+        // min over axes of h_i - |x_i - c_i| (centre at [8, 11), half extent at [12, 15))
+        Real d = domp(l, a, 12) - fabsf(x[0] - domp(l, a, 8));
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) d = fminf(d, domp(l, a, 12 + i) - fabsf(x[i] - domp(l, a, 8 + i)));
+        return d;
+      } else {
+        Real d = x[0] - domp(l, a, 0);
+        d = pmin(d, domp(l, a, 4) - x[0]);
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) {
+          d = pmin(d, x[i] - domp(l, a, i));
+          d = pmin(d, domp(l, a, 4 + i) - x[i]);
+        }
+        return d;
+      }
     }
   }
 
@@ -1545,6 +1553,47 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
   };
 
+  // Loop order. Jump-first (default): an iteration jumps with the distance carried
+  // from the previous query, then queries the new position and records the walk at
+  // once if it terminated; a new walk queries its start when it is issued (and is
+  // recorded there with 0 steps if it starts in the shell). A walk of s jumps then
+  // occupies s iterations of its lane instead of s + 1 (test-first: the terminating
+  // query used an iteration of its own), so fewer lane slots of the jump block idle.
+  // Termination semantics are unchanged: d < eps first (hit), then step >= max_steps,
+  // the same state tested in the same order (walker.py:273-283).
+  // Closed-form domains only: a polygon / polar / mesh query costs more than the jump,
+  // and the extra divergent query of every issued walk outweighed the saved slots
+  // (cfg3 +9 %; cfg4 -1.7 %, cfg2 -12 % with it).
+#ifndef WOS_JUMP_FIRST
+#define WOS_JUMP_FIRST 1
+#endif
+  constexpr bool kJumpFirst = WOS_JUMP_FIRST && (S::DOM == DOM_BALL || S::DOM == DOM_BOX);
+  auto record = [&](Real d) {
+    // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
+    const Real v = W::finish_value(l, a);
+    lane_steps += (unsigned long long)l.step;
+    if constexpr (est) {
+      *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = v;
+      atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
+    } else {
+      a.out_values[l.seq] = (double)v;
+      a.out_steps[l.seq] = (int64_t)l.step;
+      // a dead walk (const kernel path) reports hit = 1 unless it also ran out of steps
+      a.out_hits[l.seq] = (uint8_t)(d < eps || (l.step < a.max_steps && W::dead(l, a)));
+    }
+    active = false;
+  };
+  // jump-first: query a freshly started walk; one starting in the shell ends here
+  auto first_query = [&]() {
+    if constexpr (kJumpFirst) {
+      l.d = W::dist(l, a, srec);
+      if (l.d < eps) record(l.d);
+    }
+  };
+  // the fast refill's walks all start at the cached point: its distance is queried once
+  // per unit (warp-uniform) and an in-shell start is a uniform branch
+  Real cu_d = Real(0);
+
   // ======================================================================
   // Eager fast path (ESTIMATE, one point per unit, polygon domains): finished walks
   // are recorded and their lanes re-issued in the same divergent block right after
@@ -1701,6 +1750,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
               cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
               cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
+              if constexpr (kJumpFirst && S::ONE) cu_d = W::dist_at(l, a, cu_x);
               if constexpr (S::NATIVE && S::ONE) {
                 // walk j0 + jj has tid = traj_start + j0 + jj (antithetic: jj even; j0 even)
                 const uint64_t tid0 = a.traj_start + cu_j0;
@@ -1740,6 +1790,12 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               }
               l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
               active = true;
+              if constexpr (kJumpFirst && S::ONE) {
+                l.d = cu_d;
+                if (cu_d < eps) record(cu_d);
+              } else {
+                first_query();
+              }
             } else {  // null item padding the point's last chunk: complete at once
               atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
             }
@@ -1792,6 +1848,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                        a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p, tid, sg);
               l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
               active = true;
+              first_query();
             } else {  // null item padding the last unit: complete at once
               atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
             }
@@ -1802,6 +1859,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                        a.row_tid[row], a.row_sign[row]);
               l.seq = (uint32_t)row;
               active = true;
+              first_query();
             }
           }
         }
@@ -1811,28 +1869,28 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 
     // ================= one step of every active walk =================
     if (active) {
-      const Real d = W::dist(l, a, srec);
-      if (d < eps || l.step >= a.max_steps || W::dead(l, a)) {
-        // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
-        const Real v = W::finish_value(l, a);
-        lane_steps += (unsigned long long)l.step;
-        if constexpr (est) {
-          *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = v;
-          atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
-        } else {
-          a.out_values[l.seq] = (double)v;
-          a.out_steps[l.seq] = (int64_t)l.step;
-          // a dead walk (const kernel path) reports hit = 1 unless it also ran out of steps
-          a.out_hits[l.seq] = (uint8_t)(d < eps || (l.step < a.max_steps && W::dead(l, a)));
-        }
-        active = false;
-      } else {
+      if constexpr (kJumpFirst) {
+        // the walk is live at l.d >= eps, step < max_steps (tested when l.d was queried)
         if constexpr (W::kScr) {
-          if constexpr (S::NATIVE) W::advance_screened_native(l, d, a);
-          else W::advance_screened_replay(l, d, a);
-        } else if constexpr (S::NATIVE) W::advance_native(l, d, a);
-        else W::advance_replay(l, d, a);
+          if constexpr (S::NATIVE) W::advance_screened_native(l, l.d, a);
+          else W::advance_screened_replay(l, l.d, a);
+        } else if constexpr (S::NATIVE) W::advance_native(l, l.d, a);
+        else W::advance_replay(l, l.d, a);
         l.step += 1;
+        l.d = W::dist(l, a, srec);
+        if (l.d < eps || l.step >= a.max_steps || W::dead(l, a)) record(l.d);
+      } else {
+        const Real d = W::dist(l, a, srec);
+        if (d < eps || l.step >= a.max_steps || W::dead(l, a)) {
+          record(d);
+        } else {
+          if constexpr (W::kScr) {
+            if constexpr (S::NATIVE) W::advance_screened_native(l, d, a);
+            else W::advance_screened_replay(l, d, a);
+          } else if constexpr (S::NATIVE) W::advance_native(l, d, a);
+          else W::advance_replay(l, d, a);
+          l.step += 1;
+        }
       }
     }
     idle = __ballot_sync(WOS_FULL, !active);
