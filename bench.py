@@ -244,7 +244,7 @@ def main():
     shard = w.subset(idx)
     ctx = engine.get_context(local)
     if args.refill_min or args.blocks_per_sm:
-        ctx.set_tuning(args.refill_min or 4, args.blocks_per_sm or 0)
+        ctx.set_tuning(args.refill_min or 5, args.blocks_per_sm or 0)
     pset = engine.ProblemSet(ctx, w.problems)
     pts = torch.from_numpy(np.ascontiguousarray(shard.points)).to(dev)
     ids = torch.from_numpy(np.ascontiguousarray(shard.point_ids)).to(dev)

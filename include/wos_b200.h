@@ -307,7 +307,7 @@ int wos_philox4x32(wos_context* ctx, int64_t n, const uint32_t* ctr, uint32_t ke
 
 /* ---- launch tuning ---------------------------------------------------- */
 /* refill_min: a warp refills idle lanes once at least this many are idle
- * (1..32, default 4). blocks_per_sm: persistent grid = SMs * blocks_per_sm (0 = auto). */
+ * (1..32, default 5). blocks_per_sm: persistent grid = SMs * blocks_per_sm (0 = auto). */
 int wos_set_tuning(wos_context* ctx, int32_t refill_min, int32_t blocks_per_sm);
 
 /* ---- roofline probes ---------------------------------------------------

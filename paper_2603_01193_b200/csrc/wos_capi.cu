@@ -70,7 +70,7 @@ struct wos_context {
   int64_t host_exterior = -1;
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
-  int refill_min = 4;
+  int refill_min = 5;  // measured optimum with the jump-first loop (4..6 within 1.5 %)
   int blocks_per_sm = 0;
   std::mutex mu;  // serialises the *_host entry points' scratch
 };

@@ -141,7 +141,7 @@ class Context:
         except Exception:
             pass
 
-    def set_tuning(self, refill_min: int = 4, blocks_per_sm: int = 0):
+    def set_tuning(self, refill_min: int = 5, blocks_per_sm: int = 0):
         _lib.check(self._lib.wos_set_tuning(self.handle, int(refill_min), int(blocks_per_sm)))
 
     def probe_peaks(self):

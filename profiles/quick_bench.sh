@@ -2,7 +2,7 @@
 # quick per-config timing (no CPU baseline); usage: quick_bench.sh "4 3" [refill_min]
 # small configs run with label replicas per launch (cfg0 x64, cfg1 x16, cfg2 x16)
 CFGS=${1:-"4"}
-R=${2:-4}
+R=${2:-5}
 for c in $CFGS; do
   case $c in 0) REP=64;; 1) REP=16;; 2) REP=16;; *) REP=1;; esac
   timeout 120 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --config $c --replicas $REP --refill-min $R > gpurun_out/qb_$c.log 2>&1
