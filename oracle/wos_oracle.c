@@ -701,14 +701,23 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       *hit = (uint8_t)shell;
       return;
     }
-    /* one Philox4x32 block per jump at counter (2*step, pid, tid, hi-words) */
+    /* one Philox4x32 block per jump at counter (2*step, pid, tid, hi-words); a
+       source-free jump needs one word (2D) or two (3D), so a block serves 4 (2D) or
+       2 (3D) consecutive jumps: jump s reads the block at counter 2*floor(s/per)
+       (wos_walk.cuh kPerBlock) */
+    const int per = has_src ? 1 : (dim == 2 ? 4 : 2);
+    const int sub = (int)(step % per);
     uint32_t u[4];
     {
-      uint32_t ca[4] = {(uint32_t)(2 * step), c1, c2, c3};
+      uint32_t ca[4] = {(uint32_t)(2 * (step / per)), c1, c2, c3};
       philox4x32(ca, k0, k1, u);
     }
     double dir[3];
-    if (dim == 2) {
+    if (dim == 2 && !has_src) {
+      double th = TWO_PI * u23(u[sub]);
+      dir[0] = cos(th);
+      dir[1] = sin(th);
+    } else if (dim == 2) {
       double th = TWO_PI * u23(u[0]);
       dir[0] = cos(th);
       dir[1] = sin(th);
@@ -719,9 +728,9 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
         acc -= (d * d * 0.25) * source(pb, g);
       }
     } else if (!has_src) {
-      double z = 2.0 * u23(u[0]) - 1.0;
+      double z = 2.0 * u23(u[2 * sub]) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
-      double phi = TWO_PI * u23(u[1]);
+      double phi = TWO_PI * u23(u[2 * sub + 1]);
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;

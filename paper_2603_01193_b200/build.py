@@ -31,6 +31,7 @@ UNITS = {
     "wos_capi.cu": [],
     "wos_kernels_native.cu": [],
     "wos_kernels_native_est.cu": [],
+    "wos_kernels_native_est_bc.cu": [],
     "wos_kernels_native_rows.cu": [],
     "wos_kernels_replay_f64.cu": ["--fmad=false"],
     "wos_kernels_replay_f32.cu": ["--fmad=false"],

@@ -1226,7 +1226,7 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
   } else {
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
     k.one = (s->n == 1 && s->stride <= kCP);
-    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows);
+    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows, s->bnd_kind == WOS_BND_CONST);
     k.elem = 4;
   }
   return k;

@@ -6,8 +6,10 @@ namespace wos {
 // rows = walk_poisson_values sink (per-walk outputs) instead of the per-point estimate
 const void* get_kernel_replay_f64(int dim, int dom, int src, int sk, bool rows);
 const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows);
-// one = single-instance launch (instance row + Philox keys in the kernel parameters)
-const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows);
+// one = single-instance launch (instance row + Philox keys in the kernel parameters);
+// bnd_const = the boundary value is a constant (single-instance estimate kernels
+// then drop the deferred-recording path)
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const);
 }  // namespace wos
 
 // host helpers shared by the C-ABI units (defined in wos_capi.cu)

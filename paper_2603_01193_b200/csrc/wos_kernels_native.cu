@@ -4,8 +4,11 @@
 namespace wos {
 const void* get_kernel_native_est(int dim, int dom, int src, int sk, bool one);
 const void* get_kernel_native_rows(int dim, int dom, int src, int sk, bool one);
+const void* get_kernel_native_est_bc(int dim, int dom, int src, int sk, bool one);
 
-const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows) {
-  return rows ? get_kernel_native_rows(dim, dom, src, sk, one) : get_kernel_native_est(dim, dom, src, sk, one);
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const) {
+  if (rows) return get_kernel_native_rows(dim, dom, src, sk, one);
+  if (one && bnd_const) return get_kernel_native_est_bc(dim, dom, src, sk, one);
+  return get_kernel_native_est(dim, dom, src, sk, one);
 }
 }  // namespace wos

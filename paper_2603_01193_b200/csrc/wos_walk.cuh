@@ -116,11 +116,17 @@ __device__ __forceinline__ void native_uniforms7(uint4 W, float f[7]) {
   f[6] = f12_m12((W.z << 14) | ((W.w << 5) & 0x3800u));
 }
 
-template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false, int SINK_ = SINK_ESTIMATE>
+// BC_: single-instance launch of a problem whose boundary value is a constant
+// (a.bnd_c): the walk value is acc + g with no projection, so the kernel carries
+// no deferred-recording code (it only costs registers and issue there)
+template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false, int SINK_ = SINK_ESTIMATE,
+          bool BC_ = false>
 struct Spec {
   static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_, SINK = SINK_;
   static constexpr bool NATIVE = (MODE_ == MODE_NATIVE_F32);
   static constexpr bool ONE = ONE_;
+  static constexpr bool BC = BC_;
+  static_assert(!BC_ || ONE_, "constant-boundary kernels are single-instance launches");
   using Real = typename std::conditional<MODE_ == MODE_REPLAY_F64, double, float>::type;
   static_assert(!ONE_ || MODE_ == MODE_NATIVE_F32, "single-instance launches are NATIVE only");
 };
@@ -1152,6 +1158,7 @@ struct Walker {
       }
       return (l.acc + l.thr * g) / l.sa;
     }
+    if constexpr (S::BC) return l.acc + a.bnd_c;
     if constexpr (ONE) {
       if (a.bnd_kind == BND_CONST) return l.acc + a.bnd_c;
     }
@@ -1224,8 +1231,17 @@ struct Walker {
     for (int i = 0; i < DIM; ++i) l.x[i] += sg * d * dir[i];
   }
 
+  // Source-free NATIVE walks need one uniform per jump in 2D and two in 3D, so a block
+  // serves kPerBlock consecutive jumps: jump s takes word s % 4 (2D) / words
+  // 2 (s % 2), 2 (s % 2) + 1 (3D) of the block at counter 2 floor(s / kPerBlock).
+  // Kernels whose lanes run in phase lock (the amortised loop) draw each block once;
+  // the others redraw it per jump and select the words (same stream).
+  static constexpr int kPerBlock = (S::NATIVE && S::SRC == SRC_NONE) ? (DIM == 2 ? 4 : 2) : 1;
+
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
-    const uint32_t c0 = 2u * (uint32_t)l.step;
+    return native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)kPerBlock));
+  }
+  __device__ static __forceinline__ uint4 native_block_at(const Lane& l, const KArgs& a, uint32_t c0) {
     if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1);
     else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1);
     else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1);
@@ -1246,14 +1262,41 @@ struct Walker {
       l.pc = philox_pre(c1, c2, c3, a.nkey0, l.k1, a.nkey0 + 0x9E3779B9u, l.k1 + 0xBB67AE85u);
   }
 
+  // source-free NATIVE jumps from their words of the block (kPerBlock above)
+  __device__ static __forceinline__ void move_native_2d(Lane& l, float d, uint32_t w) {
+    float sth, cth;
+    __sincosf(fmaf(f12(w), kTwoPiF, -kTwoPiF), &sth, &cth);
+    const float sd = l.sgn * d;
+    l.x[0] = fmaf(sd, cth, l.x[0]);
+    l.x[1] = fmaf(sd, sth, l.x[1]);
+  }
+  __device__ static __forceinline__ void move_native_3d(Lane& l, float d, uint32_t wz, uint32_t wphi) {
+    const float z = f2x(wz) - 3.0f;
+    const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
+    float sph, cph;
+    __sincosf(fmaf(f12(wphi), kTwoPiF, -kTwoPiF), &sph, &cph);
+    const float sd = l.sgn * d, sdxy = sd * sxy;
+    l.x[0] = fmaf(sdxy, cph, l.x[0]);
+    l.x[1] = fmaf(sdxy, sph, l.x[1]);
+    l.x[2] = fmaf(sd, z, l.x[2]);
+  }
+  // the block's words for sub-jump k of an amortised round
+  __device__ static __forceinline__ void move_native_word(Lane& l, float d, const uint4& B, int k) {
+    if constexpr (DIM == 2) move_native_2d(l, d, k == 0 ? B.x : k == 1 ? B.y : k == 2 ? B.z : B.w);
+    else move_native_3d(l, d, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
+  }
+
   // NATIVE: Green's-function importance sampling, fp32 fast math, one Philox block
   __device__ static __forceinline__ void advance_native(Lane& l, float d, const KArgs& a) {
     const uint4 A = native_block(l, a);
     const float sd = l.sgn * d;
-    if constexpr (DIM == 2) {
+    if constexpr (DIM == 2 && S::SRC == SRC_NONE) {
+      const uint32_t k = (uint32_t)l.step & 3u;
+      move_native_2d(l, d, k == 0 ? A.x : k == 1 ? A.y : k == 2 ? A.z : A.w);
+    } else if constexpr (DIM == 2) {
       float sth, cth;
       __sincosf(fmaf(f12(A.x), kTwoPiF, -kTwoPiF), &sth, &cth);
-      if constexpr (S::SRC != SRC_NONE) {
+      {
         float sph, cph;
         __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
         const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
@@ -1264,14 +1307,8 @@ struct Walker {
       l.x[0] = fmaf(sd, cth, l.x[0]);
       l.x[1] = fmaf(sd, sth, l.x[1]);
     } else if constexpr (S::SRC == SRC_NONE) {
-      const float z = f2x(A.x) - 3.0f;
-      const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
-      float sph, cph;
-      __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
-      const float sdxy = sd * sxy;
-      l.x[0] = fmaf(sdxy, cph, l.x[0]);
-      l.x[1] = fmaf(sdxy, sph, l.x[1]);
-      l.x[2] = fmaf(sd, z, l.x[2]);
+      const bool odd = (l.step & 1) != 0;
+      move_native_3d(l, d, odd ? A.z : A.x, odd ? A.w : A.y);
     } else {
       float u[7];
       native_uniforms7(A, u);
@@ -1568,6 +1605,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #define WOS_JUMP_FIRST 1
 #endif
   constexpr bool kJumpFirst = WOS_JUMP_FIRST && (S::DOM == DOM_BALL || S::DOM == DOM_BOX);
+  // Amortised RNG (source-free NATIVE walks on closed-form domains): lanes are refilled
+  // only between rounds of kPerBlock jumps, so every live lane enters a round at a step
+  // that is a multiple of kPerBlock and one Philox block serves the whole round.
+#ifndef WOS_AMORT_RNG
+#define WOS_AMORT_RNG 1
+#endif
+  constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1;
   auto record = [&](Real d) {
     // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
     const Real v = W::finish_value(l, a);
@@ -1583,11 +1627,39 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
     active = false;
   };
+  // Deferred recording. An expensive boundary term (Fourier / arc-length series,
+  // projections) evaluated when a walk ends runs with the one or two lanes that ended
+  // in that step while the rest of the warp waits, once per step. A finished lane
+  // instead keeps its walk's state in registers (it idles until the next refill
+  // anyway) and all such lanes are recorded together at the next refill: one pass per
+  // refill instead of one per step. Constant boundaries record at once (no gain).
+#ifndef WOS_DEFER_RECORD
+#define WOS_DEFER_RECORD 1
+#endif
+  const bool defer = WOS_DEFER_RECORD && !S::BC && a.bnd_kind != BND_CONST;
+  bool pend = false;
+  auto finish = [&](Real d) {
+    if (defer) {
+      l.d = d;
+      pend = true;
+      active = false;
+    } else {
+      record(d);
+    }
+  };
+  auto flush = [&]() {
+    if (defer && __any_sync(WOS_FULL, pend)) {
+      if (pend) {
+        record(l.d);
+        pend = false;
+      }
+    }
+  };
   // jump-first: query a freshly started walk; one starting in the shell ends here
   auto first_query = [&]() {
     if constexpr (kJumpFirst) {
       l.d = W::dist(l, a, srec);
-      if (l.d < eps) record(l.d);
+      if (l.d < eps) finish(l.d);
     }
   };
   // the fast refill's walks all start at the cached point: its distance is queried once
@@ -1703,7 +1775,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   } else
   while (true) {
     const int n_idle = __popc(idle);
-    if (n_idle >= a.refill_min || n_idle == 32) {
+    if (n_idle >= (kAmort ? 1 : a.refill_min) || n_idle == 32) {
+      flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
       if constexpr (est) {
@@ -1792,7 +1865,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               active = true;
               if constexpr (kJumpFirst && S::ONE) {
                 l.d = cu_d;
-                if (cu_d < eps) record(cu_d);
+                if (cu_d < eps) finish(cu_d);
               } else {
                 first_query();
               }
@@ -1868,7 +1941,21 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
 
     // ================= one step of every active walk =================
-    if (active) {
+    if constexpr (kAmort) {
+      // one round: kPerBlock jumps of every live lane from one Philox block
+      if (active) {
+        const uint4 B = W::native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)W::kPerBlock));
+#pragma unroll
+        for (int k = 0; k < W::kPerBlock; ++k) {
+          if (active) {
+            W::move_native_word(l, l.d, B, k);
+            l.step += 1;
+            l.d = W::dist(l, a, srec);
+            if (l.d < eps || l.step >= a.max_steps) finish(l.d);
+          }
+        }
+      }
+    } else if (active) {
       if constexpr (kJumpFirst) {
         // the walk is live at l.d >= eps, step < max_steps (tested when l.d was queried)
         if constexpr (W::kScr) {
@@ -1878,11 +1965,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         else W::advance_replay(l, l.d, a);
         l.step += 1;
         l.d = W::dist(l, a, srec);
-        if (l.d < eps || l.step >= a.max_steps || W::dead(l, a)) record(l.d);
+        if (l.d < eps || l.step >= a.max_steps || W::dead(l, a)) finish(l.d);
       } else {
         const Real d = W::dist(l, a, srec);
         if (d < eps || l.step >= a.max_steps || W::dead(l, a)) {
-          record(d);
+          finish(d);
         } else {
           if constexpr (W::kScr) {
             if constexpr (S::NATIVE) W::advance_screened_native(l, d, a);
