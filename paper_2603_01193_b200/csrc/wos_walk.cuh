@@ -1943,17 +1943,21 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     // ================= one step of every active walk =================
     if constexpr (kAmort) {
       // one round: kPerBlock jumps of every live lane from one Philox block
+      // (a lane whose walk ends mid-round stops moving and is finished after the round:
+      // the sub-jumps stay straight-line predicated code)
       if (active) {
         const uint4 B = W::native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)W::kPerBlock));
+        bool live = true;
 #pragma unroll
         for (int k = 0; k < W::kPerBlock; ++k) {
-          if (active) {
+          if (live) {
             W::move_native_word(l, l.d, B, k);
             l.step += 1;
             l.d = W::dist(l, a, srec);
-            if (l.d < eps || l.step >= a.max_steps) finish(l.d);
+            live = !(l.d < eps || l.step >= a.max_steps);
           }
         }
+        if (!live) finish(l.d);
       }
     } else if (active) {
       if constexpr (kJumpFirst) {
