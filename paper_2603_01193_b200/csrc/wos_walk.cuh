@@ -1242,7 +1242,13 @@ struct Walker {
     return native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)kPerBlock));
   }
   __device__ static __forceinline__ uint4 native_block_at(const Lane& l, const KArgs& a, uint32_t c0) {
-    if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1);
+// the hot kernels fold too since the jump-first loop made refills cheaper (cfg4 -0.7 %;
+// it had cost +1.7 % with the test-first loop)
+#ifndef WOS_HOT_FOLD
+#define WOS_HOT_FOLD 1
+#endif
+    if constexpr (kHot && WOS_HOT_FOLD) return philox4x32_rk_pre(c0, l.pc, l.hk0, l.hk1);
+    else if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1);
     else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1);
     else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1);
   }
@@ -1250,9 +1256,9 @@ struct Walker {
   // the walk's Philox counter words (c1, c2, c3) folded through rounds 0-1 (wos_rng.cuh)
   __device__ static __forceinline__ void set_counter(Lane& l, const KArgs& a, uint32_t c1, uint32_t c2,
                                                      uint32_t c3) {
-    // kHot walks are short against the refill cadence: the per-walk fold would cost a
-    // warp more at each refill than it saves per step (measured on cfg4)
-    if constexpr (kHot) {
+    if constexpr (kHot && WOS_HOT_FOLD) {
+      l.pc = philox_pre(c1, c2, c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+    } else if constexpr (kHot) {
       l.c1 = c1;
       l.c2 = c2;
       l.c3 = c3;
