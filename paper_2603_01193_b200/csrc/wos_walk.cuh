@@ -420,7 +420,22 @@ struct Walker {
 
   // closest boundary point at termination
   __device__ static __forceinline__ void project(const Lane& l, const KArgs& a, Real* q) {
-    if constexpr (S::DOM == DOM_BALL) {
+    if constexpr (S::DOM == DOM_BALL && S::NATIVE) {
+      // explicit fma / IEEE sqrt and division: every kernel variant (estimate or rows
+      // sink, single- or multi-instance) rounds the projection alike
+      float s = 0.0f, u[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        u[i] = l.x[i] - domp(l, a, i);
+        s = fmaf(u[i], u[i], s);
+      }
+      const float rho = __fsqrt_rn(s), R = domp(l, a, 3);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        const float dir = (rho == 0.0f) ? (i == 0 ? 1.0f : 0.0f) : __fdiv_rn(u[i], rho);
+        q[i] = fmaf(R, dir, domp(l, a, i));
+      }
+    } else if constexpr (S::DOM == DOM_BALL) {
       Real s = Real(0), u[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
