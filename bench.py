@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=1,
                     help="independent label replicas per point per step (small configs)")
     ap.add_argument("--refill-min", type=int, default=None)
+    ap.add_argument("--refill-min-deferred", type=int, default=None)
     ap.add_argument("--blocks-per-sm", type=int, default=None)
     args = ap.parse_args()
 
@@ -243,8 +244,8 @@ def main():
     idx = shard_indices(w.n_points, rank, world)
     shard = w.subset(idx)
     ctx = engine.get_context(local)
-    if args.refill_min or args.blocks_per_sm:
-        ctx.set_tuning(args.refill_min or 5, args.blocks_per_sm or 0)
+    if args.refill_min or args.blocks_per_sm or args.refill_min_deferred:
+        ctx.set_tuning(args.refill_min or 5, args.blocks_per_sm or 0, args.refill_min_deferred or 12)
     pset = engine.ProblemSet(ctx, w.problems)
     pts = torch.from_numpy(np.ascontiguousarray(shard.points)).to(dev)
     ids = torch.from_numpy(np.ascontiguousarray(shard.point_ids)).to(dev)

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define WOS_ABI_VERSION 2
+#define WOS_ABI_VERSION 3
 
 /* ---- status codes ---------------------------------------------------- */
 typedef enum wos_status {
@@ -309,6 +309,10 @@ int wos_philox4x32(wos_context* ctx, int64_t n, const uint32_t* ctr, uint32_t ke
 /* refill_min: a warp refills idle lanes once at least this many are idle
  * (1..32, default 5). blocks_per_sm: persistent grid = SMs * blocks_per_sm (0 = auto). */
 int wos_set_tuning(wos_context* ctx, int32_t refill_min, int32_t blocks_per_sm);
+/* refill threshold of launches that defer recording finished walks to the refill
+ * (non-constant boundary terms: recording pays once per refill, so larger batches
+ * win; 1..32, default 12). ABI version 3. */
+int wos_set_refill_deferred(wos_context* ctx, int32_t refill_min);
 
 /* ---- roofline probes ---------------------------------------------------
  * Measured on the device of ctx: MUFU (SFU) op/s and FP32 flop/s (FFMA = 2)

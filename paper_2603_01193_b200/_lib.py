@@ -36,7 +36,7 @@ WOS_ERR_CUDA = 3
 WOS_ERR_EXTERIOR = 4
 WOS_ERR_NOMEM = 5
 WOS_ERR_MAJORANT = 6
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("WOS_B200_LIB") or os.path.join(_HERE, "libwos_b200.so")
@@ -123,6 +123,7 @@ _SIGNATURES = {
     "wos_philox4x64": (c_int32, [_P, c_int64, _P, c_uint64, c_uint64, _P, _P]),
     "wos_philox4x32": (c_int32, [_P, c_int64, _P, c_uint32, c_uint32, _P, _P]),
     "wos_set_tuning": (c_int32, [_P, c_int32, c_int32]),
+    "wos_set_refill_deferred": (c_int32, [_P, c_int32]),
     "wos_probe_peaks": (
         c_int32,
         [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double), POINTER(c_int32)],

@@ -71,6 +71,7 @@ struct wos_context {
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
   int refill_min = 5;  // measured optimum with the jump-first loop (4..6 within 1.5 %)
+  int refill_min_deferred = 12;  // launches with deferred recording (8..16 within 3 % on cfg1-3)
   int blocks_per_sm = 0;
   std::mutex mu;  // serialises the *_host entry points' scratch
 };
@@ -189,6 +190,13 @@ extern "C" int wos_set_tuning(wos_context* c, int32_t refill_min, int32_t blocks
   if (blocks_per_sm < 0 || blocks_per_sm > 32) return fail(WOS_ERR_INVALID, "blocks_per_sm must be 0..32");
   c->refill_min = refill_min;
   c->blocks_per_sm = blocks_per_sm;
+  return WOS_OK;
+}
+
+extern "C" int wos_set_refill_deferred(wos_context* c, int32_t refill_min) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (refill_min < 1 || refill_min > 32) return fail(WOS_ERR_INVALID, "refill_min must be 1..32");
+  c->refill_min_deferred = refill_min;
   return WOS_OK;
 }
 
@@ -1302,6 +1310,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.bnd_kind = s->bnd_kind;
   a.bnd_M = s->bnd_M;
   a.refill_min = c->refill_min;
+  a.refill_min_deferred = c->refill_min_deferred;
   a.eps = cfg->eps;
   a.eps_f = (float)cfg->eps;
   a.max_steps = (int32_t)std::min<int64_t>(cfg->max_steps, 0x7fffffff);

@@ -72,6 +72,7 @@ struct KArgs {
   int32_t bnd_kind;
   int32_t bnd_M;        // Fourier / arc-length order (uniform over the set; padded)
   int32_t refill_min;   // refill idle lanes once this many are idle
+  int32_t refill_min_deferred;  // ... in launches that defer recording finished walks
   float bnd_c;          // single-instance NATIVE launches: the BND_CONST boundary value
   // ---- walk config ----
   double eps;

@@ -141,8 +141,9 @@ class Context:
         except Exception:
             pass
 
-    def set_tuning(self, refill_min: int = 5, blocks_per_sm: int = 0):
+    def set_tuning(self, refill_min: int = 5, blocks_per_sm: int = 0, refill_min_deferred: int = 12):
         _lib.check(self._lib.wos_set_tuning(self.handle, int(refill_min), int(blocks_per_sm)))
+        _lib.check(self._lib.wos_set_refill_deferred(self.handle, int(refill_min_deferred)))
 
     def probe_peaks(self):
         sfu, fp32, clk = c_double(), c_double(), c_double()

@@ -164,7 +164,7 @@ def test_native_determinism_and_layout_invariance(gpu):
     assert np.array_equal(d[0], a[0][:7])
     ctx = engine.get_context(0)
     try:
-        ctx.set_tuning(refill_min=17, blocks_per_sm=1)
+        ctx.set_tuning(refill_min=17, blocks_per_sm=1, refill_min_deferred=3)
         e = estimate_arrays(w.problems, w.points, 256, w.cfg, point_ids=w.point_ids)
     finally:
         ctx.set_tuning()

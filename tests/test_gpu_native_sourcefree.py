@@ -106,3 +106,24 @@ def test_sourcefree_multi_instance_equals_single(gpu, dim, dom, bnd):
         sel = inst == k
         m1, q1, _ = estimate_arrays([probs[k]], pts[sel], 64, cfg, point_ids=np.flatnonzero(sel))
         np.testing.assert_allclose(mean[sel], m1, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("dim,dom", [(2, "ball"), (3, "box"), (2, "poly")])
+def test_deferred_recording_is_tuning_invariant(gpu, dim, dom):
+    """Deferred recording changes when a finished walk is recorded, never its value or
+    its place in the per-point reduction: estimates are bitwise identical for any
+    refill thresholds and launch shape."""
+    from paper_2603_01193_b200 import WalkConfig, engine, estimate_arrays
+
+    prob = _problem(dim, dom, "linear")
+    pts = _points(prob.domain, dim, 64, seed=5)
+    cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=2)
+    ref = estimate_arrays([prob], pts, 300, cfg)
+    ctx = engine.get_context(0)
+    try:
+        for rm, rmd, bps in ((5, 1, 0), (3, 32, 1), (17, 7, 2)):
+            ctx.set_tuning(refill_min=rm, blocks_per_sm=bps, refill_min_deferred=rmd)
+            got = estimate_arrays([prob], pts, 300, cfg)
+            assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    finally:
+        ctx.set_tuning()
