@@ -311,7 +311,7 @@ int wos_philox4x32(wos_context* ctx, int64_t n, const uint32_t* ctr, uint32_t ke
 int wos_set_tuning(wos_context* ctx, int32_t refill_min, int32_t blocks_per_sm);
 /* refill threshold of launches that defer recording finished walks to the refill
  * (non-constant boundary terms: recording pays once per refill, so larger batches
- * win; 1..32, default 12). ABI version 3. */
+ * win; delta-tracking launches keep refill_min; 1..32, default 12). ABI version 3. */
 int wos_set_refill_deferred(wos_context* ctx, int32_t refill_min);
 
 /* ---- roofline probes ---------------------------------------------------

@@ -1796,7 +1796,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   } else
   while (true) {
     const int n_idle = __popc(idle);
-    if (n_idle >= (defer ? a.refill_min_deferred : kAmort ? 1 : a.refill_min) || n_idle == 32) {
+    // (delta tracking: a step costs far more than recording, so the plain threshold)
+    if (n_idle >= ((defer && !W::kScr) ? a.refill_min_deferred : kAmort ? 1 : a.refill_min) || n_idle == 32) {
       flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
