@@ -123,7 +123,6 @@ def cpu_baseline(w, budget_s=12.0, nthreads=None):
     nthreads = nthreads or O.default_threads()
     O.load()
     n = 64
-    stride = max(1, w.n_points // n)
     t_used = 0.0
     while True:
         idx = np.arange(0, w.n_points, max(1, w.n_points // n))[:n]
@@ -137,7 +136,6 @@ def cpu_baseline(w, budget_s=12.0, nthreads=None):
         if dt >= budget_s * 0.5 or n >= w.n_points or t_used > budget_s * 2:
             break
         n = min(w.n_points, int(n * max(2.0, min(16.0, budget_s * 0.6 / max(dt, 1e-3)))))
-    del stride
     return {
         "value": steps / dt,
         "unit": "walk-steps/s",
