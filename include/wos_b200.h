@@ -321,6 +321,13 @@ int wos_set_refill_deferred(wos_context* ctx, int32_t refill_min);
 int wos_probe_peaks(wos_context* ctx, double* out_sfu_ops_per_s, double* out_fp32_flops_per_s,
                     double* out_sm_clock_hz, int32_t* out_num_sms);
 
+/* ---- fast-math error probe (ABI 3) -------------------------------------
+ * The NATIVE kernels' fast-math primitives on device arrays x [n] fp32: __sincosf,
+ * sqrt.approx(|x|), ex2.approx(x), so their error can be bounded against libm
+ * (north-star: a fast-math path whose error is bounded against the reference).  */
+int wos_fastmath_probe(wos_context* ctx, int64_t n, const float* x, float* out_sin, float* out_cos,
+                       float* out_sqrt, float* out_ex2, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,6 +124,7 @@ _SIGNATURES = {
     "wos_philox4x32": (c_int32, [_P, c_int64, _P, c_uint32, c_uint32, _P, _P]),
     "wos_set_tuning": (c_int32, [_P, c_int32, c_int32]),
     "wos_set_refill_deferred": (c_int32, [_P, c_int32]),
+    "wos_fastmath_probe": (c_int32, [_P, c_int64, _P, _P, _P, _P, _P, _P]),
     "wos_probe_peaks": (
         c_int32,
         [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double), POINTER(c_int32)],

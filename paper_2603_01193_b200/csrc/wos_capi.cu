@@ -1758,6 +1758,17 @@ __global__ void __launch_bounds__(256) probe_ffma_kernel(int iters, float seed, 
   if (s == 1234.5f) sink[0] = s;
 }
 
+extern "C" int wos_fastmath_probe(wos_context* c, int64_t n, const float* x, float* out_sin, float* out_cos,
+                                  float* out_sqrt, float* out_ex2, void* stream) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (n < 0 || (n > 0 && (!x || !out_sin || !out_cos || !out_sqrt || !out_ex2)))
+    return fail(WOS_ERR_INVALID, "bad fastmath probe arguments");
+  CUDA_TRY(cudaSetDevice(wos_context_device(c)));
+  const int err = launch_fastmath_probe(n, x, out_sin, out_cos, out_sqrt, out_ex2, stream);
+  if (err) return fail(WOS_ERR_CUDA, "fastmath probe: %s", cudaGetErrorString((cudaError_t)err));
+  return WOS_OK;
+}
+
 extern "C" int wos_probe_peaks(wos_context* c, double* sfu, double* fp32, double* clk, int32_t* nsm) {
   if (!c) return fail(WOS_ERR_INVALID, "null context");
   CUDA_TRY(cudaSetDevice(c->device));

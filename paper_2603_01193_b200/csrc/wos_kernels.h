@@ -1,5 +1,6 @@
 // Kernel registry: one lookup per numeric mode (each compiled in its own unit).
 #pragma once
+#include <stdint.h>
 
 namespace wos {
 // Returns the __global__ entry for (dim, domain, source, sine order) or nullptr.
@@ -10,6 +11,8 @@ const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows);
 // bnd_const = the boundary value is a constant (single-instance estimate kernels
 // then drop the deferred-recording path)
 const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const);
+// fast-math primitives of the NATIVE kernels on given arguments (returns a cudaError_t)
+int launch_fastmath_probe(int64_t n, const float* x, float* s, float* c, float* q, float* e, void* stream);
 }  // namespace wos
 
 // host helpers shared by the C-ABI units (defined in wos_capi.cu)

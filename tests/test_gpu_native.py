@@ -46,7 +46,8 @@ def test_native_rows_match_native_oracle(gpu, cfg):
     m = s == so
     rms = np.sqrt(np.mean(vo**2)) + 1e-30
     err = np.abs(v[m] - vo[m]) / np.maximum(np.abs(vo[m]), rms)
-    assert np.quantile(err, 0.99) < 1e-3, f"p99 rel err {np.quantile(err, 0.99):.2e}"
+    # fast-math bound in the estimator (measured p99 <= 1.4e-5)
+    assert np.quantile(err, 0.99) < 1e-4, f"p99 rel err {np.quantile(err, 0.99):.2e}"
 
 
 def _z(m1, se1, m2, se2):
