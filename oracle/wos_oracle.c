@@ -38,6 +38,8 @@
 #include <string.h>
 
 #define TWO_PI 6.283185307179586
+/* NATIVE direction angles are 2 pi u - pi in [-pi, pi) (wos_walk.cuh dir_angle) */
+#define PI 3.141592653589793
 #define INV_TWO_PI (1.0 / TWO_PI)
 #define INV_FOUR_PI (1.0 / (4.0 * 3.141592653589793))
 #define PI 3.141592653589793
@@ -574,7 +576,7 @@ static void walk_screened_one(const wos_problem* pb, const double* x0, uint64_t 
     }
     const double z = 2.0 * uz - 1.0; /* walker._sphere_dirs_3d */
     const double s = sqrt(fmax(0.0, 1.0 - z * z));
-    const double phi = TWO_PI * uphi;
+    const double phi = TWO_PI * uphi - (native ? PI : 0.0);
     const double dir[3] = {s * cos(phi), s * sin(phi), z};
     const int vol = ue >= surf;
     const double rad = vol ? d * invert_bisect(qq, ur) : d;
@@ -714,15 +716,15 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
     }
     double dir[3];
     if (dim == 2 && !has_src) {
-      double th = TWO_PI * u23(u[sub]);
+      double th = TWO_PI * u23(u[sub]) - PI;
       dir[0] = cos(th);
       dir[1] = sin(th);
     } else if (dim == 2) {
-      double th = TWO_PI * u23(u[0]);
+      double th = TWO_PI * u23(u[0]) - PI;
       dir[0] = cos(th);
       dir[1] = sin(th);
       if (has_src) {
-        double phi = TWO_PI * u23(u[1]);
+        double phi = TWO_PI * u23(u[1]) - PI;
         double r = d * sqrt(u23(u[2]) * u23(u[3]));
         double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
         acc -= (d * d * 0.25) * source(pb, g);
@@ -730,7 +732,7 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
     } else if (!has_src) {
       double z = 2.0 * u23(u[2 * sub]) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
-      double phi = TWO_PI * u23(u[2 * sub + 1]);
+      double phi = TWO_PI * u23(u[2 * sub + 1]) - PI;
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;
@@ -748,13 +750,13 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       v[6] = ((double)b6 + 0.5) * (1.0 / 4096.0);
       double z = 2.0 * v[0] - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
-      double phi = TWO_PI * v[1];
+      double phi = TWO_PI * v[1] - PI;
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;
       double vz = 2.0 * v[2] - 1.0;
       double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
-      double vphi = TWO_PI * v[3];
+      double vphi = TWO_PI * v[3] - PI;
       double r = d * med3(v[4], v[5], v[6]);
       double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
                      x[2] + sgn * r * vz};

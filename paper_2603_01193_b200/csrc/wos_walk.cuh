@@ -70,6 +70,11 @@ constexpr double kTwoPi = 6.283185307179586;
 constexpr double kInvTwoPi = 1.0 / 6.283185307179586;
 constexpr double kInvFourPi = 1.0 / (4.0 * 3.141592653589793);
 constexpr float kTwoPiF = 6.283185307179586f;
+constexpr float kThreePiF = 9.42477796076938f;
+// NATIVE direction angle 2 pi u - pi in [-pi, pi) from a 23-bit field f = 1 + u: the
+// range on which MUFU.SIN/COS keep their 2^-21.4 bound (2^-20.4 on [0, 2 pi);
+// tests/test_gpu_fastmath.py). Uniform in angle either way.
+__device__ __forceinline__ float dir_angle(float f) { return fmaf(f, kTwoPiF, -kThreePiF); }
 constexpr float kPiF = 3.141592653589793f;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -1148,7 +1153,7 @@ struct Walker {
     const float z = f2x(A.y) - 3.0f;
     const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
     float sph, cph;
-    __sincosf(fmaf(f12(A.z), kTwoPiF, -kTwoPiF), &sph, &cph);
+    __sincosf(dir_angle(f12(A.z)), &sph, &cph);
     const bool vol = (f12(A.x) - 1.0f) >= surf;
     float rad = d;
     if (vol) rad = d * invert_radial_f32(qf, (f12(A.w) - 1.0f) + 0x1p-24f);
@@ -1286,7 +1291,7 @@ struct Walker {
   // source-free NATIVE jumps from their words of the block (kPerBlock above)
   __device__ static __forceinline__ void move_native_2d(Lane& l, float d, uint32_t w) {
     float sth, cth;
-    __sincosf(fmaf(f12(w), kTwoPiF, -kTwoPiF), &sth, &cth);
+    __sincosf(dir_angle(f12(w)), &sth, &cth);
     const float sd = l.sgn * d;
     l.x[0] = fmaf(sd, cth, l.x[0]);
     l.x[1] = fmaf(sd, sth, l.x[1]);
@@ -1295,7 +1300,7 @@ struct Walker {
     const float z = f2x(wz) - 3.0f;
     const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
     float sph, cph;
-    __sincosf(fmaf(f12(wphi), kTwoPiF, -kTwoPiF), &sph, &cph);
+    __sincosf(dir_angle(f12(wphi)), &sph, &cph);
     const float sd = l.sgn * d, sdxy = sd * sxy;
     l.x[0] = fmaf(sdxy, cph, l.x[0]);
     l.x[1] = fmaf(sdxy, sph, l.x[1]);
@@ -1316,10 +1321,10 @@ struct Walker {
       move_native_2d(l, d, k == 0 ? A.x : k == 1 ? A.y : k == 2 ? A.z : A.w);
     } else if constexpr (DIM == 2) {
       float sth, cth;
-      __sincosf(fmaf(f12(A.x), kTwoPiF, -kTwoPiF), &sth, &cth);
+      __sincosf(dir_angle(f12(A.x)), &sth, &cth);
       {
         float sph, cph;
-        __sincosf(fmaf(f12(A.y), kTwoPiF, -kTwoPiF), &sph, &cph);
+        __sincosf(dir_angle(f12(A.y)), &sph, &cph);
         const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
         const float sr = l.sgn * r;
         const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
@@ -1337,11 +1342,11 @@ struct Walker {
       const float z = f2x(A.x) - 3.0f;
       const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
-      __sincosf(fmaf(u[1], kTwoPiF, -kTwoPiF), &sph, &cph);
+      __sincosf(dir_angle(u[1]), &sph, &cph);
       const float vz = f2x(A.z) - 3.0f;
       const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
       float vsp, vcp;
-      __sincosf(fmaf(u[3], kTwoPiF, -kTwoPiF), &vsp, &vcp);
+      __sincosf(dir_angle(u[3]), &vsp, &vcp);
       // Beta(2,2) radius fraction = median of three uniforms; r = d * (med - 1)
       const float med = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6]));
       const float sr = l.sgn * fmaf(d, med, -d);

@@ -16,15 +16,18 @@ pytestmark = pytest.mark.gpu
 
 # argument ranges the NATIVE kernels use
 RANGES = {
-    # direction angles: fmaf(f12(w), 2 pi, -2 pi) with f12 in [1, 2)
-    "direction angle [0, 2pi)": (0.0, 2.0 * math.pi),
+    # direction angles: dir_angle(f12(w)) = fmaf(f, 2 pi, -3 pi) with f in [1, 2)
+    "direction angle [-pi, pi)": (-math.pi, math.pi),
+    # the arc-length boundary's 2 pi s / 4, s in [0, 4) (once per walk)
+    "arc-length angle [0, 2pi)": (0.0, 2.0 * math.pi),
     # sine sources on the unit box: k pi y for y in [0, 1] (monomial / Chebyshev rows)
     "sine source [0, pi]": (0.0, math.pi),
     # delta-tracking family coefficients (arguments below ~25 rad)
     "screened family [-25, 25]": (-25.0, 25.0),
 }
 SIN_BOUND = {  # max |error| (absolute)
-    "direction angle [0, 2pi)": 2.0 ** -20,
+    "direction angle [-pi, pi)": 2.0 ** -21,
+    "arc-length angle [0, 2pi)": 2.0 ** -20,
     "sine source [0, pi]": 2.0 ** -21,
     "screened family [-25, 25]": 2.0 ** -18,
 }
