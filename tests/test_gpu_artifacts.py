@@ -95,3 +95,19 @@ def test_bench_replay_matches_reference_cli(gpu, tmp_path):
             assert abs(float(r[j]) - float(q[j])) <= 1e-10 * max(1e-12, abs(float(q[j])))
     s = json.loads(summ.read_text())
     assert s["header"] == ref_stamp and s["replicas"] == cfg["replicas"]
+
+
+def test_solve_bytes_invariant_to_workers(gpu, tmp_path):
+    """The reference's criterion 12 (test_acceptance.py:355-391): CSV bytes after the run
+    stamp are identical for workers 1/4/8 (here: GPUs, clamped to the devices present)
+    and the stamps differ only in their workers field."""
+    from paper_2603_01193_b200 import artifacts
+
+    cfg = json.loads(str(Z["solve_disk_grid__config"]))
+    bodies, stamps = {}, {}
+    for workers in (1, 4, 8):
+        out = tmp_path / f"w{workers}.csv"
+        artifacts.solve(dict(cfg, workers=workers, output=str(out)))
+        stamps[workers], bodies[workers] = out.read_bytes().split(b"\n", 1)
+    assert bodies[1] == bodies[4] == bodies[8]
+    assert len({h.replace(b"workers=%d" % w, b"workers=*") for w, h in stamps.items()}) == 1
