@@ -644,6 +644,16 @@ struct Walker {
         return (s[0] * s[1]) * q;
       } else {
         auto A = [&](int p, int qd, int r) { return a[(p * K + qd) * K + r]; };
+#ifndef WOS_ESTRIN_HEADS
+#define WOS_ESTRIN_HEADS 1
+#endif
+        // K = 3 innermost chains as c2 A1 + c2^2 A2 (FMUL2 + FFMA2, coefficient pairs as
+        // uniform operands) then + A0 (FADD2): no uniform->vector moves for the heads
+        constexpr bool kEstrin = WOS_ESTRIN_HEADS && K == 3;
+        const float c2sq = c[2] * c[2];
+        auto chain2 = [&](float2 a0, float2 a1, float2 a2) {
+          return __fadd2_rn(__ffma2_rn(f2(c[2], c[2]), a1, __fmul2_rn(f2(c2sq, c2sq), a2)), a0);
+        };
         float mp[K];  // mp[p] = sum_qd c1^qd sum_r a[p][qd][r] c2^r
         // pairs of p: both chains of every level share the broadcast c2 / c1
 #pragma unroll
@@ -651,10 +661,15 @@ struct Walker {
           float2 hq[K];
 #pragma unroll
           for (int qd = 0; qd < K; ++qd) {
-            float2 h = f2(A(p, qd, K - 1), A(p + 1, qd, K - 1));
+            if constexpr (kEstrin) {
+              hq[qd] = chain2(f2(A(p, qd, 0), A(p + 1, qd, 0)), f2(A(p, qd, 1), A(p + 1, qd, 1)),
+                              f2(A(p, qd, 2), A(p + 1, qd, 2)));
+            } else {
+              float2 h = f2(A(p, qd, K - 1), A(p + 1, qd, K - 1));
 #pragma unroll
-            for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p + 1, qd, r)));
-            hq[qd] = h;
+              for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p + 1, qd, r)));
+              hq[qd] = h;
+            }
           }
           float2 m = hq[K - 1];
 #pragma unroll
@@ -667,13 +682,21 @@ struct Walker {
           float hq[K];
 #pragma unroll
           for (int qd = 0; qd + 1 < K; qd += 2) {
-            float2 h = f2(A(p, qd, K - 1), A(p, qd + 1, K - 1));
+            float2 h;
+            if constexpr (kEstrin) {
+              h = chain2(f2(A(p, qd, 0), A(p, qd + 1, 0)), f2(A(p, qd, 1), A(p, qd + 1, 1)),
+                         f2(A(p, qd, 2), A(p, qd + 1, 2)));
+            } else {
+              h = f2(A(p, qd, K - 1), A(p, qd + 1, K - 1));
 #pragma unroll
-            for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p, qd + 1, r)));
+              for (int r = K - 2; r >= 0; --r) h = __ffma2_rn(h, f2(c[2], c[2]), f2(A(p, qd, r), A(p, qd + 1, r)));
+            }
             hq[qd] = h.x;
             hq[qd + 1] = h.y;
           }
-          {
+          if constexpr (kEstrin) {
+            hq[K - 1] = __fadd_rn(fmaf(c[2], A(p, K - 1, 1), __fmul_rn(c2sq, A(p, K - 1, 2))), A(p, K - 1, 0));
+          } else {
             float h = A(p, K - 1, K - 1);
 #pragma unroll
             for (int r = K - 2; r >= 0; --r) h = fmaf(h, c[2], A(p, K - 1, r));
