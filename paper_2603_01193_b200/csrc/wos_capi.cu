@@ -103,6 +103,7 @@ struct wos_problem_set {
   float* d_polar_f = nullptr;             //        the same, fp32
   size_t bytes_polar_d = 0, bytes_polar_f = 0;
   std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
+  std::vector<float> h_row_n_scaled;      // ... with the box in X = pi x (scaled-coordinate kernels)
   double scr_sprime_max = -1.0;           // SRC_SCR_CONST: largest s' of the set (majorant check)
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
@@ -962,6 +963,12 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     for (int k = 0; k < nb; ++k) rn[s->bnd_off + k] = (float)bd[k];
   }
   s->h_row_n.assign(tn.begin(), tn.begin() + stride);
+  s->h_row_n_scaled = s->h_row_n;
+  if (s->dom_kind == WOS_DOM_BOX)  // centre and half extent times pi, from the fp64 row
+    for (int k = 0; k < s->dim; ++k) {
+      s->h_row_n_scaled[8 + k] = (float)(M_PI * 0.5 * (td[k] + td[4 + k]));
+      s->h_row_n_scaled[12 + k] = (float)(M_PI * 0.5 * (td[4 + k] - td[k]));
+    }
   s->h_nkey1 = hd[0].nkey1;
   std::vector<float> tf(td.size());
   for (size_t k = 0; k < td.size(); ++k) tf[k] = (float)td[k];
@@ -1252,6 +1259,7 @@ static size_t smem_bytes(size_t stage, size_t elem) {
 static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
                        KArgs a, cudaStream_t st) {
   const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS);
+  bool scaled = false;  // the walk runs in X = pi x (see below)
   if (!k.fn)
     return fail(WOS_ERR_UNSUPPORTED, "no kernel for dim %d domain %d source %d mode %d", s->dim,
                 s->dom_kind, s->src_kind, cfg->mode);
@@ -1279,7 +1287,12 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     if (k.one) {
       // instance row and Philox4x32 round keys ride in the kernel parameters
       a.stage_bytes = 0;
-      memcpy(a.cp, s->h_row_n.data(), sizeof(float) * s->stride);
+      // scaled-coordinate kernels (wos_walk.cuh Walker::kScaled: single-instance,
+      // constant boundary, box, monomial sine source, estimate sink) walk in X = pi x
+      scaled = WOS_SCALED_COORDS && a.sink == SINK_ESTIMATE && s->bnd_kind == WOS_BND_CONST &&
+               s->dom_kind == WOS_DOM_BOX && s->src_kind == WOS_SRC_SINE &&
+               (s->sk_native == 3 || s->sk_native == 4);
+      memcpy(a.cp, (scaled ? s->h_row_n_scaled : s->h_row_n).data(), sizeof(float) * s->stride);
       a.bnd_c = s->h_row_n[s->bnd_off];
       const uint32_t k0 = (uint32_t)cfg->rng_seed;
       const uint32_t k1 = (uint32_t)(cfg->rng_seed >> 32) ^ s->h_nkey1;
@@ -1312,7 +1325,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.refill_min = c->refill_min;
   a.refill_min_deferred = c->refill_min_deferred;
   a.eps = cfg->eps;
-  a.eps_f = (float)cfg->eps;
+  a.eps_f = (float)(scaled ? M_PI * cfg->eps : cfg->eps);
   a.max_steps = (int32_t)std::min<int64_t>(cfg->max_steps, 0x7fffffff);
   a.antithetic = cfg->antithetic ? 1 : 0;
   a.seed = cfg->rng_seed;

@@ -22,6 +22,11 @@ enum : int { SINK_ROWS = 0, SINK_ESTIMATE = 1 };
 
 constexpr int kBlock = 256;       // threads per CTA (8 warps)
 constexpr int kWarps = kBlock / 32;
+// single-instance constant-boundary box kernels with a monomial sine source walk in
+// X = pi x (wos_walk.cuh Walker::kScaled; the host scales box and eps to match)
+#ifndef WOS_SCALED_COORDS
+#define WOS_SCALED_COORDS 1
+#endif
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units

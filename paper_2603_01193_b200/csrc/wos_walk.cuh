@@ -611,13 +611,27 @@ struct Walker {
   // series is s_x s_y (s_z) Q(c_x, c_y (, c_z)) with Q a polynomial whose monomial
   // coefficients the host precomputes (wos_capi.cu sine_monomial); nested Horner.
   static constexpr bool kMonomial = S::NATIVE && (S::SK == 3 || S::SK == 4);
+  // Scaled coordinates (single-instance constant-boundary box kernels with a monomial
+  // sine source): the walk runs in X = pi x (the host scales the box and eps), so the
+  // source terms sin(k pi x) take MUFU arguments without the pi multiply (three fewer
+  // FMUL per 3D jump); the Green weight carries 1/pi^2. The walk value acc + g needs no
+  // exit point, so nothing is scaled back. wos_capi.cu launch_walk mirrors this test.
+  static constexpr bool kScaled =
+      WOS_SCALED_COORDS && kMonomial && ONE && S::BC && S::DOM == DOM_BOX && S::SINK == SINK_ESTIMATE;
+  static constexpr float kInvPi2F = 0.10132118364233778f;  // 1 / pi^2
+  // a query point's coordinate in the walk's units (already-converted Real values pass)
+  __device__ static __forceinline__ Real start_coord(double x) {
+    if constexpr (kScaled) return (Real)(kPi * x);
+    else return (Real)x;
+  }
+  __device__ static __forceinline__ Real start_coord(float x) { return x; }
 
   template <int K>
   __device__ static __forceinline__ Real sine_eval(const Real* __restrict__ a, const Real* y) {
     if constexpr (kMonomial) {
       float s[DIM], c[DIM];
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) __sincosf(kPiF * y[i], &s[i], &c[i]);
+      for (int i = 0; i < DIM; ++i) __sincosf(kScaled ? y[i] : kPiF * y[i], &s[i], &c[i]);
       // Independent Horner chains run two at a time as packed FFMA2 (fma.rn.f32x2,
       // elementwise fma.rn): the same operations in the same order as scalar fmaf, so
       // bit-identical to it, at half the issue slots.
@@ -1351,7 +1365,7 @@ struct Walker {
         const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
         const float sr = l.sgn * r;
         const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
-        l.acc = fmaf(-0.25f * d * d, source(l, a, g), l.acc);
+        l.acc = fmaf(-(kScaled ? 0.25f * kInvPi2F : 0.25f) * d * d, source(l, a, g), l.acc);
       }
       l.x[0] = fmaf(sd, cth, l.x[0]);
       l.x[1] = fmaf(sd, sth, l.x[1]);
@@ -1378,7 +1392,7 @@ struct Walker {
       const float2 xy = make_float2(l.x[0], l.x[1]);
       const float2 gxy = __ffma2_rn(make_float2(srv, srv), make_float2(vcp, vsp), xy);
       const float g[3] = {gxy.x, gxy.y, fmaf(sr, vz, l.x[2])};
-      l.acc = fmaf(-(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
+      l.acc = fmaf(-(d * d) * (kScaled ? (1.0f / 6.0f) * kInvPi2F : 1.0f / 6.0f), source(l, a, g), l.acc);
       const float sdxy = sd * sxy;
       const float2 nxy = __ffma2_rn(make_float2(sdxy, sdxy), make_float2(cph, sph), xy);
       l.x[0] = nxy.x;
@@ -1404,7 +1418,7 @@ struct Walker {
                                                const KArgs& a, const X* x0, int inst,
                                                uint64_t pid, uint64_t tid, double sgn) {
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) l.x[i] = (Real)x0[i];
+    for (int i = 0; i < DIM; ++i) l.x[i] = start_coord(x0[i]);
     l.acc = Real(0);
     l.sgn = (Real)sgn;
     l.step = 0;
@@ -1791,7 +1805,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               cu_jend = min(L, cu_j0 + kChunk);
             }
 #pragma unroll
-            for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
+            for (int i = 0; i < DIM; ++i) cu_x[i] = W::start_coord(a.points[(size_t)p * DIM + i]);
             cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
             cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
             room = IU;
@@ -1870,7 +1884,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                 cu_jend = min(L, cu_j0 + kChunk);
               }
 #pragma unroll
-              for (int i = 0; i < DIM; ++i) cu_x[i] = (Real)a.points[(size_t)p * DIM + i];
+              for (int i = 0; i < DIM; ++i) cu_x[i] = W::start_coord(a.points[(size_t)p * DIM + i]);
               cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
               cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
               if constexpr (kJumpFirst && S::ONE) cu_d = W::dist_at(l, a, cu_x);

@@ -202,3 +202,23 @@ def test_long_ensembles_use_chunked_reduction(gpu, mode):
         np.testing.assert_allclose(mean, om, rtol=2e-3, atol=2e-6)
         np.testing.assert_allclose(m2, om2, rtol=2e-2)
     assert np.all(n == L)
+
+
+@pytest.mark.parametrize("cfg", [0, 2, 4])
+def test_native_estimate_matches_native_oracle(gpu, cfg):
+    """The estimate kernels themselves (cfg0 / cfg4: the single-instance constant-boundary
+    variants that walk in scaled coordinates X = pi x; cfg2: multi-instance, deferred
+    recording) against the oracle's fp64 estimate of the same native walks."""
+    from paper_2603_01193_b200 import configs, estimate_arrays
+
+    w = _subset(configs.build(cfg), 96, seed=20 + cfg)
+    L = 64
+    mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, point_ids=w.point_ids,
+                                  inst_index=w.inst_index if len(w.problems) > 1 else None, traj_start=7)
+    mo, m2o, _ = O.estimate(w.problems, w.points, L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
+                            max_steps=w.cfg.max_steps, point_ids=w.point_ids,
+                            inst_index=w.inst_index if len(w.problems) > 1 else None, traj_start=7, native=True)
+    rms = float(np.sqrt(np.mean(m2o / L + mo**2)))  # rms walk value
+    close = np.abs(mean - mo) <= 1e-4 * rms
+    assert close.mean() >= 0.97, f"{close.mean():.3f} of points within 1e-4 rms"
+    assert np.max(np.abs(mean - mo)) <= 1e-2 * rms
