@@ -847,8 +847,26 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       segn.push_back(make_float4((float)g.lo[0], (float)g.lo[1], (float)g.ih[0], (float)g.ih[1]));
       grid_fix.push_back({segn.size(), pcells.size(), pidx.size()});
       segn.push_back(make_float4(bits_f32(g.G), 0.f, 0.f, 0.f));  // offsets patched below
+#if WOS_GRID_INLINE
+      // one 16-byte record per cell: {overflow offset, count, pairs 0-1, pairs 2-3} as
+      // uint16 pair indices; pairs 4.. of a cell go to the polygon's overflow list
+      if (g.G > 0) {
+        const size_t pbase = pidx.size();
+        for (size_t c = 0; c + 1 < g.cells.size(); ++c) {
+          const uint32_t b = g.cells[c], e = g.cells[c + 1], n = e - b;
+          uint32_t in[4] = {0, 0, 0, 0};
+          for (uint32_t k = 0; k < n && k < 4; ++k) in[k] = g.idx[b + k];
+          pcells.push_back((uint32_t)(pidx.size() - pbase));
+          pcells.push_back(n);
+          pcells.push_back(in[0] | (in[1] << 16));
+          pcells.push_back(in[2] | (in[3] << 16));
+          for (uint32_t k = 4; k < n; ++k) pidx.push_back(g.idx[b + k]);
+        }
+      }
+#else
       pcells.insert(pcells.end(), g.cells.begin(), g.cells.end());
       pidx.insert(pidx.end(), g.idx.begin(), g.idx.end());
+#endif
       hd[i].rec_off = (int)segn.size();
       if (nv & 1) {
         vx.push_back((float)V[0]);

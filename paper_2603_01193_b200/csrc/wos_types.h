@@ -27,6 +27,11 @@ constexpr int kWarps = kBlock / 32;
 #ifndef WOS_SCALED_COORDS
 #define WOS_SCALED_COORDS 1
 #endif
+// polygon candidate grids: 16-byte cell records with up to four pair indices inline
+// (one dependent load fewer per query; wos_capi.cu build, wos_walk.cuh poly_grid_scan)
+#ifndef WOS_GRID_INLINE
+#define WOS_GRID_INLINE 1
+#endif
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units

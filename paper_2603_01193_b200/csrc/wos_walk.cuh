@@ -329,13 +329,23 @@ struct Walker {
                                                          float px, float py, int* bi_out) {
     const int cx = min(max((int)((px - H0.x) * H0.z), 0), G - 1);
     const int cy = min(max((int)((py - H0.y) * H0.w), 0), G - 1);
-    const uint32_t* cell = gw + cells_off + cy * G + cx;
-    const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
     const uint16_t* idx = reinterpret_cast<const uint16_t*>(gw) + idx_off;
     float best = 3.0e38f;
     int bi = 0;
+#if WOS_GRID_INLINE
+    // the cell record carries its first four pair indices: most queries (near the
+    // boundary, where the walks spend their steps) need no index load of their own
+    const uint4 C = __ldg(reinterpret_cast<const uint4*>(gw + cells_off) + cy * G + cx);
+    const uint32_t e = C.y;
+    for (uint32_t k = 0; k < e; ++k) {
+      const uint32_t wd = k < 2 ? C.z : C.w;
+      const int j = k < 4 ? (int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)) : (int)__ldg(idx + C.x + (k - 4));
+#else
+    const uint32_t* cell = gw + cells_off + cy * G + cx;
+    const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
     for (uint32_t k = b; k < e; ++k) {
       const int j = __ldg(idx + k);
+#endif
       const float2 d = pair_d2(__ldg(R + 2 * j), __ldg(R + 2 * j + 1), __ldg(R + 2 * j + 2), px, py);
       if (d.x < best) {
         best = d.x;
