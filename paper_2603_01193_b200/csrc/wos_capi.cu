@@ -412,6 +412,8 @@ static double seg_box_dist(double ax, double ay, double bx, double by, double x0
 // zero-length segment at vertex 0). The lists are refined down a quadtree: a child
 // cell's candidates are a subset of its parent's (its U is no larger, its box
 // distances no smaller), so each level only tests the parent's list.
+static int np_pairs(int nv) { return (nv + 1) / 2; }  // segment pairs of an nv-gon
+
 static void build_poly_grid(const double* V, int nv, PolyGrid* g) {
   const int np = nv + (nv & 1);
   g->G = 0;
@@ -848,21 +850,48 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       grid_fix.push_back({segn.size(), pcells.size(), pidx.size()});
       segn.push_back(make_float4(bits_f32(g.G), 0.f, 0.f, 0.f));  // offsets patched below
 #if WOS_GRID_INLINE
-      // one 16-byte record per cell: {overflow offset, count, pairs 0-1, pairs 2-3} as
-      // uint16 pair indices; pairs 4.. of a cell go to the polygon's overflow list
+      // one 16-byte record per cell. Byte format (every pair index < 256, counts and the
+      // overflow list < 65536): {count | overflow offset << 16, pairs 0-11 as bytes};
+      // else the uint16 format {overflow offset, count, pairs 0-1, pairs 2-3}. The rest
+      // of a cell's pairs go to the polygon's overflow list (bytes packed two per
+      // uint16 slot in the byte format). Header record 1's w says which (1 = bytes).
+      bool bytes8 = WOS_GRID_BYTES && g.G > 0 && (np_pairs(nv) <= 256);
       if (g.G > 0) {
+        size_t over = 0;
+        uint32_t maxn = 0;
+        for (size_t c = 0; c + 1 < g.cells.size(); ++c) {
+          const uint32_t n = g.cells[c + 1] - g.cells[c];
+          maxn = std::max(maxn, n);
+          over += n > 12 ? n - 12 : 0;
+        }
+        bytes8 = bytes8 && maxn < 65536 && over < 65536;
         const size_t pbase = pidx.size();
+        std::vector<uint8_t> ov8;
         for (size_t c = 0; c + 1 < g.cells.size(); ++c) {
           const uint32_t b = g.cells[c], e = g.cells[c + 1], n = e - b;
-          uint32_t in[4] = {0, 0, 0, 0};
-          for (uint32_t k = 0; k < n && k < 4; ++k) in[k] = g.idx[b + k];
-          pcells.push_back((uint32_t)(pidx.size() - pbase));
-          pcells.push_back(n);
-          pcells.push_back(in[0] | (in[1] << 16));
-          pcells.push_back(in[2] | (in[3] << 16));
-          for (uint32_t k = 4; k < n; ++k) pidx.push_back(g.idx[b + k]);
+          if (bytes8) {
+            uint32_t w[3] = {0, 0, 0};
+            for (uint32_t k = 0; k < n && k < 12; ++k) w[k >> 2] |= (uint32_t)g.idx[b + k] << (8 * (k & 3));
+            pcells.push_back(n | ((uint32_t)ov8.size() << 16));
+            pcells.push_back(w[0]);
+            pcells.push_back(w[1]);
+            pcells.push_back(w[2]);
+            for (uint32_t k = 12; k < n; ++k) ov8.push_back((uint8_t)g.idx[b + k]);
+          } else {
+            uint32_t in[4] = {0, 0, 0, 0};
+            for (uint32_t k = 0; k < n && k < 4; ++k) in[k] = g.idx[b + k];
+            pcells.push_back((uint32_t)(pidx.size() - pbase));
+            pcells.push_back(n);
+            pcells.push_back(in[0] | (in[1] << 16));
+            pcells.push_back(in[2] | (in[3] << 16));
+            for (uint32_t k = 4; k < n; ++k) pidx.push_back(g.idx[b + k]);
+          }
         }
+        if (bytes8)
+          for (size_t k = 0; k < ov8.size(); k += 2)
+            pidx.push_back((uint16_t)(ov8[k] | ((k + 1 < ov8.size() ? ov8[k + 1] : 0) << 8)));
       }
+      segn.back().w = bits_f32(bytes8 ? 1 : 0);
 #else
       pcells.insert(pcells.end(), g.cells.begin(), g.cells.end());
       pidx.insert(pidx.end(), g.idx.begin(), g.idx.end());

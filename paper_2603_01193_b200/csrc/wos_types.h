@@ -32,6 +32,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef WOS_GRID_INLINE
 #define WOS_GRID_INLINE 1
 #endif
+#ifndef WOS_GRID_BYTES  // byte pair indices (12 inline) when a polygon has <= 256 pairs
+#define WOS_GRID_BYTES 1
+#endif
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units

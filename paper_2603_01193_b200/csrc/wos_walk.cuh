@@ -325,7 +325,7 @@ struct Walker {
   // candidate-grid query (wos_capi.cu build_poly_grid): the cell's ascending list of
   // segment pairs; records the exact first nearest segment
   __device__ static __forceinline__ float poly_grid_scan(const float4* __restrict__ R, float4 H0, int G, int cells_off,
-                                                         int idx_off, const uint32_t* __restrict__ gw,
+                                                         int idx_off, bool bytes8, const uint32_t* __restrict__ gw,
                                                          float px, float py, int* bi_out) {
     const int cx = min(max((int)((px - H0.x) * H0.z), 0), G - 1);
     const int cy = min(max((int)((py - H0.y) * H0.w), 0), G - 1);
@@ -333,13 +333,21 @@ struct Walker {
     float best = 3.0e38f;
     int bi = 0;
 #if WOS_GRID_INLINE
-    // the cell record carries its first four pair indices: most queries (near the
-    // boundary, where the walks spend their steps) need no index load of their own
+    // the cell record carries its first pair indices (12 as bytes, or 4 as uint16):
+    // most queries (near the boundary, where the walks spend their steps) need no
+    // index load of their own
     const uint4 C = __ldg(reinterpret_cast<const uint4*>(gw + cells_off) + cy * G + cx);
-    const uint32_t e = C.y;
+    const uint32_t e = bytes8 ? (C.x & 0xFFFFu) : C.y;
+    const uint8_t* idx8 = reinterpret_cast<const uint8_t*>(idx);
     for (uint32_t k = 0; k < e; ++k) {
-      const uint32_t wd = k < 2 ? C.z : C.w;
-      const int j = k < 4 ? (int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)) : (int)__ldg(idx + C.x + (k - 4));
+      int j;
+      if (bytes8) {
+        const uint32_t wd = k < 4 ? C.y : (k < 8 ? C.z : C.w);
+        j = k < 12 ? (int)((wd >> (8 * (k & 3))) & 0xFFu) : (int)__ldg(idx8 + (C.x >> 16) + (k - 12));
+      } else {
+        const uint32_t wd = k < 2 ? C.z : C.w;
+        j = k < 4 ? (int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)) : (int)__ldg(idx + C.x + (k - 4));
+      }
 #else
     const uint32_t* cell = gw + cells_off + cy * G + cx;
     const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
@@ -368,7 +376,7 @@ struct Walker {
       const float4 H1 = R[-1];
       const int G = __float_as_int(H1.x);
       if (G > 0) {  // (sets with grids are never staged: R is global)
-        best = poly_grid_scan(R, R[-2], G, __float_as_int(H1.y), __float_as_int(H1.z),
+        best = poly_grid_scan(R, R[-2], G, __float_as_int(H1.y), __float_as_int(H1.z), __float_as_int(H1.w) != 0,
                               reinterpret_cast<const uint32_t*>(a.nodes), l.x[0], l.x[1], &bi);
       } else {  // R: shared memory when staged, else global
         best = poly_scan(R, l.n_seg, l.x[0], l.x[1], &bi);
