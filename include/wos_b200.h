@@ -15,6 +15,14 @@
  *   estimator.PointEstimate.from_values (estimator.py:106-110) fused per-point reduce
  *   rng.philox4x64                  (rng.py:57-82)          wos_philox4x64
  *   geometry.*.contains             (geometry.py:190-194)   wos_check_interior
+ *   estimator.EstimateCache.update / cache_update (estimator.py:217-244,338-341)
+ *                                                           wos_cache_fold
+ *   surrogate.train label epoch     (surrogate.py:288-298)  wos_estimate_fold
+ *
+ * Entry points without a reference counterpart: wos_philox4x32 (the NATIVE stream's
+ * generator, for KATs), wos_set_tuning / wos_set_refill_deferred (launch tuning; results
+ * are bitwise independent of it), wos_probe_peaks (roofline denominators) and
+ * wos_fastmath_probe (the fast-math error bound).
  *
  * Conventions (kept from the reference):
  *   - The reference solves  Laplacian(u) = f,  u = g on the boundary, and SUBTRACTS
