@@ -1856,8 +1856,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   } else
   while (true) {
     const int n_idle = __popc(idle);
-    // (delta tracking: a step costs far more than recording, so the plain threshold)
-    if (n_idle >= ((defer && !W::kScr) ? a.refill_min_deferred : kAmort ? 1 : a.refill_min) || n_idle == 32) {
+    // (delta tracking: a step costs far more than recording, so the plain threshold;
+    // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
+    if (n_idle >= ((defer && !W::kScr) ? a.refill_min_deferred + (kAmort ? 4 : 0) : kAmort ? 1 : a.refill_min) ||
+        n_idle == 32) {
       flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
