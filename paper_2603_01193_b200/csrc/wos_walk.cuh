@@ -10,7 +10,10 @@
 //   * each lane carries one walk in registers (position, Green accumulator,
 //     step, RNG counter words); when lanes finish (eps-shell hit or max_steps)
 //     they are refilled with the next items of the warp's stream (lane refill),
-//     so lanes do not idle while work remains;
+//     so lanes do not idle while work remains; closed-form domains run the loop
+//     jump-first (jump with the carried distance, query, finish at once);
+//   * a finished walk with a non-constant boundary term is recorded at the next
+//     refill together with the other finished lanes (deferred recording);
 //   * ESTIMATE sink: walk values go to a per-warp shared-memory ring indexed by
 //     the item's stream position; a unit (whole points for L <= 128, else a
 //     128-walk chunk of one point) is reduced as soon as all its walks are done,
@@ -30,9 +33,14 @@
 //   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
 //   and ONE Philox4x32-10 block per jump (counter (2*step, pid, tid, hi-words));
 //   the 3D source jump needs 7 uniforms and takes them as bit fields of the
-//   block's 128 bits (native_uniforms7 below; oracle/wos_oracle.c restates it).
-//   Single-instance NATIVE launches (ONE) read the instance row and the Philox
-//   round keys from the kernel parameters (constant bank), not shared memory.
+//   block's 128 bits (native_uniforms7 below; oracle/wos_oracle.c restates it);
+//   source-free jumps share a block between 4 (2D) / 2 (3D) consecutive jumps
+//   (kPerBlock; phase-locked amortised rounds on closed-form domains). Direction
+//   angles are 2 pi u - pi (MUFU's accurate range). Single-instance NATIVE launches
+//   (ONE) read the instance row and the Philox round keys from the kernel
+//   parameters, kept in uniform registers; those with a constant boundary are
+//   built without the deferral code (Spec BC), and box + monomial-sine ones walk
+//   in scaled coordinates X = pi x (kScaled).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
