@@ -80,3 +80,39 @@ def test_missing_library_raises(tmp_path):
 
     with pytest.raises(_lib.WosUnavailableError):
         _lib.load_library(str(tmp_path / "nope.so"))
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The ctypes mirrors of wos_problem / wos_walk_config (and the INTEGRATION.md stub,
+    which uses the same fields) have the C header's size and field offsets."""
+    import ctypes
+    import os
+    import shutil
+    import subprocess
+
+    from paper_2603_01193_b200 import _lib
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:  # pragma: no cover - the image has gcc
+        import pytest
+
+        pytest.skip("no C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "layout.c"
+    fields = {"wos_problem": [f for f, _ in _lib.WosProblem._fields_],
+              "wos_walk_config": [f for f, _ in _lib.WosWalkConfig._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "wos_b200.h"', "int main(void) {"]
+    for st, fs in fields.items():
+        lines.append(f'  printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            lines.append(f'  printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines += ["  return 0;", "}"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for st, cls in (("wos_problem", _lib.WosProblem), ("wos_walk_config", _lib.WosWalkConfig)):
+        assert int(got[st]) == ctypes.sizeof(cls), st
+        for f in fields[st]:
+            assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
