@@ -1694,6 +1694,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #define WOS_JUMP_FIRST 1
 #endif
   constexpr bool kJumpFirst = WOS_JUMP_FIRST && (S::DOM == DOM_BALL || S::DOM == DOM_BOX);
+  // Polygons run jump-first in the cached-point refill only: there a unit's start
+  // distance (and nearest segment) is queried once per unit, not per walk
+#ifndef WOS_JUMP_FIRST_POLY
+#define WOS_JUMP_FIRST_POLY 1
+#endif
+  constexpr bool kJumpFirstPoly = WOS_JUMP_FIRST_POLY && S::DOM == DOM_POLY && est;
+  const bool jf = kJumpFirst || (kJumpFirstPoly && fast);
   // Amortised RNG (source-free NATIVE walks on closed-form domains): lanes are refilled
   // only between rounds of kPerBlock jumps, so every live lane enters a round at a step
   // that is a multiple of kPerBlock and one Philox block serves the whole round.
@@ -1754,6 +1761,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // the fast refill's walks all start at the cached point: its distance is queried once
   // per unit (warp-uniform) and an in-shell start is a uniform branch
   Real cu_d = Real(0);
+  int cu_seg = 0;  // polygons: the nearest segment at the cached point
 
   // ======================================================================
   // Eager fast path (ESTIMATE, one point per unit, polygon domains): finished walks
@@ -1916,6 +1924,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
               cu_inst = (!S::ONE && a.inst_index) ? a.inst_index[p] : 0;
               if constexpr (kJumpFirst && S::ONE) cu_d = W::dist_at(l, a, cu_x);
+              if constexpr (kJumpFirstPoly) {
+                // the whole warp queries the unit's start point once (uniform work)
+                typename W::Lane t = l;
+                W::start(t, table, a.hdr, a, cu_x, cu_inst, cu_pid, 0ull, 1.0);
+                cu_d = W::dist(t, a, srec);
+                cu_seg = t.seg_i;
+              }
               if constexpr (S::NATIVE && S::ONE) {
                 // walk j0 + jj has tid = traj_start + j0 + jj (antithetic: jj even; j0 even)
                 const uint64_t tid0 = a.traj_start + cu_j0;
@@ -1955,7 +1970,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               }
               l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
               active = true;
-              if constexpr (kJumpFirst && S::ONE) {
+              if constexpr (kJumpFirstPoly) {
+                l.d = cu_d;
+                l.seg_i = cu_seg;
+                if (cu_d < eps) finish(cu_d);
+              } else if constexpr (kJumpFirst && S::ONE) {
                 l.d = cu_d;
                 if (cu_d < eps) finish(cu_d);
               } else {
@@ -2052,7 +2071,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         if (!live) finish(l.d);
       }
     } else if (active) {
-      if constexpr (kJumpFirst) {
+      if (jf) {
         // the walk is live at l.d >= eps, step < max_steps (tested when l.d was queried)
         if constexpr (W::kScr) {
           if constexpr (S::NATIVE) W::advance_screened_native(l, l.d, a);
