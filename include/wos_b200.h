@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define WOS_ABI_VERSION 3
+#define WOS_ABI_VERSION 4
 
 /* ---- status codes ---------------------------------------------------- */
 typedef enum wos_status {
@@ -247,8 +247,8 @@ int wos_walk_rows_host(wos_context* ctx, const wos_problem_set* set,
  * (mean, m2) with m2 = sum (v - mean)^2 over its n = L (or L/2) samples.
  * Device pointers: points [P, dim] fp64, point_ids [P] int64 or NULL (ids = 0..P-1,
  * estimator.py:165), inst_index [P] int32 or NULL, out_mean/out_m2 [P] fp64, out_total_steps: device uint64 accumulator
- * (added to, not overwritten) or NULL. Exterior start points are detected on the
- * device; query them with wos_context_exterior().                           */
+ * (added to, not overwritten) or NULL. Exterior start points and a watchdog trip
+ * are flagged on the device without a sync; query them with wos_context_status().    */
 int wos_estimate(wos_context* ctx, const wos_problem_set* set, const wos_walk_config* cfg,
                  int64_t n_points, const double* points, const int64_t* point_ids,
                  const int32_t* inst_index, int64_t L, uint64_t traj_start,
@@ -273,6 +273,22 @@ int wos_context_majorant(wos_context* ctx, void* stream, double* out_worst_sigma
 /* Synchronizes `stream` and returns the first exterior point index seen by
  * wos_estimate / wos_estimate_host since the last call (-1 if none), resetting it. */
 int wos_context_exterior(wos_context* ctx, void* stream, int64_t* out_first_exterior);
+
+/* Status of the last walking call on this context (device API error reporting).
+ * Every walking entry point (wos_estimate, wos_walk_rows, wos_estimate_fold and the
+ * *_host variants) clears the context's status block with one stream-ordered memset
+ * before it walks, so the flags read here belong to that call; the device entry
+ * points never synchronize on them. This synchronizes `stream`, returns and clears:
+ *   *out_first_exterior     index of the first exterior start point, -1 if none
+ *                           (estimator.py:156-159 raises ExteriorQueryError for it);
+ *   *out_watchdog           non-zero if the walk kernel hit its iteration limit
+ *                           (results of that call are invalid);
+ *   *out_worst_sigma_prime  largest sigma' above sigma_bar met by a delta-tracking
+ *                           volume event, -1 if none (walker.py:409-413).
+ * Any output pointer may be NULL. The status is per context: calls interleaved on
+ * several streams of one context share it. */
+int wos_context_status(wos_context* ctx, void* stream, int64_t* out_first_exterior,
+                       uint32_t* out_watchdog, double* out_worst_sigma_prime);
 
 /* ---- epoch-averaged estimate cache (estimator.EstimateCache) -----------
  * replaces                                                      by

@@ -36,7 +36,7 @@ WOS_ERR_CUDA = 3
 WOS_ERR_EXTERIOR = 4
 WOS_ERR_NOMEM = 5
 WOS_ERR_MAJORANT = 6
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("WOS_B200_LIB") or os.path.join(_HERE, "libwos_b200.so")
@@ -110,6 +110,7 @@ _SIGNATURES = {
     ),
     "wos_context_exterior": (c_int32, [_P, _P, POINTER(c_int64)]),
     "wos_context_majorant": (c_int32, [_P, _P, POINTER(c_double)]),
+    "wos_context_status": (c_int32, [_P, _P, POINTER(c_int64), POINTER(c_uint32), POINTER(c_double)]),
     "wos_cache_fold": (
         c_int32,
         [_P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P],

@@ -12,6 +12,8 @@
 #include <atomic>
 #include <mutex>
 #include <thread>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "../../include/wos_b200.h"
@@ -49,6 +51,7 @@ static int fail(int code, const char* fmt, ...) {
 // context and problem set
 // ------------------------------------------------------------------------
 constexpr int kCounterRing = 256;
+constexpr size_t kStatusBytes = 32;
 constexpr int kPipeChunks = 4;                 // host pipeline: point chunks per call (at most)
 constexpr int64_t kPipeMinWork = 1ll << 23;    // walks per chunk (at least)
 
@@ -63,10 +66,20 @@ struct wos_context {
   cudaEvent_t ev_start = nullptr;
   unsigned int* d_counters = nullptr;     // work counters, one per launch slot
   std::atomic<unsigned> next_counter{0};
-  unsigned long long* d_exterior = nullptr;  // first exterior point (ULLONG_MAX = none)
+  // Device status block (one 32-byte allocation, reset by ONE stream-ordered memset at
+  // the start of every walking entry point, so a flag always belongs to the call that
+  // raised it; wos_context_status reads it): the first exterior point stored inverted
+  // (atomicMax of ~index, 0 = none), the worst sigma' above sigma_bar (fp64 bits, 0 =
+  // none), the kernel watchdog flag.
+  unsigned long long* d_status = nullptr;
+  unsigned long long* d_exterior = nullptr;  // = d_status + 0
+  unsigned long long* d_majorant = nullptr;  // = d_status + 1
+  unsigned int* d_watchdog = nullptr;        // = (unsigned*)(d_status + 2)
   unsigned long long* d_steps = nullptr;     // total-steps scratch of the *_host variants
-  unsigned int* d_watchdog = nullptr;        // kernel iteration-limit flag
-  unsigned long long* d_majorant = nullptr;  // delta tracking: worst sigma' > sigma_bar (fp64 bits)
+  // per-kernel launch attributes (dynamic shared memory set, occupancy at that size):
+  // computed on the first launch of a (kernel, smem) pair instead of every launch
+  std::unordered_map<const void*, std::pair<size_t, int>> launch_cache;
+  std::mutex launch_mu;
   int64_t host_exterior = -1;
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -150,13 +163,14 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, sizeof(unsigned) * kCounterRing);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_exterior, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_status, kStatusBytes);
+  if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, kStatusBytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_watchdog, sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(c->d_watchdog, 0, sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_majorant, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(c->d_majorant, 0, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(c->d_exterior, 0xff, sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    c->d_exterior = c->d_status;
+    c->d_majorant = c->d_status + 1;
+    c->d_watchdog = reinterpret_cast<unsigned int*>(c->d_status + 2);
+  }
   if (e != cudaSuccess) {
     delete c;
     return fail(WOS_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
@@ -169,10 +183,8 @@ extern "C" void wos_context_destroy(wos_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaFree(c->d_counters);
-  cudaFree(c->d_exterior);
+  cudaFree(c->d_status);
   cudaFree(c->d_steps);
-  cudaFree(c->d_watchdog);
-  cudaFree(c->d_majorant);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1178,7 +1190,7 @@ __global__ void wos_interior_kernel(int64_t n, const double* __restrict__ pts,
       }
       inside = in;
     }
-    if (!inside) atomicMin(first, (unsigned long long)(idx_base + p));
+    if (!inside) atomicMax(first, ~(unsigned long long)(idx_base + p));  // 0 = none
   }
 }
 
@@ -1237,10 +1249,36 @@ extern "C" int wos_context_majorant(wos_context* c, void* stream, double* out) {
 static int read_exterior(wos_context* c, cudaStream_t st, int64_t* out) {
   unsigned long long v = 0;
   CUDA_TRY(cudaMemcpyAsync(&v, c->d_exterior, sizeof(v), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, sizeof(v), st));
+  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0, sizeof(v), st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  *out = (v == ~0ull) ? -1 : (int64_t)v;
+  *out = v ? (int64_t)~v : -1;
   return check_watchdog(c, st);
+}
+
+// one stream-ordered memset clears every status flag before a call walks
+static int reset_status(wos_context* c, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(c->d_status, 0, kStatusBytes, st));
+  return WOS_OK;
+}
+
+extern "C" int wos_context_status(wos_context* c, void* stream, int64_t* out_first_exterior,
+                                  uint32_t* out_watchdog, double* out_worst_sigma_prime) {
+  if (!c) return fail(WOS_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long h[kStatusBytes / 8];
+  CUDA_TRY(cudaMemcpyAsync(h, c->d_status, kStatusBytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(c->d_status, 0, kStatusBytes, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int64_t ext = h[0] ? (int64_t)~h[0] : -1;
+  if (ext < 0) ext = c->host_exterior;
+  c->host_exterior = -1;
+  double w = -1.0;
+  if (h[1]) memcpy(&w, &h[1], sizeof(w));
+  if (out_first_exterior) *out_first_exterior = ext;
+  if (out_watchdog) *out_watchdog = (uint32_t)(h[2] & 0xffffffffu);
+  if (out_worst_sigma_prime) *out_worst_sigma_prime = w;
+  return WOS_OK;
 }
 
 extern "C" int wos_check_interior(wos_context* c, const wos_problem_set* s, int64_t n,
@@ -1396,9 +1434,18 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     return fail(WOS_ERR_UNSUPPORTED,
                 "problem table too large for shared memory (%zu bytes); split the batch",
                 (size_t)a.stage_bytes);
-  CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kBlock, smem));
+  {
+    std::lock_guard<std::mutex> g(c->launch_mu);
+    auto it = c->launch_cache.find(k.fn);
+    if (it != c->launch_cache.end() && it->second.first == smem) {
+      per_sm = it->second.second;
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kBlock, smem));
+      c->launch_cache[k.fn] = std::make_pair(smem, per_sm);
+    }
+  }
   if (per_sm < 1) return fail(WOS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   if (c->blocks_per_sm > 0) per_sm = std::min(per_sm, c->blocks_per_sm);
   int64_t grid = (int64_t)c->num_sms * per_sm;
@@ -1449,6 +1496,8 @@ extern "C" int wos_walk_rows(wos_context* c, const wos_problem_set* s, const wos
   if (n == 0) return WOS_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  int r0 = reset_status(c, st);
+  if (r0) return r0;
   for (int64_t off = 0; off < n; off += kMaxItemsPerLaunch) {
     const int64_t m = std::min<int64_t>(kMaxItemsPerLaunch, n - off);
     KArgs a;
@@ -1558,6 +1607,11 @@ extern "C" int wos_estimate(wos_context* c, const wos_problem_set* s, const wos_
                             const int32_t* inst_index, int64_t L, uint64_t traj_start,
                             double* out_mean, double* out_m2, uint64_t* out_total_steps,
                             void* stream) {
+  if (c && s && cfg && P > 0) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    int r = reset_status(c, (cudaStream_t)stream);
+    if (r) return r;
+  }
   return estimate_impl(c, s, cfg, P, points, point_ids, inst_index, L, traj_start, out_mean, out_m2,
                        out_total_steps, (cudaStream_t)stream, 0);
 }
@@ -1573,6 +1627,8 @@ extern "C" int wos_estimate_fold(wos_context* c, const wos_problem_set* s,
   if (P == 0) return WOS_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  int r0 = reset_status(c, st);
+  if (r0) return r0;
   // the epoch's fresh (mean, m2) live only in stream-ordered scratch
   double* fresh = nullptr;
   CUDA_TRY(cudaMallocAsync((void**)&fresh, 2 * (size_t)P * sizeof(double), st));
@@ -1688,6 +1744,7 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   int32_t* d_inst = inst_index ? (int32_t*)(base + bp + 3 * b8) : nullptr;
   const cudaStream_t cs = c->stream, xs = c->copy_stream, cs2 = c->stream2;
   CUDA_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(unsigned long long), cs));
+  if ((r = reset_status(c, cs))) return r;
   CUDA_TRY(cudaEventRecord(c->ev_start, cs));
   CUDA_TRY(cudaStreamWaitEvent(cs2, c->ev_start, 0));
   // Software pipeline over point chunks: copies on `xs`, walks alternately on `cs` and
@@ -1727,7 +1784,7 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   unsigned long long steps = 0, ext = 0;
   CUDA_TRY(cudaMemcpyAsync(&steps, c->d_steps, 8, cudaMemcpyDeviceToHost, cs));
   CUDA_TRY(cudaMemcpyAsync(&ext, c->d_exterior, 8, cudaMemcpyDeviceToHost, cs));
-  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0xff, 8, cs));
+  CUDA_TRY(cudaMemsetAsync(c->d_exterior, 0, 8, cs));
   CUDA_TRY(cudaStreamSynchronize(cs));
   CUDA_TRY(cudaStreamSynchronize(xs));
   if (out_total_steps) *out_total_steps = steps;
@@ -1735,9 +1792,9 @@ extern "C" int wos_estimate_host(wos_context* c, const wos_problem_set* s,
   if (r) return r;
   r = check_majorant(c, cfg, cs);
   if (r) return r;
-  if (ext != ~0ull) {
-    c->host_exterior = (int64_t)ext;
-    return fail(WOS_ERR_EXTERIOR, "exterior query: start point %lld", (long long)ext);
+  if (ext != 0ull) {
+    c->host_exterior = (int64_t)~ext;
+    return fail(WOS_ERR_EXTERIOR, "exterior query: start point %lld", (long long)~ext);
   }
   return WOS_OK;
 }

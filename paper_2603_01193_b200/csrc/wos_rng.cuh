@@ -12,6 +12,10 @@
 
 namespace wos {
 
+#ifndef WOS_PHILOX_R
+#define WOS_PHILOX_R 10
+#endif
+
 __device__ __forceinline__ void philox4x64(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
                                            uint64_t k0, uint64_t k1, uint64_t out[4]) {
 #pragma unroll
@@ -99,7 +103,7 @@ __device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t c0, const PhiloxPre&
                                                    const uint32_t* rk1) {
   uint4 c = philox_pre_r01(c0, p);
 #pragma unroll
-  for (int r = 2; r < 10; ++r) {
+  for (int r = 2; r < WOS_PHILOX_R; ++r) {
     const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
     uint64_t p0 = (uint64_t)M0 * c.x;
     uint64_t p1 = (uint64_t)M1 * c.z;

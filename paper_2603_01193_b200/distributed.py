@@ -17,7 +17,7 @@ import math
 
 import numpy as np
 
-__all__ = ["shard_indices", "gather_estimates", "estimate_sharded"]
+__all__ = ["shard_indices", "pack_shard", "unpack_gathered", "gather_estimates", "estimate_sharded"]
 
 
 def shard_indices(n_points: int, rank: int, world: int) -> np.ndarray:
@@ -25,6 +25,26 @@ def shard_indices(n_points: int, rank: int, world: int) -> np.ndarray:
     if not 0 <= rank < world:
         raise ValueError("rank out of range")
     return np.arange(rank, n_points, world, dtype=np.int64)
+
+
+def pack_shard(mean, m2, n_points: int, world: int):
+    """This rank's (mean, m2) shard as the (2, ceil(P / world)) gather buffer (zero padded)."""
+    import torch
+
+    n_max = math.ceil(n_points / world)
+    buf = torch.zeros((2, n_max), dtype=mean.dtype, device=mean.device)
+    n_loc = mean.shape[0]
+    buf[0, :n_loc] = mean
+    buf[1, :n_loc] = m2
+    return buf
+
+
+def unpack_gathered(out, n_points: int):
+    """(world, 2, n_max) gathered buffers -> full-length (mean, m2) in global point order:
+    global point p = r + world * k  <->  out[r, :, k]."""
+    world, _, n_max = out.shape
+    full = out.permute(1, 2, 0).reshape(2, n_max * world)[:, :n_points]
+    return full[0], full[1]
 
 
 def gather_estimates(mean, m2, n_points: int, rank: int, world: int, group=None):
@@ -36,21 +56,15 @@ def gather_estimates(mean, m2, n_points: int, rank: int, world: int, group=None)
     import torch
     import torch.distributed as dist
 
-    n_max = math.ceil(n_points / world)
-    buf = torch.zeros((2, n_max), dtype=mean.dtype, device=mean.device)
-    n_loc = mean.shape[0]
-    buf[0, :n_loc] = mean
-    buf[1, :n_loc] = m2
+    buf = pack_shard(mean, m2, n_points, world)
     if dist.get_backend(group) == "nccl":
-        out = torch.empty((world, 2, n_max), dtype=mean.dtype, device=mean.device)
+        out = torch.empty((world,) + tuple(buf.shape), dtype=mean.dtype, device=mean.device)
         dist.all_gather_into_tensor(out, buf, group=group)
     else:
         parts = [torch.empty_like(buf) for _ in range(world)]
         dist.all_gather(parts, buf, group=group)
         out = torch.stack(parts)
-    # global point p = r + world * k  <->  out[r, :, k]
-    full = out.permute(1, 2, 0).reshape(2, n_max * world)[:, :n_points]
-    return full[0], full[1]
+    return unpack_gathered(out, n_points)
 
 
 def estimate_sharded(problems, points, L, cfg, *, inst_index=None, point_ids=None, traj_start=0):
@@ -69,10 +83,15 @@ def estimate_sharded(problems, points, L, cfg, *, inst_index=None, point_ids=Non
     P = pts.shape[0]
     ids = np.arange(P, dtype=np.int64) if point_ids is None else np.asarray(point_ids, dtype=np.int64)
     idx = shard_indices(P, rank, world)
-    mean, m2, n = estimate_arrays(
-        problems, pts[idx], L, cfg, point_ids=ids[idx],
-        inst_index=None if inst_index is None else np.asarray(inst_index)[idx], traj_start=traj_start,
-    )
+    if idx.size:
+        mean, m2, _ = estimate_arrays(
+            problems, pts[idx], L, cfg, point_ids=ids[idx],
+            inst_index=None if inst_index is None else np.asarray(inst_index)[idx], traj_start=traj_start,
+        )
+    else:  # more ranks than points: this rank's strided shard is empty
+        mean, m2 = np.empty(0), np.empty(0)
     dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
     gm, gv = gather_estimates(torch.from_numpy(mean).to(dev), torch.from_numpy(m2).to(dev), P, rank, world)
-    return gm.cpu().numpy(), gv.cpu().numpy(), np.full(P, n[0] if P else L, dtype=np.int64)
+    # samples per point from the config, not from a (possibly empty) local shard
+    n_samples = L // 2 if cfg.antithetic else L
+    return gm.cpu().numpy(), gv.cpu().numpy(), np.full(P, n_samples, dtype=np.int64)

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from ctypes import byref, c_double, c_int32, c_int64, c_void_p
+from ctypes import byref, c_double, c_int32, c_int64, c_uint32, c_void_p
 
 import numpy as np
 
@@ -157,6 +157,14 @@ class Context:
             "sm_clock_hz": clk.value,
             "num_sms": nsm.value,
         }
+
+    def status(self, stream=None):
+        """(first exterior index or -1, watchdog flag, worst sigma' above sigma_bar or -1)
+        of the last walking call on this context; synchronizes ``stream`` and clears."""
+        first, wd, sp = c_int64(-1), c_uint32(0), c_double(-1.0)
+        _lib.check(self._lib.wos_context_status(self.handle, _stream_ptr(stream), byref(first), byref(wd),
+                                        byref(sp)))
+        return first.value, int(wd.value), sp.value
 
     def exterior(self, stream=None) -> int:
         first = c_int64(-1)

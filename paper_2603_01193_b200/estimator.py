@@ -4,8 +4,9 @@
 L trajectories per point (traj ids ``traj_start + j``; antithetic pairs share an
 id and their pair means are the samples), reduced to ``PointEstimate(mean, m2,
 n_samples)``. The walks and the per-point reduction run fused in one persistent
-sm_100a kernel; ``workers`` > 1 spreads the points over that many visible GPUs
-(threads, one context per device). Results are bit-identical for any worker
+sm_100a kernel; ``workers`` > 1 splits the points into that many strided shards
+(point p -> shard p mod workers), shard i on GPU i mod n_gpus (threads, one context
+per device). Results are bit-identical for any worker
 count, batch layout or point order, like the reference's.
 
 ``estimate_arrays`` returns numpy arrays instead of a list of dataclasses and
@@ -17,7 +18,6 @@ stream-ordered, no host copies) used for benchmarking and multi-GPU sharding.
 from __future__ import annotations
 
 import math
-import threading
 from ctypes import byref, c_int64, c_uint64
 from dataclasses import dataclass
 
@@ -34,6 +34,7 @@ __all__ = [
     "estimate",
     "estimate_arrays",
     "estimate_tensors",
+    "check_status",
     "ExteriorQueryError",
 ]
 
@@ -114,6 +115,43 @@ def _device_count():
         return 1
 
 
+def _estimate_shards(problems, pts, pids, inst, L, cfg, eps, traj_start, n_shards):
+    """Strided shards (point p -> shard p mod n_shards, distributed.shard_indices), shard i
+    on device i mod n_gpus, reassembled in point order. An exception raised in a shard
+    (exterior point, majorant violation, CUDA error) is re-raised here, as the reference's
+    ``fut.result()`` does (estimator.py:176-181)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .distributed import shard_indices
+
+    P = pts.shape[0]
+    ndev = _device_count()
+    if pids is None:
+        pids = np.arange(P, dtype=np.int64)
+    shards = [shard_indices(P, i, n_shards) for i in range(n_shards)]
+
+    def run(i):
+        idx = shards[i]
+        return _estimate_one_device(
+            i % ndev, problems, np.ascontiguousarray(pts[idx]), np.ascontiguousarray(pids[idx]),
+            None if inst is None else np.ascontiguousarray(inst[idx]), L, cfg, eps, traj_start,
+        )
+
+    with ThreadPoolExecutor(max_workers=min(n_shards, ndev)) as ex:
+        futs = [ex.submit(run, i) for i in range(n_shards)]
+        results = [f.result() for f in futs]
+    # the reference reports the first exterior point in point order (estimator.py:156-159)
+    firsts = [int(idx[first]) for (_, _, first, _), idx in zip(results, shards) if first >= 0]
+    if firsts:
+        raise_exterior(pts, min(firsts))
+    mean = np.empty(P, dtype=np.float64)
+    m2 = np.empty(P, dtype=np.float64)
+    for (m, v, _, _), idx in zip(results, shards):
+        mean[idx] = m
+        m2[idx] = v
+    return mean, m2, sum(r[3] for r in results)
+
+
 def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None, traj_start=0,
                     workers=1, return_steps=False):
     """Per-point (mean, m2, n_samples) arrays for a batch of problem instances.
@@ -151,34 +189,14 @@ def estimate_arrays(problems, points, L, cfg, *, inst_index=None, point_ids=None
         raise_exterior(pts, first.value)
         _validate_counts(L, cfg.antithetic)
     n_samples = L // 2 if cfg.antithetic else L
-    ndev = min(max(1, int(workers)), _device_count(), max(P, 1))
-    if ndev <= 1 or P <= 1:
+    # workers = strided point shards (the reference's process fan-out, estimator.py:166-181:
+    # here shard i runs on GPU i mod n_gpus); results are bit-identical for any count
+    n_shards = min(max(1, int(workers)), max(P, 1))
+    if n_shards <= 1:
         mean, m2, first, steps = _estimate_one_device(None, problems, pts, pids, inst, L, cfg, eps, traj_start)
         raise_exterior(pts, first)
     else:
-        chunks = np.array_split(np.arange(P), ndev)
-        results = [None] * ndev
-
-        if pids is None:
-            pids = np.arange(P, dtype=np.int64)
-
-        def run(i, idx):
-            results[i] = _estimate_one_device(
-                i, problems, np.ascontiguousarray(pts[idx]), np.ascontiguousarray(pids[idx]),
-                None if inst is None else np.ascontiguousarray(inst[idx]), L, cfg, eps, traj_start,
-            )
-
-        threads = [threading.Thread(target=run, args=(i, c)) for i, c in enumerate(chunks)]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        for (m, v, first, _), idx in zip(results, chunks):
-            if first >= 0:
-                raise_exterior(pts, int(idx[first]))
-        mean = np.concatenate([r[0] for r in results])
-        m2 = np.concatenate([r[1] for r in results])
-        steps = sum(r[3] for r in results)
+        mean, m2, steps = _estimate_shards(problems, pts, pids, inst, L, cfg, eps, traj_start, n_shards)
     n = np.full(P, n_samples, dtype=np.int64)
     if return_steps:
         return mean, m2, n, steps
@@ -199,11 +217,19 @@ def estimate(inst, points, L, cfg, *, workers=1, traj_start=0, point_ids=None):
 
 
 def estimate_tensors(pset, points, point_ids, L, cfg, *, inst_index=None, traj_start=0,
-                     out_mean=None, out_m2=None, total_steps=None, stream=None, eps=None):
+                     out_mean=None, out_m2=None, total_steps=None, stream=None, eps=None,
+                     check=False):
     """Device-resident estimate: torch CUDA tensors in/out, ordered on ``stream``.
 
     points float64 (P, dim), point_ids int64 (P,), inst_index int32 (P,) or None,
     total_steps: uint64-compatible int64 tensor (1,) accumulated on the device.
+
+    The call never synchronizes: an exterior start point, a majorant violation or a
+    kernel watchdog trip is flagged on the device (the context's status block, cleared
+    at the start of every call). ``check=True`` synchronizes ``stream`` after the launch
+    and raises what the reference would (ExteriorQueryError naming the point,
+    estimator.py:156-159; MajorantViolationError, walker.py:409-413) or a RuntimeError
+    for a watchdog trip; otherwise ``pset.ctx.status(stream)`` reads the flags later.
     """
     import torch
 
@@ -225,4 +251,21 @@ def estimate_tensors(pset, points, point_ids, L, cfg, *, inst_index=None, traj_s
             None if total_steps is None else total_steps.data_ptr(), stream.cuda_stream,
         )
     )
+    if check:
+        check_status(ctx, stream, points, cfg)
     return out_mean, out_m2
+
+
+def check_status(ctx, stream, points, cfg):
+    """Raise the error the last walking call on ``ctx`` flagged on the device, if any."""
+    from .walker import MajorantViolationError
+
+    first, watchdog, worst = ctx.status(stream)
+    if watchdog:
+        raise RuntimeError("walk kernel watchdog tripped (iteration limit): results invalid")
+    if worst >= 0.0:
+        raise MajorantViolationError(
+            f"majorant violated: sigma'={worst!r} > sigma_bar={cfg.sigma_bar!r}")
+    if first >= 0:
+        pt = points[first].detach().cpu().numpy() if hasattr(points, "detach") else np.asarray(points)[first]
+        raise_exterior(np.asarray(pt)[None, :], 0)

@@ -33,26 +33,23 @@ def calls(name):
 
 def effective(name):
     cfg, _, _ = case(name)
-    defaults = artifacts.SOLVE_DEFAULTS if str(Z[f"{name}__command"]) == "solve" else artifacts.BENCH_DEFAULTS
-    eff = artifacts.effective_config(defaults, dict(cfg, output="x.csv"))
-    artifacts.resolve_workers(eff)
-    return eff
+    return artifacts.RunConfig.load(str(Z[f"{name}__command"]), dict(cfg, output="x.csv"))
 
 
 @pytest.mark.parametrize("name", CASES)
 def test_run_stamp_matches_reference(name):
     _, csv_bytes, summary = case(name)
-    stamp = artifacts.run_stamp(effective(name), program="spherewalk", version="0.1.0")
+    stamp = effective(name).stamp(program="spherewalk", version="0.1.0")
     assert csv_bytes.split(b"\n", 1)[0].decode() == stamp == summary["header"]
-    ours = artifacts.run_stamp(effective(name))
+    ours = effective(name).stamp()
     assert ours.startswith("# wos-b200 ") and ours.split(" ", 3)[3] == stamp.split(" ", 3)[3]
 
 
 @pytest.mark.parametrize("name", SOLVES)
 def test_grid_points_match_reference(name):
     cfg, _, _ = case(name)
-    prob = artifacts.build_problem(cfg["problem"])
-    pts, ids = artifacts.build_points(cfg, prob.domain, "solve")
+    prob = artifacts.problem_from_spec(cfg["problem"])
+    pts, ids = artifacts.query_points(artifacts.RunConfig.load("solve", cfg), prob.domain)
     (c,) = list(calls(name))
     np.testing.assert_array_equal(pts, c["points"])
     np.testing.assert_array_equal(ids, c["ids"])
@@ -63,15 +60,15 @@ def test_grid_points_match_reference(name):
 def test_solve_csv_bytes_from_reference_estimates(tmp_path, name, as_arrays):
     _, csv_bytes, _ = case(name)
     (c,) = list(calls(name))
-    stamp = artifacts.run_stamp(effective(name), program="spherewalk", version="0.1.0")
+    stamp = effective(name).stamp(program="spherewalk", version="0.1.0")
     if as_arrays:
         res = (c["mean"], c["m2"], c["n"])
     else:
         res = [PointEstimate(float(a), float(b), int(n)) for a, b, n in zip(c["mean"], c["m2"], c["n"])]
     out = tmp_path / "s.csv"
-    artifacts.write_estimate_csv(out, stamp, c["ids"], c["points"], res)
+    artifacts.write_solve_csv(out, stamp, c["ids"], c["points"], res)
     assert out.read_bytes() == csv_bytes
-    stamp2, ids, pts, ests = artifacts.read_estimate_csv(out)
+    stamp2, ids, pts, ests = artifacts.read_solve_csv(out)
     assert stamp2 == stamp
     np.testing.assert_array_equal(ids, c["ids"])
     np.testing.assert_array_equal(pts, c["points"])
@@ -99,51 +96,58 @@ def test_bench_rows_from_reference_means(tmp_path):
     for c in calls(name):
         by_L.setdefault(int(c["L"]), []).append((int(c["traj_start"]), c["mean"]))
     lines = csv_bytes.decode().splitlines()
+    rows = []
     assert lines[1] == "trajectories,replicas,mean,replica_variance,variance_times_l,seconds_per_replica"
     for line, srow, L in zip(lines[2:], summary["rows"], cfg["trajectory_counts"]):
         reps = sorted(by_L[L])
         assert [t for t, _ in reps] == [k * L for k in range(cfg["replicas"])]
         wall = float(line.split(",")[-1]) * cfg["replicas"]
-        row, s = artifacts.bench_row(L, np.stack([m for _, m in reps]), wall)
-        assert ",".join(str(v) for v in row[:5]) == ",".join(line.split(",")[:5])
+        row, s = artifacts.bench_stats(L, np.stack([m for _, m in reps]), wall)
+        assert ",".join(repr(v) for v in row[:5]) == ",".join(line.split(",")[:5])
         assert s == srow
+        rows.append(row[:5] + [float(line.split(",")[-1])])
     out = tmp_path / "b.csv"
-    rows = [line.split(",") for line in lines[2:]]
     artifacts.write_bench_csv(out, lines[0], rows)
     assert out.read_bytes() == csv_bytes
 
 
 def test_config_errors(monkeypatch):
+    load = artifacts.RunConfig.load
     with pytest.raises(artifacts.UsageError, match="unknown config field"):
-        artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {"trajectoriez": 3})
-    eff = artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {})
+        load("solve", {"trajectoriez": 3})
+    with pytest.raises(artifacts.UsageError, match="unknown config field"):
+        load("solve", {"replicas": 3})  # a bench-only field
+    rc = load("solve", {})
     with pytest.raises(artifacts.UsageError, match="exactly one of 'problem' or 'instance'"):
-        artifacts.build_instance(eff, "solve")
-    eff["instance"] = {"family": "linear"}
+        artifacts.run_problem(rc)
+    rc.values["instance"] = {"family": "linear"}
     with pytest.raises(artifacts.UsageError, match="out of scope"):
-        artifacts.build_instance(eff, "solve")
+        artifacts.run_problem(rc)
     with pytest.raises(artifacts.UsageError, match="bad domain config"):
-        artifacts.build_problem({"domain": {"kind": "torus"}})
-    monkeypatch.setenv(artifacts.ENV_WORKERS, "3")
-    eff = artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {})
-    assert artifacts.resolve_workers(eff) == 3 and eff["workers"] == 3
-    monkeypatch.setenv(artifacts.ENV_WORKERS, "x")
+        artifacts.problem_from_spec({"domain": {"kind": "torus"}})
+    monkeypatch.setenv(artifacts.WORKERS_ENV, "3")
+    assert load("solve", {}).workers == 3
+    assert load("solve", {"workers": 2}).workers == 2
+    monkeypatch.setenv(artifacts.WORKERS_ENV, "x")
     with pytest.raises(artifacts.UsageError, match="not an integer"):
-        artifacts.resolve_workers(artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {}))
+        load("solve", {})
     with pytest.raises(artifacts.UsageError, match="at least 1"):
-        artifacts.resolve_workers({"workers": 0})
-    prob = artifacts.build_problem({"domain": {"kind": "ball", "center": [0, 0], "radius": 1.0}})
+        load("solve", {"workers": 0})
+    monkeypatch.delenv(artifacts.WORKERS_ENV)
+    assert load("bench", {}).workers == 1 and load("bench", {})["output"] == "bench.csv"
+    prob = artifacts.problem_from_spec({"domain": {"kind": "ball", "center": [0, 0], "radius": 1.0}})
     with pytest.raises(artifacts.UsageError, match="no interior points"):
-        artifacts.build_points({"grid": {"lo": [2, 2], "hi": [3, 3], "shape": [2, 2]}}, prob.domain, "solve")
+        artifacts.query_points(load("solve", {"grid": {"lo": [2, 2], "hi": [3, 3], "shape": [2, 2]}}), prob.domain)
     with pytest.raises(artifacts.UsageError, match="dimension 2"):
-        artifacts.build_points({"points": [[0, 0, 0]]}, prob.domain, "solve")
+        artifacts.query_points(load("solve", {"points": [[0, 0, 0]]}), prob.domain)
     with pytest.raises(artifacts.UsageError, match="exactly one of 'points' or 'grid'"):
-        artifacts.build_points({}, prob.domain, "solve")
+        artifacts.query_points(load("solve", {}), prob.domain)
 
 
 def test_runtime_keys_do_not_change_the_hash():
-    a = artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {"seed": 4, "workers": 1, "output": "a.csv"})
-    b = artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {"seed": 4, "workers": 8, "output": "b.csv"})
-    assert artifacts.config_hash(a) == artifacts.config_hash(b)
-    c = artifacts.effective_config(artifacts.SOLVE_DEFAULTS, {"seed": 5})
-    assert artifacts.config_hash(a) != artifacts.config_hash(c)
+    load = artifacts.RunConfig.load
+    a = load("solve", {"seed": 4, "workers": 1, "output": "a.csv"})
+    b = load("solve", {"seed": 4, "workers": 8, "output": "b.csv"})
+    assert a.identity_hash() == b.identity_hash()
+    assert a.identity_hash() != load("solve", {"seed": 5}).identity_hash()
+    assert a.identity_hash() != load("bench", {"seed": 4}).identity_hash()

@@ -47,7 +47,7 @@ def test_abi_version_and_error_string():
     from paper_2603_01193_b200 import _lib
 
     L = _lib.load_library()
-    assert L.wos_abi_version() == _lib.ABI_VERSION == 3
+    assert L.wos_abi_version() == _lib.ABI_VERSION == 4
     assert isinstance(_lib.last_error(), str)
 
 

@@ -67,7 +67,7 @@ def test_solve_native_is_deterministic_and_close(gpu, tmp_path):
     a, _ = artifacts.solve(dict(cfg, output=str(tmp_path / "a.csv")))
     b, _ = artifacts.solve(dict(cfg, output=str(tmp_path / "b.csv")))
     assert a.read_bytes() == b.read_bytes()
-    _, ids, pts, ests = artifacts.read_estimate_csv(a)
+    _, ids, pts, ests = artifacts.read_solve_csv(a)
     # Laplacian u = 1 on the unit disk, u = 0 on the circle: u = (r^2 - 1) / 4
     exact = (np.sum(pts * pts, axis=1) - 1.0) / 4.0
     mean = np.array([e.mean for e in ests])
@@ -99,7 +99,7 @@ def test_bench_replay_matches_reference_cli(gpu, tmp_path):
 
 def test_solve_bytes_invariant_to_workers(gpu, tmp_path):
     """The reference's criterion 12 (test_acceptance.py:355-391): CSV bytes after the run
-    stamp are identical for workers 1/4/8 (here: GPUs, clamped to the devices present)
+    stamp are identical for workers 1/4/8 (strided point shards, here all on cuda:0)
     and the stamps differ only in their workers field."""
     from paper_2603_01193_b200 import artifacts
 
