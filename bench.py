@@ -1,6 +1,7 @@
 """Benchmark of the B200 WoS label estimator (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+                    [--mode native|replay|replay_f32] [--philox-rounds 10|7]
 
 One "step" = one full pass of the estimator over the workload: every query
 point of the config runs its L walks and is reduced to (mean, m2). Default
@@ -12,13 +13,18 @@ names for 1/2/4/8-GPU scaling. Under torchrun each rank takes a strided
 
 Metric: walk-steps/s (whole job), plus walks/s. Timing: CUDA events on the
 launching stream around each step, L2 flushed (256 MiB write) before every step
-outside the timed window, max over ranks. The CPU baseline is the oracle
-(oracle/wos_oracle.c, a C restatement of the reference's path) on the host cores.
+outside the timed window, max over ranks. On rank 0 at N = 1 the line also
+carries: the cfg4 reference form on the GPU (REPLAY_F64, the reference's
+estimator draw for draw, fp64), per-config sub-records for cfg0-cfg3 (one
+estimate's latency and replica-batched throughput, each with its roofline), and
+the CPU baseline: the oracle (oracle/wos_oracle.c, a C restatement of the
+reference's path) on the host cores over a seeded random sample of the points.
 """
 
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -31,24 +37,42 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# algorithmic work per walk-step / per walk (native form):
-# (F_step, S_step, F_walk, S_walk) in FP32 flops (FFMA = 2) and SFU ops
+# Algorithmic work per walk-step / per walk (native form):
+# (F_step, S_step, F_walk, S_walk) in FP32 flops (FFMA = 2) and SFU ops.
+# cfg3 is measured instead (see work()): its candidate-grid query evaluates a
+# varying number of segments, counted in the kernel.
 WORK = {
     0: (71, 9, 9, 0),
     1: (13, 3, 87, 1),
     2: (187, 9, 31, 2),
-    3: (2072, 7, 4232, 2),
+    3: (None, 7, 87, 2),
     4: (125, 12, 12, 0),
 }
+SEG_FLOPS = 16        # one point-to-segment distance (128 segments x 16)
+CFG3_STEP_FLOPS = 24  # the rest of a cfg3 jump: Gaussian f 6 + move, sample, tests 18
+SFU_PER_SM_CLK = 16   # MUFU ops per SM per clock (sin/cos/sqrt/rsqrt/ex2/lg2/rcp)
+FP32_PER_SM_CLK = 256  # 128 FP32 lanes x 2 flops (FFMA)
+LABEL_BYTES = 16      # per point written by the estimate: mean, m2 (fp64)
+DEFAULT_REPLICAS = {0: 64, 1: 16, 2: 16, 3: 1, 4: 1}
+
+
+def work(cfg_index, steps, walks, seg_evals=0):
+    """(FP32 flops, SFU ops) of `steps` walk-steps and `walks` walks of config cfg_index."""
+    F_step, S_step, F_walk, S_walk = WORK[cfg_index]
+    if F_step is None:  # measured: segment distances counted by the kernel
+        fp32 = SEG_FLOPS * seg_evals + CFG3_STEP_FLOPS * steps + F_walk * walks
+    else:
+        fp32 = F_step * steps + F_walk * walks
+    return fp32, S_step * steps + S_walk * walks
 
 
 def _ncu_traffic(workload):
     """DRAM bytes (read + write) per launch of the walk kernel from the committed ncu capture."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[workload]
-        return d["dram_bytes_read"] + d["dram_bytes_write"]
+        return d["dram_bytes_read"] + d["dram_bytes_write"], d.get("source")
     except (OSError, KeyError, ValueError):
-        return None
+        return None, None
 
 
 def _env_int(name, default):
@@ -56,6 +80,23 @@ def _env_int(name, default):
         return int(os.environ.get(name, default))
     except ValueError:
         return default
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
 
 
 class ClockSampler:
@@ -116,35 +157,52 @@ class ClockSampler:
         }
 
 
-def cpu_baseline(w, budget_s=12.0, nthreads=None):
-    """Oracle (reference-form C port) on the host cores over a bounded, strided sample."""
+def sample_points(w, n, seed=12345):
+    """A seeded random sample of n points (sorted): representative of the whole config,
+    unlike a fixed stride (every 128th point of cfg4's C-order 64^3 grid is one face
+    plane)."""
+    n = min(n, w.n_points)
+    return np.sort(np.random.default_rng(seed).permutation(w.n_points)[:n])
+
+
+def _oracle_sample(w, n, traj_start, nthreads):
+    from oracle import oracle as O
+
+    sub = w.subset(sample_points(w, n))
+    t0 = time.perf_counter()
+    _, _, steps = O.estimate(sub.problems, sub.points, w.L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
+                             max_steps=w.cfg.max_steps, point_ids=sub.point_ids, inst_index=sub.inst_index,
+                             traj_start=traj_start, nthreads=nthreads)
+    return time.perf_counter() - t0, steps, sub.n_points
+
+
+def cpu_baseline(w, budget_s=12.0, nthreads=None, full_steps_per_walk=None):
+    """Oracle (reference-form C port) on the host cores over a bounded seeded sample."""
     from oracle import oracle as O
 
     nthreads = nthreads or O.default_threads()
     O.load()
-    n = 64
-    t_used = 0.0
+    n, t_used = 64, 0.0
     while True:
-        idx = np.arange(0, w.n_points, max(1, w.n_points // n))[:n]
-        sub = w.subset(idx)
-        t0 = time.perf_counter()
-        _, _, steps = O.estimate(sub.problems, sub.points, w.L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
-                                 max_steps=w.cfg.max_steps, point_ids=sub.point_ids,
-                                 inst_index=sub.inst_index, nthreads=nthreads)
-        dt = time.perf_counter() - t0
+        dt, steps, m = _oracle_sample(w, n, 0, nthreads)
         t_used += dt
         if dt >= budget_s * 0.5 or n >= w.n_points or t_used > budget_s * 2:
             break
         n = min(w.n_points, int(n * max(2.0, min(16.0, budget_s * 0.6 / max(dt, 1e-3)))))
-    return {
+    out = {
         "value": steps / dt,
         "unit": "walk-steps/s",
         "cores": nthreads,
+        "cpu_model": cpu_model(),
         "kind": "port",
-        "walks_per_s": sub.n_points * w.L / dt,
-        "sample": f"{sub.n_points} of {w.n_points} points (strided) x {w.L} walks, reference form "
+        "walks_per_s": m * w.L / dt,
+        "sample": f"{m} of {w.n_points} points (seeded random sample) x {w.L} walks, reference form "
                   f"(Philox4x64, uniform-ball source, fp64), {steps} walk-steps in {dt:.2f}s",
+        "sample_mean_steps_per_walk": steps / (m * w.L),
     }
+    if full_steps_per_walk is not None:
+        out["full_config_mean_steps_per_walk"] = full_steps_per_walk
+    return out
 
 
 def run_reference(args, rank, world):
@@ -156,28 +214,18 @@ def run_reference(args, rank, world):
 
     w = configs.build(args.config, mode="replay")
     nthreads = O.default_threads()
-    # a bounded strided sample per step, sized to ~1 s of host work
+    # a bounded seeded sample per step, sized to ~1 s of host work
     n = max(32, min(w.n_points, 2048 if args.config in (4, 3) else 8192))
-    idx = np.arange(0, w.n_points, max(1, w.n_points // n))[:n]
-    sub = w.subset(idx)
-
-    def one(step):
-        t0 = time.perf_counter()
-        _, _, s = O.estimate(sub.problems, sub.points, w.L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
-                             max_steps=w.cfg.max_steps, point_ids=sub.point_ids,
-                             inst_index=sub.inst_index, traj_start=step * w.L, nthreads=nthreads)
-        return time.perf_counter() - t0, s
-
     for i in range(args.warmup):
-        one(i)
+        _oracle_sample(w, n, i * w.L, nthreads)
     tot_t, tot_s = 0.0, 0
     for i in range(args.steps):
-        dt, s = one(args.warmup + i)
+        dt, s, m = _oracle_sample(w, n, (args.warmup + i) * w.L, nthreads)
         tot_t += dt
         tot_s += s
     val = tot_s / tot_t
-    walks = sub.n_points * w.L * args.steps / tot_t
-    sample = (f"{sub.n_points} of {w.n_points} points (strided) x {w.L} walks per step, "
+    walks = m * w.L * args.steps / tot_t
+    sample = (f"{m} of {w.n_points} points (seeded random sample) x {w.L} walks per step, "
               f"reference form (Philox4x64, uniform-ball source, fp64) via oracle/wos_oracle.c")
     line = {
         "impl": "reference",
@@ -194,13 +242,146 @@ def run_reference(args, rank, world):
         "dtype": "f64",
         "data": "synthetic (BASELINE config, pinned seeds)",
         "walks_per_s": walks,
-        "config": {"workload": w.name, "walks_per_point": w.L, "sample_points": int(sub.n_points)},
-        "cpu_baseline": {"value": val, "unit": "walk-steps/s", "cores": nthreads, "kind": "port",
-                         "sample": sample},
+        "mean_steps_per_walk": tot_s / (m * w.L * args.steps),
+        "config": {"workload": w.name, "walks_per_point": w.L, "sample_points": int(m)},
+        "cpu_baseline": {"value": val, "unit": "walk-steps/s", "cores": nthreads, "cpu_model": cpu_model(),
+                         "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": "walk-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def roofline(cfg_index, steps, walks, seconds, seg_evals, peaks, n_sm, clk_hz):
+    """Fractions of the FP32 / SFU issue roofline for `steps` walk-steps and `walks` walks in
+    `seconds` of one GPU: against the nominal peak (n_SM x {16 MUFU, 256 flop} x clock)
+    and against the probes measured in this run."""
+    fp32, sfu = work(cfg_index, steps, walks, seg_evals)
+    a_sfu, a_fp32 = sfu / seconds, fp32 / seconds
+    nom_sfu, nom_fp32 = n_sm * SFU_PER_SM_CLK * clk_hz, n_sm * FP32_PER_SM_CLK * clk_hz
+    fr_sfu, fr_fp32 = a_sfu / nom_sfu, a_fp32 / nom_fp32
+    bound = "sfu" if fr_sfu >= fr_fp32 else "fp32"
+    out = {
+        "bound": bound,
+        "achieved": a_sfu if bound == "sfu" else a_fp32,
+        "peak": nom_sfu if bound == "sfu" else nom_fp32,
+        "unit": "SFU op/s" if bound == "sfu" else "FP32 flop/s",
+        "frac": fr_sfu if bound == "sfu" else fr_fp32,
+        "peak_source": f"nominal: {n_sm} SMs x {SFU_PER_SM_CLK} MUFU (or {FP32_PER_SM_CLK} flop) per clock "
+                       f"x {clk_hz / 1e6:.0f} MHz (max SM clock)",
+        "sfu": {"achieved": a_sfu, "peak_nominal": nom_sfu, "frac": fr_sfu},
+        "fp32": {"achieved": a_fp32, "peak_nominal": nom_fp32, "frac": fr_fp32},
+    }
+    if peaks:
+        out["sfu"].update(peak_probe=peaks["sfu_ops_per_s"], frac_probe=a_sfu / peaks["sfu_ops_per_s"])
+        out["fp32"].update(peak_probe=peaks["fp32_flops_per_s"], frac_probe=a_fp32 / peaks["fp32_flops_per_s"])
+    F_step, S_step, F_walk, S_walk = WORK[cfg_index]
+    out["work"] = {"S_step": S_step, "S_walk": S_walk, "F_walk": F_walk}
+    if F_step is None:
+        out["work"].update(F_step="measured", seg_evals=seg_evals,
+                           segments_per_step=seg_evals / max(steps, 1),
+                           F_rule=f"{SEG_FLOPS} x segment distances + {CFG3_STEP_FLOPS} x steps + "
+                                  f"{F_walk} x walks")
+    else:
+        out["work"]["F_step"] = F_step
+    return out
+
+
+def _time_estimates(step_fn, stream, n, flush=None):
+    """CUDA-event times (s) of n calls of step_fn(i) on `stream`."""
+    import torch
+
+    times = []
+    for i in range(n):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step_fn(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) * 1e-3)
+    return times
+
+
+def config_record(ctx, cfg_index, replicas, peaks, n_sm, clk_hz, flush, philox_rounds, reps=5):
+    """One BASELINE config on this GPU: a single estimate's latency (median of reps
+    launches, inputs resident) and replica-batched throughput (R independent label
+    replicas per launch, SURVEY.md 8(d) protocol items (i) and (ii))."""
+    import torch
+
+    from paper_2603_01193_b200 import configs, engine
+    from paper_2603_01193_b200.estimator import estimate_tensors
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    for label, R in (("single", 1), ("replicas", replicas)):
+        w = configs.build(cfg_index).replicate(R)
+        cfg = dataclasses.replace(w.cfg, philox_rounds=philox_rounds)
+        pset = engine.ProblemSet(ctx, w.problems)
+        pts = torch.from_numpy(np.ascontiguousarray(w.points)).to(dev)
+        ids = torch.from_numpy(np.ascontiguousarray(w.point_ids)).to(dev)
+        inst = torch.from_numpy(np.ascontiguousarray(w.inst_index)).to(dev) if len(w.problems) > 1 else None
+        eps = cfg.resolve_eps(w.problems[0].domain)
+        acc = torch.zeros(1, dtype=torch.int64, device=dev)
+
+        def one(i, acc_=None):
+            estimate_tensors(pset, pts, ids, w.L, cfg, inst_index=inst, traj_start=(100 + i) * w.L,
+                             total_steps=acc_, stream=stream, eps=eps)
+
+        for i in range(2):
+            one(i)
+        _, seg0 = ctx.counters(stream)
+        t = _time_estimates(lambda i: one(i, acc), stream, reps, flush)
+        _, seg1 = ctx.counters(stream)
+        S = int(acc.item()) / reps
+        t_med = float(np.median(t))
+        rec = {
+            "replicas": R,
+            "points": w.n_points,
+            "walks_per_point": w.L,
+            "ms": 1e3 * t_med,
+            "walk_steps_per_s": S / t_med,
+            "walks_per_s": w.n_walks / t_med,
+            "mean_steps_per_walk": S / w.n_walks,
+            "roofline": roofline(cfg_index, S, w.n_walks, t_med, (seg1 - seg0) / reps, peaks, n_sm, clk_hz),
+        }
+        out[label] = rec
+        pset.close()
+    return {"workload": configs.CONFIG_NAMES[cfg_index], "mode": "native",
+            "timing": f"CUDA events, median of {reps} launches, L2 flushed before each", **out}
+
+
+def replay_f64_record(ctx, cfg_index, flush, reps=2):
+    """The reference's estimator on the GPU (REPLAY_F64: Philox4x64, uniform-ball source,
+    fp64, draw for draw the reference's) over the full config: the like-for-like fp64
+    throughput and the full config's reference-form steps per walk."""
+    import torch
+
+    from paper_2603_01193_b200 import configs, engine
+    from paper_2603_01193_b200.estimator import estimate_tensors
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    w = configs.build(cfg_index, mode="replay")
+    pset = engine.ProblemSet(ctx, w.problems)
+    pts = torch.from_numpy(np.ascontiguousarray(w.points)).to(dev)
+    ids = torch.from_numpy(np.ascontiguousarray(w.point_ids)).to(dev)
+    inst = torch.from_numpy(np.ascontiguousarray(w.inst_index)).to(dev) if len(w.problems) > 1 else None
+    eps = w.cfg.resolve_eps(w.problems[0].domain)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    estimate_tensors(pset, pts, ids, w.L, w.cfg, inst_index=inst, stream=stream, eps=eps)
+    t = _time_estimates(lambda i: estimate_tensors(pset, pts, ids, w.L, w.cfg, inst_index=inst,
+                                                   traj_start=(1 + i) * w.L, total_steps=acc,
+                                                   stream=stream, eps=eps), stream, reps, flush)
+    S = int(acc.item()) / reps
+    ts = float(np.mean(t))
+    pset.close()
+    return {"workload": w.name, "mode": "replay_f64",
+            "what": "the reference's estimator draw for draw (Philox4x64, uniform-ball source, fp64)",
+            "ms": 1e3 * ts, "walk_steps_per_s": S / ts, "walks_per_s": w.n_walks / ts,
+            "mean_steps_per_walk": S / w.n_walks, "dtype": "f64"}
 
 
 def main():
@@ -211,8 +392,12 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", default="native")
+    ap.add_argument("--philox-rounds", type=int, default=10, choices=[10, 7],
+                    help="NATIVE Philox4x32 rounds (10: production stream; 7: opt-in)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--replicas", type=int, default=1,
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the per-config sub-records and the REPLAY_F64 line")
+    ap.add_argument("--replicas", type=int, default=None,
                     help="independent label replicas per point per step (small configs)")
     ap.add_argument("--refill-min", type=int, default=None)
     ap.add_argument("--refill-min-deferred", type=int, default=None)
@@ -238,7 +423,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    w = configs.build(args.config, mode=args.mode).replicate(args.replicas)
+    replicas = args.replicas or 1
+    w = configs.build(args.config, mode=args.mode).replicate(replicas)
+    w.cfg = dataclasses.replace(w.cfg, philox_rounds=args.philox_rounds)
     idx = shard_indices(w.n_points, rank, world)
     shard = w.subset(idx)
     ctx = engine.get_context(local)
@@ -264,12 +451,17 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    # the first exterior point / watchdog / majorant flags of the warm-up: all clear
+    first, watchdog, _ = ctx.status(stream)
+    if first >= 0 or watchdog:
+        raise RuntimeError(f"estimate flagged an error during warm-up: exterior {first}, watchdog {watchdog}")
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launches0, seg0 = ctx.counters(stream)
     clocks.start()
     time.sleep(0.3)
     for i in range(args.steps):
@@ -281,6 +473,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    launches1, seg1 = ctx.counters(stream)
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     tot_steps = steps_acc.clone()
@@ -293,15 +486,24 @@ def main():
     value = S / (ms * 1e-3)
     walks_per_s = n_walks / (ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (the persistent walk kernel) ----
-    F_step, S_step, F_walk, S_walk = WORK[args.config]
+    # ---- roofline of the dominant kernel (the persistent walk kernel), per rank ----
     t_launch = ms * 1e-3 / args.steps
-    # per-rank algorithmic work per launch; the slowest rank defines t_launch
-    S_rank = S / args.steps / world
-    Nw_rank = w.n_walks / world
-    sfu_ach = (S_rank * S_step + Nw_rank * S_walk) / t_launch
-    fp32_ach = (S_rank * F_step + Nw_rank * F_walk) / t_launch
     peaks = ctx.probe_peaks() if rank == 0 else None
+    n_sm = peaks["num_sms"] if peaks else torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_max_mhz = clk.get("sm_max_mhz") or _measured_peaks().get("sm_max_mhz") or 1965.0
+    clk_hz = clk_max_mhz * 1e6
+    rl = roofline(args.config, S / args.steps / world, w.n_walks / world, t_launch,
+                  (seg1 - seg0) / args.steps, peaks, n_sm, clk_hz)
+    traffic, traffic_src = _ncu_traffic(w.name)
+    rl["traffic"] = traffic
+    rl["traffic_source"] = traffic_src or "none committed"
+    # the labels the estimate writes (mean, m2 per point): bytes per launch and the
+    # bandwidth they take over the kernel, against the measured HBM copy bandwidth
+    hbm = _measured_peaks().get("hbm_gbs")
+    label_bytes = LABEL_BYTES * shard.n_points
+    label = {"bytes_per_step": label_bytes, "gbs": label_bytes / t_launch / 1e9,
+             "hbm_peak_gbs": hbm, "frac_of_hbm": (label_bytes / t_launch / 1e9 / hbm) if hbm else None,
+             "note": "written by the fused in-kernel reduction as units retire; HBM is not the bound"}
 
     # ---- e2e through the C-ABI with host buffers (H2D + kernel + D2H per step) ----
     def pinned(a):
@@ -314,14 +516,15 @@ def main():
 
     host_pts, _keep_pts = pinned(np.ascontiguousarray(shard.points))
     # default ids (0..P-1, the reference's estimate() default) are generated on the device
-    host_ids, _keep_ids = (None, None) if world == 1 and args.replicas == 1 and np.array_equal(
+    host_ids, _keep_ids = (None, None) if world == 1 and replicas == 1 and np.array_equal(
         shard.point_ids, np.arange(shard.n_points)) else pinned(np.ascontiguousarray(shard.point_ids))
     host_inst, _keep_inst = pinned(np.ascontiguousarray(shard.inst_index)) if inst is not None else (None, None)
     out_mean, _keep_mean = pinned(np.empty(shard.n_points))
     out_m2, _keep_m2 = pinned(np.empty(shard.n_points))
     from ctypes import byref, c_uint64
 
-    wc = engine.walk_config_struct(eps, w.cfg.max_steps, w.cfg.antithetic, w.cfg.mode, w.cfg.rng_seed)
+    wc = engine.walk_config_struct(eps, w.cfg.max_steps, w.cfg.antithetic, w.cfg.mode, w.cfg.rng_seed,
+                                   philox_rounds=w.cfg.philox_rounds)
     e2e_steps = c_uint64(0)
 
     def e2e_once(i):
@@ -352,14 +555,21 @@ def main():
     d2h = out_mean.nbytes + out_m2.nbytes + 16
 
     if rank == 0:
+        extras = {}
+        full_spw = None
+        if world == 1 and not args.no_extras:
+            if args.config == 4 and args.mode == "native":
+                extras["replay_f64"] = replay_f64_record(ctx, 4, flush)
+                full_spw = extras["replay_f64"]["mean_steps_per_walk"]
+            extras["configs"] = {
+                f"cfg{c}": config_record(ctx, c, DEFAULT_REPLICAS[c], peaks, n_sm, clk_hz, flush,
+                                         args.philox_rounds)
+                for c in (0, 1, 2, 3) if c != args.config
+            }
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = cpu_baseline(configs.build(args.config, mode="replay").replicate(args.replicas))
-        sfu_peak = peaks["sfu_ops_per_s"]
-        fp32_peak = peaks["fp32_flops_per_s"]
-        fr_sfu = sfu_ach / sfu_peak
-        fr_fp32 = fp32_ach / fp32_peak
-        bound = "sfu" if fr_sfu >= fr_fp32 else "fp32"
+            cpu = cpu_baseline(configs.build(args.config, mode="replay").replicate(replicas),
+                               full_steps_per_walk=full_spw)
         line = {
             "metric": "walk-steps/s",
             "value": value,
@@ -371,7 +581,7 @@ def main():
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f32" if args.mode.startswith("native") else ("f64" if args.mode.startswith("replay") and not args.mode.endswith("f32") else "f32"),
+            "dtype": "f32" if args.mode.startswith("native") or args.mode.endswith("f32") else "f64",
             "data": "synthetic (BASELINE config, pinned seeds; no dataset exists for this path)",
             "walks_per_s": walks_per_s,
             "walk_steps_per_step": S / args.steps,
@@ -381,34 +591,26 @@ def main():
                 "points": w.n_points,
                 "walks_per_point": w.L,
                 "instances": len(w.problems),
-                "replicas": args.replicas,
+                "replicas": replicas,
                 "eps": w.cfg.eps_shell,
                 "max_steps": w.cfg.max_steps,
                 "mode": args.mode,
+                "philox_rounds": args.philox_rounds,
                 "parallelism": f"dp{world} strided point shards + NCCL all-gather of (mean, m2)",
                 "l2": "flushed (256 MiB write) before every timed step, outside the events",
                 "traj_windows": "step i uses traj ids [i*L, (i+1)*L)",
             },
-            "roofline": {
-                "bound": bound,
-                "achieved": sfu_ach if bound == "sfu" else fp32_ach,
-                "peak": sfu_peak if bound == "sfu" else fp32_peak,
-                "unit": "SFU op/s" if bound == "sfu" else "FP32 flop/s",
-                "frac": fr_sfu if bound == "sfu" else fr_fp32,
-                "traffic": _ncu_traffic(w.name),
-                "sfu": {"achieved": sfu_ach, "peak_measured": sfu_peak, "frac": fr_sfu,
-                        "per_step": S_step, "per_walk": S_walk},
-                "fp32": {"achieved": fp32_ach, "peak_measured": fp32_peak, "frac": fr_fp32,
-                         "per_step": F_step, "per_walk": F_walk},
-                "peak_source": "measured in this run by wos_probe_peaks (MUFU rsqrt / FFMA microkernels)",
-                "sm_clock_mhz_probe": peaks["sm_clock_hz"] / 1e6,
-            },
+            "roofline": rl,
+            "label_writeout": label,
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "walk-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "path": "wos_estimate_host (C ABI, pinned host buffers; copies inside, pipelined in point chunks)"},
-            "gpu_launches": 2 * args.steps,
+            # kernels the library launched in the timed region (its own launch counter):
+            # per step the interior check, the walk kernel and (L > 128) the chunk merge
+            "gpu_launches": int(launches1 - launches0),
         }
+        line.update(extras)
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -195,6 +195,9 @@ typedef struct wos_walk_config {
   int32_t mode;        /* wos_mode */
   uint64_t rng_seed;   /* first Philox key word */
   double sigma_bar;    /* delta tracking majorant (WalkConfig.sigma_bar); ignored otherwise */
+  int32_t philox_rounds; /* NATIVE_F32: Philox4x32 rounds per block, 10 (0 = default) or 7
+                          * (opt-in, WalkConfig.philox_rounds); REPLAY modes ignore it */
+  int32_t reserved;      /* 0 */
 } wos_walk_config;
 
 typedef struct wos_context wos_context;         /* per-device scratch + streams */
@@ -290,6 +293,14 @@ int wos_context_exterior(wos_context* ctx, void* stream, int64_t* out_first_exte
 int wos_context_status(wos_context* ctx, void* stream, int64_t* out_first_exterior,
                        uint32_t* out_watchdog, double* out_worst_sigma_prime);
 
+/* Measurement counters of this context (cumulative, never reset): *out_launches = the
+ * kernels this library has launched on it (walk, interior check, chunk merge, cache
+ * fold / targets); *out_seg_evals = segment distances evaluated by NATIVE polygon walks
+ * (the measured work of a candidate-grid query; bench.py's cfg3 roofline). Synchronizes
+ * `stream` first. Either pointer may be NULL. */
+int wos_context_counters(wos_context* ctx, void* stream, uint64_t* out_launches,
+                         uint64_t* out_seg_evals);
+
 /* ---- epoch-averaged estimate cache (estimator.EstimateCache) -----------
  * replaces                                                      by
  *   EstimateCache.update / cache_update (estimator.py:217-244, 338-341)  wos_cache_fold
@@ -328,6 +339,12 @@ int wos_philox4x64(wos_context* ctx, int64_t n, const uint64_t* ctr, uint64_t ke
                    uint64_t key1, uint64_t* out, void* stream);
 int wos_philox4x32(wos_context* ctx, int64_t n, const uint32_t* ctr, uint32_t key0,
                    uint32_t key1, uint32_t* out, void* stream);
+
+/* Philox4x32-R for R in 1..16 (Random123 round function and key schedule): the KAT and
+ * statistics hook of the NATIVE stream's opt-in 7-round variant (wos_walk_config
+ * philox_rounds). Same arguments as wos_philox4x32 plus `rounds`. */
+int wos_philox4x32_rounds(wos_context* ctx, int64_t n, const uint32_t* counters, uint32_t k0,
+                          uint32_t k1, int32_t rounds, uint32_t* out, void* stream);
 
 /* ---- launch tuning ---------------------------------------------------- */
 /* refill_min: a warp refills idle lanes once at least this many are idle

@@ -63,6 +63,8 @@ def load():
         ]
         L.oracle_philox4x64.argtypes = [c_int64, P, c_uint64, c_uint64, P]
         L.oracle_philox4x32.argtypes = [c_int64, P, c_uint32, c_uint32, P]
+        L.oracle_philox4x32_rounds.argtypes = [c_int64, P, c_uint32, c_uint32, c_int, P]
+        L.oracle_set_philox_rounds.argtypes = [c_int]
         L.oracle_contains.argtypes = [P, P]
         L.oracle_contains.restype = c_int
         L.oracle_set_sigma_bar.argtypes = [c_double]
@@ -112,7 +114,7 @@ def default_threads():
 
 
 def walk_rows(problem, points, point_ids, traj_ids, signs, *, seed, eps, max_steps, native=False,
-              nthreads=None, sigma_bar=0.0):
+              nthreads=None, sigma_bar=0.0, philox_rounds=10):
     """(values, steps, hits) like walker.walk_poisson_values (reference form by default).
 
     Screened problems walk by delta tracking with majorant ``sigma_bar``
@@ -120,6 +122,7 @@ def walk_rows(problem, points, point_ids, traj_ids, signs, *, seed, eps, max_ste
     """
     lib = load()
     lib.oracle_set_sigma_bar(float(sigma_bar))
+    lib.oracle_set_philox_rounds(int(philox_rounds))
     pr = _Problems([problem])
     pts = np.ascontiguousarray(np.asarray(points, np.float64))
     n = pts.shape[0]
@@ -137,10 +140,12 @@ def walk_rows(problem, points, point_ids, traj_ids, signs, *, seed, eps, max_ste
 
 
 def estimate(problems, points, L, *, seed, eps, max_steps, point_ids=None, inst_index=None,
-             traj_start=0, antithetic=False, native=False, nthreads=None, sigma_bar=0.0):
+             traj_start=0, antithetic=False, native=False, nthreads=None, sigma_bar=0.0,
+             philox_rounds=10):
     """(mean, m2, total_steps) like estimator.estimate (two-pass moments per point)."""
     lib = load()
     lib.oracle_set_sigma_bar(float(sigma_bar))
+    lib.oracle_set_philox_rounds(int(philox_rounds))
     if not isinstance(problems, (list, tuple)) or (isinstance(problems, tuple) and len(problems) == 8
                                                    and isinstance(problems[0], int)):
         problems = [problems]
@@ -182,11 +187,12 @@ def philox4x64(ctr, k0, k1):
     return out
 
 
-def philox4x32(ctr, k0, k1):
+def philox4x32(ctr, k0, k1, rounds=10):
     lib = load()
     c = np.ascontiguousarray(np.asarray(ctr, np.uint32).reshape(-1, 4))
     out = np.empty_like(c)
-    lib.oracle_philox4x32(c.shape[0], c.ctypes.data, int(k0) & MASK32, int(k1) & MASK32, out.ctypes.data)
+    lib.oracle_philox4x32_rounds(c.shape[0], c.ctypes.data, int(k0) & MASK32, int(k1) & MASK32,
+                                 int(rounds), out.ctypes.data)
     return out
 
 
@@ -213,10 +219,10 @@ def philox4x64_int(counter, key):
     return x
 
 
-def philox4x32_int(counter, key):
+def philox4x32_int(counter, key, rounds=10):
     x = [int(v) & MASK32 for v in counter]
     k0, k1 = (int(v) & MASK32 for v in key)
-    for _ in range(10):
+    for _ in range(rounds):
         p0 = 0xD2511F53 * x[0]
         p1 = 0xCD9E8D57 * x[2]
         x = [((p1 >> 32) ^ x[1] ^ k0) & MASK32, p1 & MASK32, ((p0 >> 32) ^ x[3] ^ k1) & MASK32,
@@ -242,3 +248,23 @@ PHILOX4X32_KAT = [
     ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
      (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
 ]
+
+
+def median3_grid_moments(bits):
+    """Exact (E[t], E[t^2]) of t = the median of three iid uniform ``bits``-bit integers,
+    midpoint-rounded to (k + 1/2) 2^-bits: the NATIVE 3D source jump's Beta(2,2) radius
+    fraction (wos_walk.cuh f_top12 / umed3). P(med <= k) = 3 F^2 - 2 F^3 with
+    F = (k + 1) 2^-bits; exact rational arithmetic."""
+    from fractions import Fraction
+
+    n = 1 << bits
+    e1 = e2 = Fraction(0)
+    prev = Fraction(0)
+    for k in range(n):
+        F = Fraction(k + 1, n)
+        G = 3 * F * F - 2 * F * F * F
+        t = Fraction(2 * k + 1, 2 * n)
+        e1 += t * (G - prev)
+        e2 += t * t * (G - prev)
+        prev = G
+    return float(e1), float(e2)

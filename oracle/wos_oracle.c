@@ -66,10 +66,14 @@ void oracle_philox4x64(int64_t n, const uint64_t* ctr, uint64_t k0, uint64_t k1,
   for (int64_t i = 0; i < n; ++i) philox4x64(ctr + 4 * i, k0, k1, out + 4 * i);
 }
 
-/* Philox 4x32-10 (Random123 constants) — the NATIVE_F32 generator. */
-static void philox4x32(const uint32_t c[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+/* Philox 4x32-R (Random123 constants) — the NATIVE_F32 generator: R = 10 rounds by
+ * default, 7 when WalkConfig.philox_rounds = 7 (oracle_set_philox_rounds). */
+static int g_native_rounds = 10;
+void oracle_set_philox_rounds(int r) { g_native_rounds = r; }
+
+static void philox4x32_r(const uint32_t c[4], uint32_t k0, uint32_t k1, int rounds, uint32_t out[4]) {
   uint32_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < rounds; ++r) {
     uint64_t p0 = (uint64_t)0xD2511F53u * x0;
     uint64_t p1 = (uint64_t)0xCD9E8D57u * x2;
     uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
@@ -82,8 +86,18 @@ static void philox4x32(const uint32_t c[4], uint32_t k0, uint32_t k1, uint32_t o
   out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
 }
 
+/* the NATIVE stream's block: g_native_rounds rounds */
+static void philox4x32(const uint32_t c[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+  philox4x32_r(c, k0, k1, g_native_rounds, out);
+}
+
 void oracle_philox4x32(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
-  for (int64_t i = 0; i < n; ++i) philox4x32(ctr + 4 * i, k0, k1, out + 4 * i);
+  for (int64_t i = 0; i < n; ++i) philox4x32_r(ctr + 4 * i, k0, k1, 10, out + 4 * i);
+}
+
+void oracle_philox4x32_rounds(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, int rounds,
+                              uint32_t* out) {
+  for (int64_t i = 0; i < n; ++i) philox4x32_r(ctr + 4 * i, k0, k1, rounds, out + 4 * i);
 }
 
 static double u53(uint64_t w) { return (double)(w >> 11) * 1.1102230246251565e-16; }
@@ -674,10 +688,13 @@ void oracle_native_keys(uint64_t seed, uint64_t ikey, uint32_t* k0, uint32_t* k1
   *k1 = (uint32_t)(seed >> 32) ^ (uint32_t)ikey ^ ((uint32_t)(ikey >> 32) * 0x9E3779B9u);
 }
 
-static double med3(double a, double b, double c) {
-  double lo = fmin(a, b), hi = fmax(a, b);
-  return fmax(lo, fmin(hi, c));
+static uint32_t umed3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+  uint32_t m = hi < c ? hi : c;
+  return lo > m ? lo : m;
 }
+/* low 20 bits, midpoint-rounded: (b + 1/2) 2^-20 */
+static double u20(uint32_t w) { return ((double)(w & 0xFFFFFu) + 0.5) * (1.0 / 1048576.0); }
 
 static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
                             double sgn, uint64_t seed, double eps, int64_t max_steps,
@@ -737,27 +754,22 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[1] = s * sin(phi);
       dir[2] = z;
     } else {
-      /* seven uniforms from the block's 128 bits (wos_walk.cuh native_uniforms7):
-         v[0..3] = top 23 bits of each word; v[4..6] = 12-bit fields (9 low bits of
-         u[0..2] and 3 bits of u[3]), midpoint-rounded (b + 1/2) 2^-12 */
-      double v[7];
-      for (int k = 0; k < 4; ++k) v[k] = u23(u[k]);
-      uint32_t b4 = ((u[0] & 0x1FFu) << 3) | (u[3] & 0x7u);
-      uint32_t b5 = ((u[1] & 0x1FFu) << 3) | ((u[3] >> 3) & 0x7u);
-      uint32_t b6 = ((u[2] & 0x1FFu) << 3) | ((u[3] >> 6) & 0x7u);
-      v[4] = ((double)b4 + 0.5) * (1.0 / 4096.0);
-      v[5] = ((double)b5 + 0.5) * (1.0 / 4096.0);
-      v[6] = ((double)b6 + 0.5) * (1.0 / 4096.0);
-      double z = 2.0 * v[0] - 1.0;
+      /* seven uniforms from the block's 128 bits (wos_walk.cuh f20 / f_top12 / umed3):
+         the Beta(2,2) radius fraction is the median of the words u[0..2] reduced to
+         their top 12 bits (the median commutes with x >> 20), midpoint-rounded
+         (b + 1/2) 2^-12; z, phi, z' are the low 20 bits of u[0], u[1], u[2]
+         (midpoint-rounded); phi' the top 23 bits of u[3] */
+      double z = 2.0 * u20(u[0]) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
-      double phi = TWO_PI * v[1] - PI;
+      double phi = TWO_PI * u20(u[1]) - PI;
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;
-      double vz = 2.0 * v[2] - 1.0;
+      double vz = 2.0 * u20(u[2]) - 1.0;
       double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
-      double vphi = TWO_PI * v[3] - PI;
-      double r = d * med3(v[4], v[5], v[6]);
+      double vphi = TWO_PI * u23(u[3]) - PI;
+      double t = ((double)(umed3(u[0], u[1], u[2]) >> 20) + 0.5) * (1.0 / 4096.0);
+      double r = d * t;
       double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
                      x[2] + sgn * r * vz};
       acc -= (d * d * (1.0 / 6.0)) * source(pb, g);

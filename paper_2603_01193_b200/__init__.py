@@ -11,7 +11,8 @@ reference CLI's solve / bench files (run stamp, CSV, summary) from GPU estimates
 
 from . import artifacts
 from .cache import CacheShapeError, EstimateCache, cache_update, export_csv
-from .estimator import PointEstimate, chan_merge, estimate, estimate_arrays, estimate_tensors
+from .estimator import (PointEstimate, WelfordAccumulator, chan_merge, estimate, estimate_arrays,
+                        estimate_tensors)
 from .engine import UnsupportedProblemError
 from .geometry import (
     BallDomain,
@@ -48,6 +49,7 @@ __all__ = [
     "ExteriorQueryError",
     "MajorantViolationError",
     "PointEstimate",
+    "WelfordAccumulator",
     "MeshDomain",
     "PolarDomain",
     "PolygonDomain",

@@ -79,6 +79,8 @@ class WosWalkConfig(ctypes.Structure):
         ("mode", c_int32),
         ("rng_seed", c_uint64),
         ("sigma_bar", c_double),
+        ("philox_rounds", c_int32),
+        ("reserved", c_int32),
     ]
 
 
@@ -111,6 +113,7 @@ _SIGNATURES = {
     "wos_context_exterior": (c_int32, [_P, _P, POINTER(c_int64)]),
     "wos_context_majorant": (c_int32, [_P, _P, POINTER(c_double)]),
     "wos_context_status": (c_int32, [_P, _P, POINTER(c_int64), POINTER(c_uint32), POINTER(c_double)]),
+    "wos_context_counters": (c_int32, [_P, _P, POINTER(c_uint64), POINTER(c_uint64)]),
     "wos_cache_fold": (
         c_int32,
         [_P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P],
@@ -123,6 +126,7 @@ _SIGNATURES = {
     ),
     "wos_philox4x64": (c_int32, [_P, c_int64, _P, c_uint64, c_uint64, _P, _P]),
     "wos_philox4x32": (c_int32, [_P, c_int64, _P, c_uint32, c_uint32, _P, _P]),
+    "wos_philox4x32_rounds": (c_int32, [_P, c_int64, _P, c_uint32, c_uint32, c_int32, _P, _P]),
     "wos_set_tuning": (c_int32, [_P, c_int32, c_int32]),
     "wos_set_refill_deferred": (c_int32, [_P, c_int32]),
     "wos_fastmath_probe": (c_int32, [_P, c_int64, _P, _P, _P, _P, _P, _P]),

@@ -32,6 +32,8 @@ UNITS = {
     "wos_kernels_native.cu": [],
     "wos_kernels_native_est.cu": [],
     "wos_kernels_native_est_bc.cu": [],
+    "wos_kernels_native_est_r7.cu": [],
+    "wos_kernels_native_est_bc_r7.cu": [],
     "wos_kernels_native_rows.cu": [],
     "wos_kernels_replay_f64.cu": ["--fmad=false"],
     "wos_kernels_replay_f32.cu": ["--fmad=false"],

@@ -280,7 +280,7 @@ class EstimateCache:
         if screened and (cfg.sigma_bar is None or cfg.sigma_bar <= 0.0):
             raise ValueError("delta tracking requires a positive cfg.sigma_bar")
         wc = walk_config_struct(cfg.resolve_eps(problem.domain), cfg.max_steps, cfg.antithetic,
-                                cfg.mode, cfg.rng_seed, cfg.sigma_bar)
+                                cfg.mode, cfg.rng_seed, cfg.sigma_bar, philox_rounds=cfg.philox_rounds)
         ms, cn, cm, c2 = self._state
         if total_steps is None:
             total_steps = torch.zeros(1, dtype=torch.int64, device=dev)

@@ -83,6 +83,7 @@ extern "C" int wos_cache_fold(wos_context* ctx, int64_t n_fresh, const int64_t* 
       n_fresh, slot, fresh_mean, fresh_m2, fresh_n, fresh_n_all, mean_sum, n, mean, m2);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return wos_fail(WOS_ERR_CUDA, cudaGetErrorString(e));
+  wos_context_count_launch(ctx);
   return WOS_OK;
 }
 
@@ -98,5 +99,6 @@ extern "C" int wos_cache_targets(wos_context* ctx, int64_t n_keys, const double*
       n_keys, mean_sum, (double)epoch, out);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return wos_fail(WOS_ERR_CUDA, cudaGetErrorString(e));
+  wos_context_count_launch(ctx);
   return WOS_OK;
 }

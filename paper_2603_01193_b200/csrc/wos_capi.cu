@@ -76,6 +76,11 @@ struct wos_context {
   unsigned long long* d_majorant = nullptr;  // = d_status + 1
   unsigned int* d_watchdog = nullptr;        // = (unsigned*)(d_status + 2)
   unsigned long long* d_steps = nullptr;     // total-steps scratch of the *_host variants
+  // measurement counters (wos_context_counters): kernels this library launched, and
+  // the segment distances NATIVE polygon walks evaluated (the measured FP32 work of a
+  // candidate-grid query)
+  std::atomic<unsigned long long> n_launches{0};
+  unsigned long long* d_perf = nullptr;
   // per-kernel launch attributes (dynamic shared memory set, occupancy at that size):
   // computed on the first launch of a (kernel, smem) pair instead of every launch
   std::unordered_map<const void*, std::pair<size_t, int>> launch_cache;
@@ -129,6 +134,19 @@ int wos_fail(int code, const char* fmt, ...) {
   return code;
 }
 int wos_context_device(const wos_context* c) { return c->device; }
+void wos_context_count_launch(wos_context* c) { c->n_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" int wos_context_counters(wos_context* c, void* stream, uint64_t* out_launches,
+                                    uint64_t* out_seg_evals) {
+  if (!c) return fail(WOS_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, c->d_perf, sizeof(v), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  if (out_launches) *out_launches = c->n_launches.load();
+  if (out_seg_evals) *out_seg_evals = v;
+  return WOS_OK;
+}
 
 extern "C" int wos_abi_version(void) { return WOS_ABI_VERSION; }
 extern "C" const char* wos_last_error(void) { return g_err; }
@@ -166,6 +184,8 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->d_status, kStatusBytes);
   if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, kStatusBytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_perf, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_perf, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) {
     c->d_exterior = c->d_status;
     c->d_majorant = c->d_status + 1;
@@ -185,6 +205,7 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_counters);
   cudaFree(c->d_status);
   cudaFree(c->d_steps);
+  cudaFree(c->d_perf);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1202,6 +1223,7 @@ static int launch_interior(wos_context* c, const wos_problem_set* s, int64_t n, 
                                               s->d_segs_d, s->dim, s->dom_kind, c->d_exterior, idx_base,
                                               s->d_mesh_nodes_d, s->d_mesh_tris_d, s->d_mesh_fnorm);
   CUDA_TRY(cudaGetLastError());
+  wos_context_count_launch(c);
   return WOS_OK;
 }
 
@@ -1314,7 +1336,7 @@ struct KernelInfo {
   bool one;     // single-instance NATIVE launch (parameters in the constant bank)
 };
 
-static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
+static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int rounds) {
   KernelInfo k{nullptr, 8, false};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
@@ -1326,7 +1348,7 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows) {
   } else {
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
     k.one = (s->n == 1 && s->stride <= kCP);
-    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows, s->bnd_kind == WOS_BND_CONST);
+    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows, s->bnd_kind == WOS_BND_CONST, rounds);
     k.elem = 4;
   }
   return k;
@@ -1343,7 +1365,10 @@ static size_t smem_bytes(size_t stage, size_t elem) {
 
 static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
                        KArgs a, cudaStream_t st) {
-  const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS);
+  const int rounds = cfg->philox_rounds == 0 ? kPhiloxRoundsDefault : cfg->philox_rounds;
+  if (cfg->mode == WOS_MODE_NATIVE_F32 && rounds != kPhiloxRoundsDefault && rounds != kPhiloxRoundsFast)
+    return fail(WOS_ERR_INVALID, "philox_rounds must be %d or %d", kPhiloxRoundsDefault, kPhiloxRoundsFast);
+  const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS, rounds);
   bool scaled = false;  // the walk runs in X = pi x (see below)
   if (!k.fn)
     return fail(WOS_ERR_UNSUPPORTED, "no kernel for dim %d domain %d source %d mode %d", s->dim,
@@ -1426,6 +1451,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
                   s->scr_sprime_max, cfg->sigma_bar);
     }
   }
+  a.philox_rounds = rounds;
   a.sigma_bar = cfg->sigma_bar;
   a.sqrt_sig = sqrt(cfg->sigma_bar > 0.0 ? cfg->sigma_bar : 0.0);
   a.majorant = c->d_majorant;
@@ -1457,7 +1483,9 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.iter_limit = (uint32_t)std::min<int64_t>(0xffffffffll, std::max<int64_t>(1ll << 27, 4 * (int64_t)a.max_steps));
   CUDA_TRY(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned), st));
   void* args[] = {&a};
+  a.seg_evals = c->d_perf;
   CUDA_TRY(cudaLaunchKernel(k.fn, dim3((unsigned)grid), dim3(kBlock), args, smem, st));
+  wos_context_count_launch(c);
   return WOS_OK;
 }
 
@@ -1596,6 +1624,7 @@ static int estimate_impl(wos_context* c, const wos_problem_set* s, const wos_wal
                                                       cfg->antithetic ? 1 : 0, partials,
                                                       out_mean + off, out_m2 + off);
       CUDA_TRY(cudaGetLastError());
+      wos_context_count_launch(c);
     }
   }
   if (partials) CUDA_TRY(cudaFreeAsync(partials, st));
@@ -1809,9 +1838,11 @@ __global__ void philox64_kernel(int64_t n, const uint64_t* ctr, uint64_t k0, uin
     for (int j = 0; j < 4; ++j) out[4 * i + j] = w[j];
   }
 }
-__global__ void philox32_kernel(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
+__global__ void philox32_kernel(int64_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, int rounds,
+                                uint32_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 w = philox4x32(make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]), k0, k1);
+    const uint4 w =
+        philox4x32(make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]), k0, k1, rounds);
     out[4 * i] = w.x;
     out[4 * i + 1] = w.y;
     out[4 * i + 2] = w.z;
@@ -1836,7 +1867,19 @@ extern "C" int wos_philox4x32(wos_context* c, int64_t n, const uint32_t* ctr, ui
   if (n <= 0) return WOS_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
-  philox32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ctr, k0, k1, out);
+  philox32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ctr, k0, k1, kPhiloxRoundsDefault, out);
+  CUDA_TRY(cudaGetLastError());
+  return WOS_OK;
+}
+
+extern "C" int wos_philox4x32_rounds(wos_context* c, int64_t n, const uint32_t* ctr, uint32_t k0,
+                                     uint32_t k1, int32_t rounds, uint32_t* out, void* stream) {
+  if (!c) return fail(WOS_ERR_INVALID, "null context");
+  if (rounds < 1 || rounds > 16) return fail(WOS_ERR_INVALID, "rounds must be in 1..16");
+  if (n <= 0) return WOS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  philox32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n, ctr, k0, k1, rounds, out);
   CUDA_TRY(cudaGetLastError());
   return WOS_OK;
 }

@@ -6,9 +6,14 @@ namespace wos {
 const void* get_kernel_native_est(int dim, int dom, int src, int sk, bool one);
 const void* get_kernel_native_rows(int dim, int dom, int src, int sk, bool one);
 const void* get_kernel_native_est_bc(int dim, int dom, int src, int sk, bool one);
+const void* get_kernel_native_est_r7(int dim, int dom, int src, int sk, bool one);
+const void* get_kernel_native_est_bc_r7(int dim, int dom, int src, int sk, bool one);
 
-const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const) {
+const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const,
+                              int rounds) {
   if (rows) return get_kernel_native_rows(dim, dom, src, sk, one);
+  if (one && rounds == kPhiloxRoundsFast)
+    return bnd_const ? get_kernel_native_est_bc_r7(dim, dom, src, sk, one) : get_kernel_native_est_r7(dim, dom, src, sk, one);
   if (one && bnd_const) return get_kernel_native_est_bc(dim, dom, src, sk, one);
   return get_kernel_native_est(dim, dom, src, sk, one);
 }

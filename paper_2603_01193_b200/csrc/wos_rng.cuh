@@ -5,16 +5,13 @@
 // round (x0,x1,x2,x3) <- (hi(M1 x2)^x1^k0, lo(M1 x2), hi(M0 x0)^x3^k1, lo(M0 x0)),
 // key bumped after each round. Used by the REPLAY modes.
 //
-// Philox4x32-10 (Random123 constants) drives the NATIVE_F32 mode: 32-bit
-// multiplies map to one IMAD.WIDE.U32 each, a 3-input XOR to one LOP3.
+// Philox4x32 (Random123 constants) drives the NATIVE_F32 mode: 32-bit multiplies
+// map to one IMAD.WIDE.U32 each, a 3-input XOR to one LOP3. 10 rounds by default,
+// 7 on request (kPhiloxRoundsFast below).
 #pragma once
 #include <stdint.h>
 
 namespace wos {
-
-#ifndef WOS_PHILOX_R
-#define WOS_PHILOX_R 10
-#endif
 
 __device__ __forceinline__ void philox4x64(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
                                            uint64_t k0, uint64_t k1, uint64_t out[4]) {
@@ -42,15 +39,23 @@ __device__ __forceinline__ double u01_53(uint64_t w) {
   return (double)(w >> 11) * 1.1102230246251565e-16;
 }
 
-__device__ __forceinline__ uint4 philox4x32(uint4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    uint64_t p0 = (uint64_t)M0 * c.x;  // IMAD.WIDE.U32
-    uint64_t p1 = (uint64_t)M1 * c.z;
-    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+// One Philox4x32 round with round key (k0, k1).
+__device__ __forceinline__ void philox4x32_round(uint4& c, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint64_t p0 = (uint64_t)M0 * c.x;  // IMAD.WIDE.U32
+  const uint64_t p1 = (uint64_t)M1 * c.z;
+  c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0);
+}
+
+// Round counts of the NATIVE stream: 10 (Random123's default, the production stream)
+// or 7 (opt-in: the fewest rounds Random123 reports Crush-resistant for Philox4x32,
+// WalkConfig.philox_rounds = 7). Rounds 7..9 sit behind one kernel-uniform branch.
+constexpr int kPhiloxRoundsDefault = 10;
+constexpr int kPhiloxRoundsFast = 7;
+
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint32_t k0, uint32_t k1, int rounds = 10) {
+  for (int r = 0; r < rounds; ++r) {
+    philox4x32_round(c, k0, k1);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
@@ -59,15 +64,12 @@ __device__ __forceinline__ uint4 philox4x32(uint4 c, uint32_t k0, uint32_t k1) {
 
 // Same with a precomputed round-key schedule (rk0[r] = k0 + r W0, rk1[r] = k1 + r W1).
 // With the schedule in the kernel parameters the XORs take c[] operands directly.
-__device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const uint32_t* rk0, const uint32_t* rk1) {
+__device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const uint32_t* rk0, const uint32_t* rk1, int rounds) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    uint64_t p0 = (uint64_t)M0 * c.x;
-    uint64_t p1 = (uint64_t)M1 * c.z;
-    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    c = make_uint4(hi1 ^ c.y ^ rk0[r], lo1, hi0 ^ c.w ^ rk1[r], lo0);
+  for (int r = 0; r < kPhiloxRoundsFast; ++r) philox4x32_round(c, rk0[r], rk1[r]);
+  if (rounds > kPhiloxRoundsFast) {
+#pragma unroll
+    for (int r = kPhiloxRoundsFast; r < kPhiloxRoundsDefault; ++r) philox4x32_round(c, rk0[r], rk1[r]);
   }
   return c;
 }
@@ -100,34 +102,35 @@ __device__ __forceinline__ uint4 philox_pre_r01(uint32_t c0, const PhiloxPre& p)
 }
 
 __device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t c0, const PhiloxPre& p, const uint32_t* rk0,
-                                                   const uint32_t* rk1) {
+                                                   const uint32_t* rk1, int rounds) {
   uint4 c = philox_pre_r01(c0, p);
 #pragma unroll
-  for (int r = 2; r < WOS_PHILOX_R; ++r) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    uint64_t p0 = (uint64_t)M0 * c.x;
-    uint64_t p1 = (uint64_t)M1 * c.z;
-    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    c = make_uint4(hi1 ^ c.y ^ rk0[r], lo1, hi0 ^ c.w ^ rk1[r], lo0);
+  for (int r = 2; r < kPhiloxRoundsFast; ++r) philox4x32_round(c, rk0[r], rk1[r]);
+  if (rounds > kPhiloxRoundsFast) {
+#pragma unroll
+    for (int r = kPhiloxRoundsFast; r < kPhiloxRoundsDefault; ++r) philox4x32_round(c, rk0[r], rk1[r]);
   }
   return c;
 }
 
-__device__ __forceinline__ uint4 philox4x32_pre(uint32_t c0, const PhiloxPre& p, uint32_t k0, uint32_t k1) {
+__device__ __forceinline__ uint4 philox4x32_pre(uint32_t c0, const PhiloxPre& p, uint32_t k0, uint32_t k1,
+                                                int rounds) {
   uint4 c = philox_pre_r01(c0, p);
   k0 += 2u * 0x9E3779B9u;
   k1 += 2u * 0xBB67AE85u;
 #pragma unroll
-  for (int r = 2; r < 10; ++r) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    uint64_t p0 = (uint64_t)M0 * c.x;
-    uint64_t p1 = (uint64_t)M1 * c.z;
-    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  for (int r = 2; r < kPhiloxRoundsFast; ++r) {
+    philox4x32_round(c, k0, k1);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
+  }
+  if (rounds > kPhiloxRoundsFast) {
+#pragma unroll
+    for (int r = kPhiloxRoundsFast; r < kPhiloxRoundsDefault; ++r) {
+      philox4x32_round(c, k0, k1);
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
   }
   return c;
 }

@@ -129,6 +129,8 @@ struct KArgs {
   double sqrt_sig;             // sqrt(sigma_bar)
   unsigned long long* majorant;  // max violating sigma' seen (fp64 bits), 0 = none
   uint32_t iter_limit;         // max(2^27, 4 * max_steps) loop iterations per warp
+  int32_t philox_rounds;       // NATIVE: Philox4x32 rounds per block (10, or 7 on request)
+  unsigned long long* seg_evals;  // NATIVE polygons: segment distances evaluated (or null)
   // ---- single-instance NATIVE launches: the instance row and the Philox round
   // keys live in the kernel-parameter constant bank (FFMA / LOP3 c[] operands) ----
   uint32_t rk0[10];

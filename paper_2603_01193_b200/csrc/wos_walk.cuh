@@ -31,9 +31,10 @@
 //   NATIVE_F32 samples the source term from the ball Green's function
 //   (radius d*sqrt(U1 U2) in 2D, d*Beta(2,2) as the median of three uniforms in
 //   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
-//   and ONE Philox4x32-10 block per jump (counter (2*step, pid, tid, hi-words));
+//   and ONE Philox4x32 block per jump (counter (2*step, pid, tid, hi-words); 10
+//   rounds, or 7 with WalkConfig.philox_rounds = 7);
 //   the 3D source jump needs 7 uniforms and takes them as bit fields of the
-//   block's 128 bits (native_uniforms7 below; oracle/wos_oracle.c restates it);
+//   block's 128 bits (f20 / f_top12 / umed3 below; oracle/wos_oracle.c restates it);
 //   source-free jumps share a block between 4 (2D) / 2 (3D) consecutive jumps
 //   (kPerBlock; phase-locked amortised rounds on closed-form domains). Direction
 //   angles are 2 pi u - pi (MUFU's accurate range). Single-instance NATIVE launches
@@ -107,35 +108,43 @@ __device__ __forceinline__ float pmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double pabs(double a) { return fabs(a); }
 __device__ __forceinline__ float pabs(float a) { return fabsf(a); }
 
-// 12-bit field (already in mantissa bits 22..11) with midpoint rounding: 1 + (b + 1/2) 2^-12
-__device__ __forceinline__ float f12_m12(uint32_t mant) {
-  return __uint_as_float(0x3f800400u | (mant & 0x007FF800u));
+// The 3D source jump's seven uniforms from one Philox4x32 block W (128 bits):
+//   radius fraction t ~ Beta(2,2) = the median of three uniforms, taken as the median
+//     of the raw words W.x, W.y, W.z: x -> x >> 20 is monotone, so med(W) >> 20 is the
+//     median of their top-12-bit fields, i.e. of three independent 12-bit uniforms, and
+//     t = (field + 1/2) 2^-12 (midpoint rounding: a 12-bit grid perturbs E[h(t)] by
+//     O(2^-24 h''); tests/test_gpu_native.py measures the moments). It depends on the
+//     words' top 12 bits only;
+//   z (move), phi (move), z' (volume sample) = the low 20 bits of W.x, W.y, W.z,
+//     midpoint-rounded (b + 1/2) 2^-20: independent of t;
+//   phi' (volume sample) = the top 23 bits of W.w.
+// Integer median (min3 / max3 / xor) and two ops per 20-bit field replace the float
+// median of bit-assembled fields (19 -> 13 instructions, no IMAD.SHL on the FMA-heavy
+// pipe for the fields). oracle/wos_oracle.c walk_native_one restates this layout.
+__device__ __forceinline__ uint32_t umed3(uint32_t a, uint32_t b, uint32_t c) {
+  // {a, b, c} = {min, med, max} as a multiset, so a ^ b ^ c = min ^ med ^ max
+  return a ^ b ^ c ^ min(min(a, b), c) ^ max(max(a, b), c);
 }
-
-// Seven uniforms from one Philox4x32 block W[0..3] (3D jump with a source term):
-//   f[k], k < 4 : top 23 bits of W[k]                      (1 + b 2^-23)
-//   f[4] : W[0] bits 0..8 . W[3] bits 0..2                  (1 + (b + 1/2) 2^-12)
-//   f[5] : W[1] bits 0..8 . W[3] bits 3..5
-//   f[6] : W[2] bits 0..8 . W[3] bits 6..8
-// f[4..6] only feed the median of three (the Beta(2,2) radius fraction); with
-// midpoint rounding a 12-bit grid perturbs E[h(t)] by O(2^-24 h'').
-__device__ __forceinline__ void native_uniforms7(uint4 W, float f[7]) {
-  f[0] = f12(W.x);
-  f[1] = f12(W.y);
-  f[2] = f12(W.z);
-  f[3] = f12(W.w);
-  f[4] = f12_m12((W.x << 14) | ((W.w << 11) & 0x3800u));
-  f[5] = f12_m12((W.y << 14) | ((W.w << 8) & 0x3800u));
-  f[6] = f12_m12((W.z << 14) | ((W.w << 5) & 0x3800u));
+// low 20 bits as 1 + (b + 1/2) 2^-20 in [1, 2) (exponent e: 0x3f8 -> [1, 2), 0x400 -> [2, 4))
+// (mask, then shift-and-add: LOP3 + LEA, no second immediate for a LOP3 to need)
+__device__ __forceinline__ float f20(uint32_t w, uint32_t expo = 0x3f800000u) {
+  return __uint_as_float(((w & 0x000fffffu) << 3) + (expo | 4u));
+}
+// the top 12 bits of w as 1 + (b + 1/2) 2^-12 (LOP3 + LEA.HI)
+__device__ __forceinline__ float f_top12(uint32_t w) {
+  return __uint_as_float(((w & 0xfff00000u) >> 9) + 0x3f800400u);
 }
 
 // BC_: single-instance launch of a problem whose boundary value is a constant
 // (a.bnd_c): the walk value is acc + g with no projection, so the kernel carries
 // no deferred-recording code (it only costs registers and issue there)
+// RND_: NATIVE Philox4x32 rounds fixed at compile time (the single-instance estimate
+// kernels are built for 10 and for 7); 0 = read KArgs::philox_rounds at run time
 template <int MODE_, int DIM_, int DOM_, int SRC_, int SK_, bool ONE_ = false, int SINK_ = SINK_ESTIMATE,
-          bool BC_ = false>
+          bool BC_ = false, int RND_ = 0>
 struct Spec {
   static constexpr int MODE = MODE_, DIM = DIM_, DOM = DOM_, SRC = SRC_, SK = SK_, SINK = SINK_;
+  static constexpr int RND = RND_;
   static constexpr bool NATIVE = (MODE_ == MODE_NATIVE_F32);
   static constexpr bool ONE = ONE_;
   static constexpr bool BC = BC_;
@@ -183,6 +192,7 @@ struct Walker {
     uint32_t k1;               // NATIVE multi-instance: the instance key
     int32_t seg_off, n_seg, rec_off;
     int32_t seg_i;  // polygon: nearest segment found by the last distance query
+    uint32_t nseg = 0;  // NATIVE polygon: segment distances evaluated (work counter)
     Real thr;       // delta tracking: throughput (walker.py:365, _kernels.py:539)
     Real sa;        // delta tracking: sqrt(alpha) at the start point (walker.py:352-354)
     // single-instance NATIVE launches: the Philox round keys and the parameters the
@@ -334,7 +344,7 @@ struct Walker {
   // segment pairs; records the exact first nearest segment
   __device__ static __forceinline__ float poly_grid_scan(const float4* __restrict__ R, float4 H0, int G, int cells_off,
                                                          int idx_off, bool bytes8, const uint32_t* __restrict__ gw,
-                                                         float px, float py, int* bi_out) {
+                                                         float px, float py, int* bi_out, uint32_t* n_pairs) {
     const int cx = min(max((int)((px - H0.x) * H0.z), 0), G - 1);
     const int cy = min(max((int)((py - H0.y) * H0.w), 0), G - 1);
     const uint16_t* idx = reinterpret_cast<const uint16_t*>(gw) + idx_off;
@@ -346,6 +356,7 @@ struct Walker {
     // index load of their own
     const uint4 C = __ldg(reinterpret_cast<const uint4*>(gw + cells_off) + cy * G + cx);
     const uint32_t e = bytes8 ? (C.x & 0xFFFFu) : C.y;
+    *n_pairs = e;
     const uint8_t* idx8 = reinterpret_cast<const uint8_t*>(idx);
     for (uint32_t k = 0; k < e; ++k) {
       int j;
@@ -359,6 +370,7 @@ struct Walker {
 #else
     const uint32_t* cell = gw + cells_off + cy * G + cx;
     const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
+    *n_pairs = e - b;
     for (uint32_t k = b; k < e; ++k) {
       const int j = __ldg(idx + k);
 #endif
@@ -384,10 +396,13 @@ struct Walker {
       const float4 H1 = R[-1];
       const int G = __float_as_int(H1.x);
       if (G > 0) {  // (sets with grids are never staged: R is global)
+        uint32_t np;
         best = poly_grid_scan(R, R[-2], G, __float_as_int(H1.y), __float_as_int(H1.z), __float_as_int(H1.w) != 0,
-                              reinterpret_cast<const uint32_t*>(a.nodes), l.x[0], l.x[1], &bi);
+                              reinterpret_cast<const uint32_t*>(a.nodes), l.x[0], l.x[1], &bi, &np);
+        l.nseg += 2u * np;
       } else {  // R: shared memory when staged, else global
         best = poly_scan(R, l.n_seg, l.x[0], l.x[1], &bi);
+        l.nseg += (uint32_t)(((l.n_seg + 1) >> 1) << 1);
       }
       l.seg_i = bi;
       return fast_sqrt(best);
@@ -1325,15 +1340,16 @@ struct Walker {
     return native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)kPerBlock));
   }
   __device__ static __forceinline__ uint4 native_block_at(const Lane& l, const KArgs& a, uint32_t c0) {
+    const int rounds = S::RND ? S::RND : a.philox_rounds;
 // the hot kernels fold too since the jump-first loop made refills cheaper (cfg4 -0.7 %;
 // it had cost +1.7 % with the test-first loop)
 #ifndef WOS_HOT_FOLD
 #define WOS_HOT_FOLD 1
 #endif
-    if constexpr (kHot && WOS_HOT_FOLD) return philox4x32_rk_pre(c0, l.pc, l.hk0, l.hk1);
-    else if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1);
-    else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1);
-    else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1);
+    if constexpr (kHot && WOS_HOT_FOLD) return philox4x32_rk_pre(c0, l.pc, l.hk0, l.hk1, rounds);
+    else if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1, rounds);
+    else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1, rounds);
+    else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1, rounds);
   }
 
   // the walk's Philox counter words (c1, c2, c3) folded through rounds 0-1 (wos_rng.cuh)
@@ -1399,19 +1415,18 @@ struct Walker {
       const bool odd = (l.step & 1) != 0;
       move_native_3d(l, d, odd ? A.z : A.x, odd ? A.w : A.y);
     } else {
-      float u[7];
-      native_uniforms7(A, u);
-      // z = 2u - 1 is exact for u = f - 1 (23-bit f in [1, 2)), so fmaf(-z, z, 1) >= 0
-      const float z = f2x(A.x) - 3.0f;
+      // the seven uniforms of the block (layout above f20): z = 2u - 1 is exact for
+      // u = f - 1, so fmaf(-z, z, 1) >= 0
+      const float z = f20(A.x, 0x40000000u) - 3.0f;
       const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
       float sph, cph;
-      __sincosf(dir_angle(u[1]), &sph, &cph);
-      const float vz = f2x(A.z) - 3.0f;
+      __sincosf(dir_angle(f20(A.y)), &sph, &cph);
+      const float vz = f20(A.z, 0x40000000u) - 3.0f;
       const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
       float vsp, vcp;
-      __sincosf(dir_angle(u[3]), &vsp, &vcp);
+      __sincosf(dir_angle(f12(A.w)), &vsp, &vcp);
       // Beta(2,2) radius fraction = median of three uniforms; r = d * (med - 1)
-      const float med = fmaxf(fminf(u[4], u[5]), fminf(fmaxf(u[4], u[5]), u[6]));
+      const float med = f_top12(umed3(A.x, A.y, A.z));
       const float sr = l.sgn * fmaf(d, med, -d);
       const float srv = sr * vs;
       // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
@@ -1930,6 +1945,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                 W::start(t, table, a.hdr, a, cu_x, cu_inst, cu_pid, 0ull, 1.0);
                 cu_d = W::dist(t, a, srec);
                 cu_seg = t.seg_i;
+                l.nseg = t.nseg;  // every lane evaluated the unit's start query
               }
               if constexpr (S::NATIVE && S::ONE) {
                 // walk j0 + jj has tid = traj_start + j0 + jj (antithetic: jj even; j0 even)
@@ -2103,6 +2119,15 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lane_steps += __shfl_xor_sync(WOS_FULL, lane_steps, o);
     if (lane == 0) atomicAdd(a.total_steps, lane_steps);
+  }
+  // ---- NATIVE polygon work counter: segment distances evaluated (measured FP32 work) ----
+  if constexpr (S::NATIVE && S::DOM == DOM_POLY) {
+    if (a.seg_evals != nullptr) {
+      unsigned long long ns = l.nseg;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(WOS_FULL, ns, o);
+      if (lane == 0) atomicAdd(a.seg_evals, ns);
+    }
   }
 }
 

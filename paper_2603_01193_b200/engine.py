@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from ctypes import byref, c_double, c_int32, c_int64, c_uint32, c_void_p
+from ctypes import byref, c_double, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 
 import numpy as np
 
@@ -166,6 +166,14 @@ class Context:
                                         byref(sp)))
         return first.value, int(wd.value), sp.value
 
+    def counters(self, stream=None):
+        """(kernels launched by the library on this context, NATIVE polygon segment
+        distances evaluated), cumulative; synchronizes ``stream``."""
+        launches, segs = c_uint64(0), c_uint64(0)
+        _lib.check(self._lib.wos_context_counters(self.handle, _stream_ptr(stream), byref(launches),
+                                                  byref(segs)))
+        return int(launches.value), int(segs.value)
+
     def exterior(self, stream=None) -> int:
         first = c_int64(-1)
         _lib.check(self._lib.wos_context_exterior(self.handle, _stream_ptr(stream), byref(first)))
@@ -266,20 +274,23 @@ def problem_set(ctx: Context, problems) -> ProblemSet:
     recs = tuple(problem_record(p) for p in problems)
     key = (id(ctx), recs)
     with _pset_lock:
-        ps = _psets.get(key)
+        ps = _psets.pop(key, None)
         if ps is None:
-            if len(_psets) >= _PSET_CACHE_MAX:
-                _psets.pop(next(iter(_psets))).close()
             ps = ProblemSet(ctx, problems)
-            _psets[key] = ps
+        _psets[key] = ps  # most recently used last
+        while len(_psets) > _PSET_CACHE_MAX:
+            # least recently used: drop the cache's reference only; the set frees its
+            # device tables (ProblemSet.__del__) once no caller or thread still holds it
+            _psets.pop(next(iter(_psets)))
         return ps
 
 
 def walk_config_struct(eps: float, max_steps: int, antithetic: bool, mode, seed: int,
-                       sigma_bar=None):
+                       sigma_bar=None, philox_rounds: int = 10):
     return _lib.WosWalkConfig(
         float(eps), int(max_steps), int(bool(antithetic)), mode_code(mode),
         int(seed) & ((1 << 64) - 1), 0.0 if sigma_bar is None else float(sigma_bar),
+        int(philox_rounds), 0,
     )
 
 

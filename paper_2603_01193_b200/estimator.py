@@ -30,6 +30,7 @@ from .walker import check_screened
 
 __all__ = [
     "PointEstimate",
+    "WelfordAccumulator",
     "chan_merge",
     "estimate",
     "estimate_arrays",
@@ -48,6 +49,36 @@ def chan_merge(n1, mean1, m21, n2, mean2, m22):
     mean = mean1 + delta * (n2 / n)
     m2 = m21 + m22 + delta * delta * (n1 * n2 / n)
     return n, mean, m2
+
+
+class WelfordAccumulator:
+    """Streaming (count, mean, m2) of a sequence of samples: the reference estimator
+    module's one-pass accumulator (estimator.py:56-83), for host-side consumers of
+    walk values. ``push`` is Welford's update; ``merge`` pools another accumulator
+    with ``chan_merge``; ``variance`` is m2 / (n - 1), nan below two samples."""
+
+    __slots__ = ("n", "mean", "m2")
+
+    def __init__(self):
+        self.n, self.mean, self.m2 = 0, 0.0, 0.0
+
+    def push(self, x):
+        x = float(x)
+        self.n += 1
+        d = x - self.mean
+        self.mean += d / self.n
+        self.m2 += d * (x - self.mean)
+
+    def extend(self, values):
+        for x in np.asarray(values, dtype=np.float64).ravel().tolist():
+            self.push(x)
+
+    def merge(self, other):
+        self.n, self.mean, self.m2 = chan_merge(self.n, self.mean, self.m2, other.n, other.mean, other.m2)
+
+    @property
+    def variance(self):
+        return self.m2 / (self.n - 1) if self.n >= 2 else math.nan
 
 
 @dataclass(frozen=True)
@@ -91,7 +122,7 @@ def _estimate_one_device(device, problems, pts, pids, inst, L, cfg, eps, traj_st
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
     P = pts.shape[0]
     wc = walk_config_struct(eps, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed,
-                            cfg.sigma_bar)
+                            cfg.sigma_bar, philox_rounds=cfg.philox_rounds)
     mean = np.empty(P, dtype=np.float64)
     m2 = np.empty(P, dtype=np.float64)
     steps = c_uint64(0)
@@ -242,7 +273,8 @@ def estimate_tensors(pset, points, point_ids, L, cfg, *, inst_index=None, traj_s
     if stream is None:
         stream = torch.cuda.current_stream(points.device)
     e = eps if eps is not None else cfg.eps_shell
-    wc = walk_config_struct(e, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed, cfg.sigma_bar)
+    wc = walk_config_struct(e, cfg.max_steps, cfg.antithetic, cfg.mode, cfg.rng_seed, cfg.sigma_bar,
+                            philox_rounds=cfg.philox_rounds)
     _lib.check(
         ctx._lib.wos_estimate(
             ctx.handle, pset.handle, byref(wc), P, points.data_ptr(), point_ids.data_ptr(),

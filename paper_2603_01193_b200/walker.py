@@ -64,12 +64,18 @@ class WalkConfig:
     sigma_bar: float | None = None
     rng_seed: int = 0
     mode: str = "native"
+    # NATIVE mode: Philox4x32 rounds per block. 10 (Random123's default) is the
+    # production stream; 7 (the fewest rounds Random123 reports Crush-resistant) is an
+    # opt-in faster stream. REPLAY modes ignore it.
+    philox_rounds: int = 10
 
     def __post_init__(self):
         if self.eps_shell is not None and self.eps_shell <= 0.0:
             raise ValueError("eps_shell must be positive")
         if self.max_steps < 1:
             raise ValueError("max_steps must be at least 1")
+        if self.philox_rounds not in (7, 10):
+            raise ValueError("philox_rounds must be 10 or 7")
         mode_code(self.mode)
 
     def resolve_eps(self, domain) -> float:
@@ -174,7 +180,8 @@ def walk_poisson_values(inst, points, point_ids, traj_ids, signs, cfg):
     pset = problem_set(ctx, [inst])
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
-    wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode, cfg.rng_seed)
+    wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode, cfg.rng_seed,
+                            philox_rounds=cfg.philox_rounds)
     values = np.empty(n, dtype=np.float64)
     steps = np.empty(n, dtype=np.int64)
     hits = np.empty(n, dtype=np.uint8)
@@ -209,7 +216,7 @@ def walk_screened_values(inst, points, point_ids, traj_ids, signs, cfg):
     if pts.shape[1] != pset.dim:
         raise ValueError(f"expected points of dimension {pset.dim}, got shape {pts.shape}")
     wc = walk_config_struct(cfg.resolve_eps(inst.domain), cfg.max_steps, False, cfg.mode,
-                            cfg.rng_seed, cfg.sigma_bar)
+                            cfg.rng_seed, cfg.sigma_bar, philox_rounds=cfg.philox_rounds)
     values = np.empty(n, dtype=np.float64)
     steps = np.empty(n, dtype=np.int64)
     hits = np.empty(n, dtype=np.uint8)

@@ -170,6 +170,32 @@ def test_antithetic_pair_from_origin_cancels_linear_data(gpu, mode):
 
 
 @pytest.mark.parametrize("mode", MODES)
+def test_antithetic_pair_mean_unbiased(gpu, mode):
+    """test_walker.py:229-238: antithetic pair means of the disk Poisson problem
+    (u(0) = -1/4) are unbiased."""
+    n = 50_000
+    pts = np.zeros((2 * n, 2))
+    v, _, _ = walk_poisson_values(DISK_POISSON, pts, np.zeros(2 * n), np.repeat(np.arange(n), 2),
+                                  np.tile([1.0, -1.0], n), WalkConfig(rng_seed=31, mode=mode))
+    m, se = mean_se(v.reshape(n, 2).mean(axis=1))
+    assert abs(m + 0.25) < 3.0 * se
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_antithetic_variance_reduction_on_smooth_problem(gpu, mode):
+    """test_walker.py:240-258: on smooth boundary data the mirrored pairs' means vary
+    less than the means of independent pairs at the same cost."""
+    inst = Problem(DISK, boundary_spec=specs.linear_boundary([1.0, 0.2, 0.0]))
+    n = 20_000
+    point = [0.3, 0.2]
+    cfg = WalkConfig(rng_seed=37, mode=mode)
+    plain, _, _ = run_walks(inst, point, 2 * n, cfg)
+    anti, _, _ = walk_poisson_values(inst, np.tile(point, (2 * n, 1)), np.zeros(2 * n),
+                                     np.repeat(np.arange(n), 2), np.tile([1.0, -1.0], n), cfg)
+    assert anti.reshape(n, 2).mean(axis=1).var(ddof=1) < plain.reshape(n, 2).mean(axis=1).var(ddof=1)
+
+
+@pytest.mark.parametrize("mode", MODES)
 def test_antithetic_estimate_counts_pairs(gpu, mode):
     cfg = WalkConfig(rng_seed=10, antithetic=True, mode=mode)
     (est,) = estimate(DISK_POISSON, [0.2, 0.0], 40, cfg)

@@ -157,3 +157,65 @@ class TestConfigPins:
                 lap += (w.analytic(x + e) - 2 * w.analytic(x) + w.analytic(x - e)) / h**2
             f = configs.sine_series(w.meta["a"], x)
             np.testing.assert_allclose(-lap, f, rtol=1e-4, atol=1e-6)
+
+
+def test_welford_matches_two_pass():
+    """estimator.py:56-83 (the reference's test_estimator.py:67-73)."""
+    from paper_2603_01193_b200 import WelfordAccumulator
+
+    v = np.random.default_rng(1).lognormal(mean=2.0, sigma=1.5, size=10_000)
+    acc = WelfordAccumulator()
+    acc.extend(v)
+    assert acc.n == v.size
+    assert acc.mean == pytest.approx(v.mean(), rel=1e-10)
+    assert acc.variance == pytest.approx(v.var(ddof=1), rel=1e-10)
+    one = WelfordAccumulator()
+    one.push(2.5)
+    assert one.mean == 2.5 and np.isnan(one.variance)
+
+
+def test_welford_merge_matches_pooled():
+    """The reference's test_estimator.py:75-85: merging equals pooling the samples."""
+    from paper_2603_01193_b200 import WelfordAccumulator
+
+    rng = np.random.default_rng(2)
+    a, b = rng.normal(size=300), rng.normal(loc=5.0, size=700)
+    left, right = WelfordAccumulator(), WelfordAccumulator()
+    left.extend(a)
+    right.extend(b)
+    left.merge(right)
+    both = np.concatenate([a, b])
+    assert left.n == 1000
+    assert left.mean == pytest.approx(both.mean(), rel=1e-12)
+    assert left.variance == pytest.approx(both.var(ddof=1), rel=1e-12)
+    empty = WelfordAccumulator()
+    empty.merge(left)
+    assert (empty.n, empty.mean, empty.m2) == (left.n, left.mean, left.m2)
+
+
+def test_problem_set_cache_is_lru_and_never_closes_a_held_set(monkeypatch):
+    """eviction drops only the cache's reference (no close() under a caller)
+    and a hit moves the entry to the most-recently-used end."""
+    from paper_2603_01193_b200 import engine
+
+    closed = []
+
+    class FakeSet:
+        def __init__(self, ctx, problems):
+            self.problems = problems
+
+        def close(self):
+            closed.append(self)
+
+    monkeypatch.setattr(engine, "ProblemSet", FakeSet)
+    monkeypatch.setattr(engine, "_psets", {})
+    monkeypatch.setattr(engine, "_PSET_CACHE_MAX", 2)
+    monkeypatch.setattr(engine, "problem_record", lambda p: p)
+    ctx = object()
+    a = engine.problem_set(ctx, ["a"])
+    engine.problem_set(ctx, ["b"])
+    assert engine.problem_set(ctx, ["a"]) is a  # hit: "a" becomes most recent
+    engine.problem_set(ctx, ["c"])  # evicts "b", not "a"
+    assert engine.problem_set(ctx, ["a"]) is a
+    assert [k[1] for k in engine._psets] == [("c",), ("a",)]
+    assert closed == []

@@ -133,3 +133,32 @@ def test_golden_records_match_config_builders():
             np.testing.assert_array_equal(mine[2], r[2])
             np.testing.assert_array_equal(mine[4], r[4])
             np.testing.assert_array_equal(mine[6], r[6])
+
+
+def test_philox4x32_rounds_restatement():
+    """The C oracle's Philox4x32-R (the NATIVE stream's 10- and opt-in 7-round blocks)
+    equals the exact-integer restatement for every round count."""
+    rng = np.random.default_rng(9)
+    ctr = rng.integers(0, 2**32, size=(64, 4), dtype=np.uint64).astype(np.uint32)
+    for rounds in (1, 2, 7, 10, 13):
+        got = O.philox4x32(ctr, 0x1234, 0xFEDC, rounds=rounds)
+        for i in range(64):
+            assert [int(v) for v in got[i]] == O.philox4x32_int(ctr[i], (0x1234, 0xFEDC), rounds=rounds)
+    assert O.philox4x32_int((0, 0, 0, 0), (0, 0), rounds=10) == list(O.PHILOX4X32_KAT[0][2])
+
+
+def test_beta22_median_grid_moments():
+    """The 3D source jump's radius fraction: the median of three 12-bit uniforms,
+    midpoint-rounded. Its exact moments (rational arithmetic) against brute-force
+    enumeration on a 4-bit grid, and against Beta(2,2) (E t = 1/2, E t^2 = 3/10):
+    the 12-bit grid's bias is 0 and 5.0e-9."""
+    import itertools
+
+    g = [(k + 0.5) / 16 for k in range(16)]
+    meds = [sorted(t)[1] for t in itertools.product(g, g, g)]
+    m1, m2 = O.median3_grid_moments(4)
+    assert abs(m1 - np.mean(meds)) < 1e-15
+    assert abs(m2 - np.mean(np.square(meds))) < 1e-15
+    e1, e2 = O.median3_grid_moments(12)
+    assert e1 == 0.5
+    assert 0 < e2 - 0.3 < 1e-8
