@@ -1723,6 +1723,12 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #define WOS_AMORT_RNG 1
 #endif
   constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1;
+  // Branch-free step (single-instance constant-boundary NATIVE kernels with a source:
+  // cfg0, cfg4): no deferred recording, so an idle lane holds no state worth keeping
+#ifndef WOS_HOT_LOOP
+#define WOS_HOT_LOOP 1
+#endif
+  constexpr bool kHotLoop = WOS_HOT_LOOP && W::kHot && S::BC && kJumpFirst && !kAmort && !W::kScr;
   auto record = [&](Real d) {
     // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
     const Real v = W::finish_value(l, a);
@@ -1884,13 +1890,18 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       s_issue += n;
       idle = __ballot_sync(WOS_FULL, !active);
     }
-  } else
+  } else {
+  // Refill threshold (idle lanes), loop-invariant and at most 32 so that an all-idle
+  // warp always refills; it goes through a shuffle so ptxas keeps it in a register
+  // instead of reloading it from the constant bank every iteration.
+  // (delta tracking: a step costs far more than recording, so the plain threshold;
+  // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
+  const int refill_thr = __shfl_sync(
+      WOS_FULL,
+      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmort ? 4 : 0) : kAmort ? 1 : a.refill_min), 0);
   while (true) {
     const int n_idle = __popc(idle);
-    // (delta tracking: a step costs far more than recording, so the plain threshold;
-    // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
-    if (n_idle >= ((defer && !W::kScr) ? a.refill_min_deferred + (kAmort ? 4 : 0) : kAmort ? 1 : a.refill_min) ||
-        n_idle == 32) {
+    if (n_idle >= refill_thr) {
       flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
@@ -2086,6 +2097,20 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         }
         if (!live) finish(l.d);
       }
+    } else if constexpr (kHotLoop) {
+      // every lane jumps, live or not: an idle lane (its walk recorded, the lane waiting
+      // for a refill) computes a jump from its stale state that is never recorded, and
+      // the warp runs the step without a divergent branch around it
+      W::advance_native(l, l.d, a);
+      l.step += 1;
+      l.d = W::dist(l, a, srec);
+      const bool fin = active & ((l.d < eps) | (l.step >= a.max_steps));
+      if (fin) {
+        lane_steps += (unsigned long long)l.step;
+        *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = l.acc + a.bnd_c;
+        atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
+      }
+      active = active & !fin;
     } else if (active) {
       if (jf) {
         // the walk is live at l.d >= eps, step < max_steps (tested when l.d was queried)
@@ -2112,6 +2137,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       }
     }
     idle = __ballot_sync(WOS_FULL, !active);
+  }
   }
 
   // ---- walk-step total (u64, deterministic integer sum) ----

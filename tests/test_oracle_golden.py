@@ -10,7 +10,7 @@ moments, and the reference's numba kernels on spec-coded disk/ball problems.
 import numpy as np
 import pytest
 
-from conftest import golden_records, load_golden
+from conftest import GOLDEN, golden_records, load_golden
 from oracle import oracle as O
 
 CFGS = [0, 1, 2, 3, 4]
@@ -162,3 +162,27 @@ def test_beta22_median_grid_moments():
     e1, e2 = O.median3_grid_moments(12)
     assert e1 == 0.5
     assert 0 < e2 - 0.3 < 1e-8
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_oracle_rows_match_large_reference_sets(cfg):
+    """The C oracle (reference form, fp64) against the reference's own walks on 40,960
+    rows per config (golden_large_cfg{i}.npz; inputs re-derived by large_rows.py)."""
+    import sys
+
+    sys.path.insert(0, GOLDEN)
+    from large_rows import large_rows
+
+    from paper_2603_01193_b200 import configs
+
+    w = configs.build(cfg)
+    z = load_golden(f"golden_large_cfg{cfg}.npz")
+    inst, pts, pid, tid, sgn = large_rows(w, cfg)
+    assert pts.shape[0] == z["values"].size >= 40960
+    for k in np.unique(inst):
+        m = inst == k
+        v, s, h = O.walk_rows(w.problems[k], pts[m], pid[m], tid[m], sgn[m], seed=w.cfg.rng_seed,
+                              eps=w.cfg.eps_shell, max_steps=w.cfg.max_steps)
+        assert np.array_equal(s, z["steps"][m])
+        assert np.array_equal(h, z["hits"][m])
+        np.testing.assert_allclose(v, z["values"][m], rtol=1e-12, atol=1e-15)
