@@ -467,18 +467,23 @@ struct Walker {
   // closest boundary point at termination
   __device__ static __forceinline__ void project(const Lane& l, const KArgs& a, Real* q) {
     if constexpr (S::DOM == DOM_BALL && S::NATIVE) {
-      // explicit fma / IEEE sqrt and division: every kernel variant (estimate or rows
-      // sink, single- or multi-instance) rounds the projection alike
+      // q = c + R u / |u| with one MUFU rsqrt (2^-22 relative: far below the Monte Carlo
+      // error of g(q)); explicit FMAs: every kernel variant (estimate or rows sink,
+      // single- or multi-instance) rounds the projection alike. |u| = 0 (or subnormal,
+      // flushed): the +x axis point, as the reference (geometry.py:196-206)
       float s = 0.0f, u[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
         u[i] = l.x[i] - domp(l, a, i);
         s = fmaf(u[i], u[i], s);
       }
-      const float rho = __fsqrt_rn(s), R = domp(l, a, 3);
+      float inv;
+      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(s));
+      const bool zero = !(s > 0.0f) || !(inv < 3.0e38f);
+      const float R = domp(l, a, 3);
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        const float dir = (rho == 0.0f) ? (i == 0 ? 1.0f : 0.0f) : __fdiv_rn(u[i], rho);
+        const float dir = zero ? (i == 0 ? 1.0f : 0.0f) : u[i] * inv;
         q[i] = fmaf(R, dir, domp(l, a, i));
       }
     } else if constexpr (S::DOM == DOM_BALL) {
@@ -914,16 +919,26 @@ struct Walker {
           const int M = a.bnd_M;
           Real g = B[1];
           if constexpr (S::NATIVE) {
-            // (cos t, sin t) = q / |q| (t = polar angle), then the rotation recurrence
+            // (cos t, sin t) = q / |q| (t = polar angle), then the rotation recurrence;
+            // orders up to 8 unrolled (coefficient offsets fixed at compile time)
             const float r2 = fmaf(q[0], q[0], q[1] * q[1]);
-            const float inv = r2 > 0.0f ? rsqrtf(r2) : 0.0f;
-            const float c1 = r2 > 0.0f ? q[0] * inv : 1.0f, s1 = q[1] * inv;
+            float inv;
+            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
+            const bool ok = r2 > 0.0f && inv < 3.0e38f;
+            const float c1 = ok ? q[0] * inv : 1.0f, s1 = ok ? q[1] * inv : 0.0f;
             float cm = c1, sm = s1;
-            for (int m = 1; m <= M; ++m) {
+            auto term = [&](int m) {
               g = fmaf(B[1 + m], cm, fmaf(B[1 + M + m], sm, g));
               const float cn = fmaf(cm, c1, -sm * s1);
               sm = fmaf(sm, c1, cm * s1);
               cm = cn;
+            };
+            if (M <= 8) {
+#pragma unroll
+              for (int m = 1; m <= 8; ++m)
+                if (m <= M) term(m);
+            } else {
+              for (int m = 1; m <= M; ++m) term(m);
             }
           } else {
             const Real t = (Real)atan2((double)q[1], (double)q[0]);
@@ -1590,6 +1605,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   __syncthreads();
 
   const bool anti = a.antithetic != 0;
+  // antithetic pairs share a traj id (walk jr uses id jr & ~1) and walk jr & 1 is the
+  // mirrored one: warp-uniform masks for the hot issue path
+  const uint32_t anti_jmask = __shfl_sync(WOS_FULL, anti ? ~1u : ~0u, 0);
+  const uint32_t anti_bit = __shfl_sync(WOS_FULL, anti ? 1u : 0u, 0);
   const uint32_t IU = a.IU, L = a.L, U = a.U;
   const bool split = a.n_chunks > 0;  // L > kChunk: units are chunks of one point
   const Real eps = sizeof(Real) == 8 ? (Real)a.eps : (Real)a.eps_f;
@@ -1973,7 +1992,44 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           }
         }
         const uint32_t n = min(min((uint32_t)n_idle, room), cap);
-        if (!active) {
+        if constexpr (kHotLoop) {
+          // Branch-light issue of the cached unit's next walks: the per-lane start state
+          // (counter fold, sign, ring slot) is computed by every lane and committed by the
+          // lanes that take a walk; the point, its distance and the unit slot are
+          // warp-uniform. Same walks and streams as the general issue below.
+          const uint32_t rank = __popc(idle & lanemask_lt());
+          const uint32_t seq = s_issue + rank;
+          const uint32_t jr = seq - (cu_end - IU);
+          const bool take = !active && rank < n;
+          const bool real = cu_j0 + jr < cu_jend;  // else a null item padding the last chunk
+          const uint32_t blk_new = (cu_k % kSlots) * 4u;
+          if (cu_fastc) {
+            const uint32_t c2 = cu_c2b + (jr & anti_jmask);
+            const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+            if (take && real) {
+#pragma unroll
+              for (int i = 0; i < DIM; ++i) l.x[i] = cu_x[i];
+              l.acc = Real(0);
+              l.step = 0;
+              l.d = cu_d;
+              l.pc = pc;
+              l.sgn = __int_as_float(0x3f800000 | ((jr & anti_bit) << 31));
+              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+              blk = blk_new;
+              active = true;
+            }
+          } else if (take && real) {  // the unit's traj ids cross a 2^32 boundary
+            const uint32_t j = cu_j0 + jr;
+            const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+            W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, (anti && (j & 1u)) ? -1.0 : 1.0);
+            l.d = cu_d;
+            l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+            blk = blk_new;
+            active = true;
+          }
+          if (take && !real) atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_new), 1u);
+          if (cu_d < eps && take && real) finish(cu_d);  // the unit's point lies in the shell
+        } else if (!active) {
           const uint32_t rank = __popc(idle & lanemask_lt());
           if (rank < n) {
             const uint32_t seq = s_issue + rank;
