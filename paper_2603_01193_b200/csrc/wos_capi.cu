@@ -761,12 +761,15 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
     default: ns = 0;
   }
   int nb = 0;
+  // NATIVE series run to an order bucket (wos_walk.cuh order_bucket): the rows hold
+  // zero coefficients up to it
+  const int Mb = M <= 4 ? 4 : (M <= 8 ? 8 : M);
   switch (s->bnd_kind) {
     case WOS_BND_CONST: nb = 1; break;
     case WOS_BND_LINEAR: nb = dim + 1; break;
     case WOS_BND_FOURIER5: nb = 5; break;
-    case WOS_BND_FOURIER: nb = 2 + 2 * M; break;
-    case WOS_BND_SQUARE_ARCSINE: nb = 4 + M; break;
+    case WOS_BND_FOURIER: nb = 2 + 2 * Mb; break;
+    case WOS_BND_SQUARE_ARCSINE: nb = 4 + Mb; break;
     case WOS_BND_QUADRATIC: nb = 6; break;
     case WOS_BND_VC: nb = 4; break;
   }
@@ -1040,7 +1043,18 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       default:
         for (int k = 0; k < p.n_bnd; ++k) bd[k] = p.bnd[k];
     }
-    for (int k = 0; k < nb; ++k) rn[s->bnd_off + k] = (float)bd[k];
+    if (p.bnd_kind == WOS_BND_FOURIER) {
+      // NATIVE row: [M, B1, b1, c1, b2, c2, ...] (pairs interleaved: offsets independent of M)
+      const int Mi = (int)p.bnd[0];
+      rn[s->bnd_off] = (float)Mb;
+      rn[s->bnd_off + 1] = (float)p.bnd[1];
+      for (int m = 1; m <= Mi; ++m) {
+        rn[s->bnd_off + 2 * m] = (float)p.bnd[1 + m];
+        rn[s->bnd_off + 2 * m + 1] = (float)p.bnd[1 + Mi + m];
+      }
+    } else {
+      for (int k = 0; k < nb; ++k) rn[s->bnd_off + k] = (float)bd[k];
+    }
   }
   s->h_row_n.assign(tn.begin(), tn.begin() + stride);
   s->h_row_n_scaled = s->h_row_n;
@@ -1233,7 +1247,8 @@ static int check_watchdog(wos_context* c, cudaStream_t st) {
   CUDA_TRY(cudaStreamSynchronize(st));
   if (w) {
     cudaMemsetAsync(c->d_watchdog, 0, sizeof(w), st);
-    return fail(WOS_ERR_CUDA, "walk kernel watchdog tripped (iteration limit): results invalid");
+    return fail(WOS_ERR_CUDA, w == 2u ? "walk kernel refused a boundary-parameter offset it was not built for"
+                                      : "walk kernel watchdog tripped (iteration limit): results invalid");
   }
   return WOS_OK;
 }

@@ -884,8 +884,26 @@ struct Walker {
     }
   }
 
+  // Offset of the boundary parameters in an instance row, known at compile time when
+  // the source kind fixes the source block's size (wos_capi.cu: bnd_off = kSrcOff + ns);
+  // -1 = read KArgs::bnd_off. The kernel checks the host's value once at entry.
+  static constexpr int kBndOff =
+      S::SRC == SRC_NONE ? kSrcOff
+      : S::SRC == SRC_CONST ? kSrcOff + 1
+      : S::SRC == SRC_RBF2 ? kSrcOff + 6
+      : S::SRC == SRC_GAUSS ? kSrcOff + 2 + DIM
+      : (S::NATIVE && S::SRC == SRC_SINE && S::SK > 0) ? kSrcOff + (DIM == 2 ? S::SK * S::SK : S::SK * S::SK * S::SK)
+      : -1;
+  __device__ static __forceinline__ const Real* bnd_row(const Lane& l, const KArgs& a) {
+    if constexpr (kBndOff >= 0) return prow(l, a) + kBndOff;
+    else return prow(l, a) + a.bnd_off;
+  }
+  // NATIVE Fourier / arc-length series are evaluated to an order bucket (4, 8, else M);
+  // the host pads the native rows with zero coefficients up to it (wos_capi.cu)
+  __device__ static __forceinline__ int order_bucket(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : M); }
+
   __device__ static __forceinline__ Real boundary(const Lane& l, const KArgs& a, const Real* q) {
-    const Real* B = prow(l, a) + a.bnd_off;
+    const Real* B = bnd_row(l, a);
     switch (a.bnd_kind) {
       case BND_CONST:
         return B[0];
@@ -926,19 +944,23 @@ struct Walker {
             asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
             const bool ok = r2 > 0.0f && inv < 3.0e38f;
             const float c1 = ok ? q[0] * inv : 1.0f, s1 = ok ? q[1] * inv : 0.0f;
+            // native rows interleave the coefficient pairs: B[2m] = b_m, B[2m + 1] = c_m
             float cm = c1, sm = s1;
             auto term = [&](int m) {
-              g = fmaf(B[1 + m], cm, fmaf(B[1 + M + m], sm, g));
+              g = fmaf(B[2 * m], cm, fmaf(B[2 * m + 1], sm, g));
               const float cn = fmaf(cm, c1, -sm * s1);
               sm = fmaf(sm, c1, cm * s1);
               cm = cn;
             };
-            if (M <= 8) {
+            const int Mb = order_bucket(M);
+            if (Mb == 4) {
 #pragma unroll
-              for (int m = 1; m <= 8; ++m)
-                if (m <= M) term(m);
+              for (int m = 1; m <= 4; ++m) term(m);
+            } else if (Mb == 8) {
+#pragma unroll
+              for (int m = 1; m <= 8; ++m) term(m);
             } else {
-              for (int m = 1; m <= M; ++m) term(m);
+              for (int m = 1; m <= Mb; ++m) term(m);
             }
           } else {
             const Real t = (Real)atan2((double)q[1], (double)q[0]);
@@ -977,11 +999,21 @@ struct Walker {
             float s1, c1;
             __sincosf(kTwoPiF * s * 0.25f, &s1, &c1);
             float sm = s1, cm = c1;
-            for (int m = 1; m <= M; ++m) {
+            auto term = [&](int m) {
               g = fmaf(B[3 + m], sm, g);
               const float sn = fmaf(sm, c1, cm * s1);
               cm = fmaf(cm, c1, -sm * s1);
               sm = sn;
+            };
+            const int Mb = order_bucket(M);  // zero-padded rows (wos_capi.cu)
+            if (Mb == 4) {
+#pragma unroll
+              for (int m = 1; m <= 4; ++m) term(m);
+            } else if (Mb == 8) {
+#pragma unroll
+              for (int m = 1; m <= 8; ++m) term(m);
+            } else {
+              for (int m = 1; m <= Mb; ++m) term(m);
             }
           } else {
             for (int m = 1; m <= M; ++m) g = g + B[3 + m] * sin((Real)kTwoPi * (Real)m * s / Real(4));
@@ -1265,9 +1297,9 @@ struct Walker {
       if constexpr (S::SRC == SRC_SCR_VC) {
         Real q[DIM];
         project(l, a, q);
-        g = vc_boundary(prow(l, a) + a.bnd_off, q);
+        g = vc_boundary(bnd_row(l, a), q);
       } else {
-        g = prow(l, a)[a.bnd_off];
+        g = bnd_row(l, a)[0];
       }
       return (l.acc + l.thr * g) / l.sa;
     }
@@ -1275,7 +1307,7 @@ struct Walker {
     if constexpr (ONE) {
       if (a.bnd_kind == BND_CONST) return l.acc + a.bnd_c;
     }
-    if (a.bnd_kind == BND_CONST) return l.acc + prow(l, a)[a.bnd_off];
+    if (a.bnd_kind == BND_CONST) return l.acc + bnd_row(l, a)[0];
     Real q[DIM];
     project(l, a, q);
     return l.acc + boundary(l, a, q);
@@ -1593,6 +1625,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (W::kBndOff >= 0) {
+    // the compile-time boundary offset must be the host's (a mismatch would be a build
+    // inconsistency): flag it through the watchdog and do nothing
+    if (a.bnd_off != W::kBndOff) {
+      if (threadIdx.x == 0) atomicExch(a.watchdog, 2u);
+      return;
+    }
+  }
   // the warp's ring offset goes through a shuffle so that ptxas keeps it in a register
   // instead of re-deriving it from %tid and the launch constants every iteration
   const uint32_t woff = __shfl_sync(WOS_FULL, (uint32_t)(a.stage_bytes + a.seg_stage_bytes +
@@ -1910,6 +1950,153 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       idle = __ballot_sync(WOS_FULL, !active);
     }
   } else {
+  bool ilp2_done = false;
+#ifndef WOS_ILP2
+#define WOS_ILP2 0
+#endif
+  if constexpr (WOS_ILP2 && kHotLoop) {
+    if (fast) {
+      // ==================================================================
+      // Two walks per lane (slots A = l, B = lb): every iteration jumps both, so the
+      // two independent dependency chains interleave and the loop / vote / refill
+      // control is paid once per two jumps. The walks are the same as in the
+      // one-slot loop (each keeps its stream and ring slot); only which lane and slot
+      // runs which walk differs, which the in-order reduction does not see.
+      // ==================================================================
+      typename W::Lane lb = l;  // (shares the keys and coefficients)
+      bool act_a = false, act_b = false;
+      uint32_t blk_a = 0, blk_b = 0;
+      unsigned idle_a = WOS_FULL, idle_b = WOS_FULL;
+      const int thr2 = __shfl_sync(WOS_FULL, min(64, 2 * a.refill_min), 0);
+      // move the cached unit to the next grabbed one; false if none is left
+      auto next_unit = [&]() -> bool {
+        if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
+          uint32_t u = 0;
+          if (lane == 0) u = atomicAdd(a.work_counter, 1u);
+          u = __shfl_sync(WOS_FULL, u, 0);
+          if (u >= a.n_units) {
+            exhausted = true;
+          } else {
+            if (lane == 0) unitq[n_grabbed % kUQ] = u;
+            ++n_grabbed;
+            s_avail += IU;
+          }
+        }
+        if (n_grabbed == cu_k + 1u) return false;
+        cu_k += 1u;
+        cu_end += IU;
+        const uint32_t unit = unitq[cu_k % kUQ];
+        uint32_t p = unit;
+        cu_j0 = 0;
+        cu_jend = L;
+        if (split) {
+          p = fast_div(unit, a.nc_mul, a.nc_shr);
+          cu_j0 = (unit - p * a.n_chunks) * kChunk;
+          cu_jend = min(L, cu_j0 + kChunk);
+        }
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) cu_x[i] = W::start_coord(a.points[(size_t)p * DIM + i]);
+        cu_pid = a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p;
+        cu_d = W::dist_at(l, a, cu_x);
+        const uint64_t tid0 = a.traj_start + cu_j0;
+        cu_c1 = (uint32_t)cu_pid;
+        cu_c2b = (uint32_t)tid0;
+        cu_c3 = (uint32_t)(tid0 >> 32) ^ ((uint32_t)(cu_pid >> 32) * 0x85EBCA6Bu);
+        cu_fastc = (uint64_t)(uint32_t)tid0 + (cu_jend - cu_j0) <= 0x100000000ull;
+        return true;
+      };
+      auto record2 = [&](typename W::Lane& s, uint32_t blk_s) {
+        lane_steps += (unsigned long long)s.step;
+        *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + s.seq) = s.acc + a.bnd_c;
+        atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_s), 1u);
+      };
+      // issue the cached unit's next walks to the idle lanes of one slot; ranks start at base
+      auto issue = [&](typename W::Lane& s, bool& act, uint32_t& blk_s, unsigned idle_s, uint32_t base,
+                       uint32_t n) {
+        const uint32_t rank = base + __popc(idle_s & lanemask_lt());
+        const uint32_t seq = s_issue + rank;
+        const uint32_t jr = seq - (cu_end - IU);
+        const bool take = !act && rank < n;
+        const bool real = cu_j0 + jr < cu_jend;
+        const uint32_t blk_new = (cu_k % kSlots) * 4u;
+        if (cu_fastc) {
+          const uint32_t c2 = cu_c2b + (jr & anti_jmask);
+          const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+          if (take && real) {
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) s.x[i] = cu_x[i];
+            s.acc = Real(0);
+            s.step = 0;
+            s.d = cu_d;
+            s.pc = pc;
+            s.sgn = __int_as_float(0x3f800000 | ((jr & anti_bit) << 31));
+            s.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+            blk_s = blk_new;
+            act = true;
+          }
+        } else if (take && real) {
+          const uint32_t j = cu_j0 + jr;
+          const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
+          W::start(s, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, (anti && (j & 1u)) ? -1.0 : 1.0);
+          s.d = cu_d;
+          s.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+          blk_s = blk_new;
+          act = true;
+        }
+        if (take && !real) atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_new), 1u);
+        if (cu_d < eps && take && real) {  // the unit's point lies in the shell
+          record2(s, blk_s);
+          act = false;
+        }
+      };
+      while (true) {
+        const uint32_t na = (uint32_t)__popc(idle_a);
+        const int n_idle = (int)na + __popc(idle_b);
+        if (n_idle >= thr2) {
+          uint32_t room = cu_end - s_issue;
+          uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
+          if (cap < (uint32_t)n_idle || room == 0) {
+            retire();
+            cap = r_seq + (uint32_t)kRing - s_issue;
+          }
+          if (room == 0 || cap == 0) {
+            if (++refills > a.iter_limit) {
+              if (lane == 0) atomicExch(a.watchdog, 1u);
+              break;
+            }
+            if (room == 0) {
+              if (next_unit()) {
+                room = IU;
+              } else if (n_idle == 64 && exhausted) {
+                retire();
+                if (r_seq == s_issue) break;  // no walk left, none running, all retired
+              }
+            }
+          }
+          const uint32_t n = min(min((uint32_t)n_idle, room), cap);
+          issue(l, act_a, blk_a, idle_a, 0u, n);
+          issue(lb, act_b, blk_b, idle_b, na, n);
+          s_issue += n;
+        }
+        W::advance_native(l, l.d, a);
+        W::advance_native(lb, lb.d, a);
+        l.step += 1;
+        lb.step += 1;
+        l.d = W::dist(l, a, srec);
+        lb.d = W::dist(lb, a, srec);
+        const bool fin_a = act_a & ((l.d < eps) | (l.step >= a.max_steps));
+        const bool fin_b = act_b & ((lb.d < eps) | (lb.step >= a.max_steps));
+        if (fin_a) record2(l, blk_a);
+        if (fin_b) record2(lb, blk_b);
+        act_a = act_a & !fin_a;
+        act_b = act_b & !fin_b;
+        idle_a = __ballot_sync(WOS_FULL, !act_a);
+        idle_b = __ballot_sync(WOS_FULL, !act_b);
+      }
+      ilp2_done = true;
+    }
+  }
+  if (!ilp2_done) {
   // Refill threshold (idle lanes), loop-invariant and at most 32 so that an all-idle
   // warp always refills; it goes through a shuffle so ptxas keeps it in a register
   // instead of reloading it from the constant bank every iteration.
@@ -1924,14 +2111,23 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
-      if constexpr (est) {
+      if (est && (!kHotLoop || !fast)) {  // (the hot loop's cached-unit refill retires lazily)
         __syncwarp();  // order the lanes' counter updates before the check
         if (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) retire();
       }
       if (fast) {
         // ============ refill, one point per unit: cached point in registers ============
         uint32_t room = cu_end - s_issue;
-        const uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
+        uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
+        if constexpr (kHotLoop) {
+          // the hot loop refills in small batches: it retires only when the ring is
+          // short of slots for them or a new unit is due (the unit queue and counter
+          // slots must have room); retire() orders the lanes' counter updates itself
+          if (cap < (uint32_t)n_idle || room == 0) {
+            retire();
+            cap = r_seq + (uint32_t)kRing - s_issue;
+          }
+        }
         if (room == 0 || cap == 0) {
           // watchdog: bail out and flag instead of spinning forever if the stream
           // bookkeeping ever stalled (a stall can only loop through here)
@@ -1986,8 +2182,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                 cu_fastc = (uint64_t)(uint32_t)tid0 + (cu_jend - cu_j0) <= 0x100000000ull;
               }
               room = IU;
-            } else if (n_idle == 32 && exhausted && r_seq == s_issue) {
-              break;  // no walk left, none running, all retired
+            } else if (n_idle == 32 && exhausted) {
+              if constexpr (kHotLoop) retire();  // (retirement is lazy there)
+              if (r_seq == s_issue) break;  // no walk left, none running, all retired
             }
           }
         }
@@ -2193,6 +2390,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       }
     }
     idle = __ballot_sync(WOS_FULL, !active);
+  }
   }
   }
 
