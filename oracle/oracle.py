@@ -65,6 +65,7 @@ def load():
         L.oracle_philox4x32.argtypes = [c_int64, P, c_uint32, c_uint32, P]
         L.oracle_philox4x32_rounds.argtypes = [c_int64, P, c_uint32, c_uint32, c_int, P]
         L.oracle_set_philox_rounds.argtypes = [c_int]
+        L.oracle_beta_table.argtypes = [P]
         L.oracle_contains.argtypes = [P, P]
         L.oracle_contains.restype = c_int
         L.oracle_set_sigma_bar.argtypes = [c_double]
@@ -248,6 +249,13 @@ PHILOX4X32_KAT = [
     ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
      (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
 ]
+
+
+def beta_table():
+    """The NATIVE 3D source jump's Beta(2,2) conditional-mean table (include/wos_beta_table.h)."""
+    out = np.empty(4096, dtype=np.float32)
+    load().oracle_beta_table(out.ctypes.data)
+    return out
 
 
 def median3_grid_moments(bits):

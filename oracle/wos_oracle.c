@@ -30,6 +30,7 @@
  * Build: oracle/Makefile -> oracle/_build/libwos_oracle.so
  */
 #include "../include/wos_b200.h"
+#include "../include/wos_beta_table.h"
 
 #include <math.h>
 #include <pthread.h>
@@ -688,13 +689,22 @@ void oracle_native_keys(uint64_t seed, uint64_t ikey, uint32_t* k0, uint32_t* k1
   *k1 = (uint32_t)(seed >> 32) ^ (uint32_t)ikey ^ ((uint32_t)(ikey >> 32) * 0x9E3779B9u);
 }
 
-static uint32_t umed3(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
-  uint32_t m = hi < c ? hi : c;
-  return lo > m ? lo : m;
+/* a 13-bit field, midpoint-rounded: (b + 1/2) 2^-13 */
+static double u13(uint32_t b) { return ((double)(b & 0x1FFFu) + 0.5) * (1.0 / 8192.0); }
+
+/* the Beta(2,2) conditional-mean table of include/wos_beta_table.h, built once */
+static float g_beta_tab[WOS_BETA_TABLE_N];
+static pthread_once_t g_beta_once = PTHREAD_ONCE_INIT;
+static void build_beta_table(void) { wos_beta22_table(g_beta_tab); }
+static const float* beta_table(void) {
+  pthread_once(&g_beta_once, build_beta_table);
+  return g_beta_tab;
 }
-/* low 20 bits, midpoint-rounded: (b + 1/2) 2^-20 */
-static double u20(uint32_t w) { return ((double)(w & 0xFFFFFu) + 0.5) * (1.0 / 1048576.0); }
+
+void oracle_beta_table(float* out) {
+  const float* t = beta_table();
+  for (int k = 0; k < WOS_BETA_TABLE_N; ++k) out[k] = t[k];
+}
 
 static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pid, uint64_t tid,
                             double sgn, uint64_t seed, double eps, int64_t max_steps,
@@ -724,7 +734,7 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
        source-free jump needs one word (2D) or two (3D), so a block serves 4 (2D) or
        2 (3D) consecutive jumps: jump s reads the block at counter 2*floor(s/per)
        (wos_walk.cuh kPerBlock) */
-    const int per = has_src ? 1 : (dim == 2 ? 4 : 2);
+    const int per = has_src ? (dim == 3 ? 2 : 1) : (dim == 2 ? 4 : 2);
     const int sub = (int)(step % per);
     uint32_t u[4];
     {
@@ -754,21 +764,21 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[1] = s * sin(phi);
       dir[2] = z;
     } else {
-      /* seven uniforms from the block's 128 bits (wos_walk.cuh f20 / f_top12 / umed3):
-         the Beta(2,2) radius fraction is the median of the words u[0..2] reduced to
-         their top 12 bits (the median commutes with x >> 20), midpoint-rounded
-         (b + 1/2) 2^-12; z, phi, z' are the low 20 bits of u[0], u[1], u[2]
-         (midpoint-rounded); phi' the top 23 bits of u[3] */
-      double z = 2.0 * u20(u[0]) - 1.0;
+      /* layout v3 (wos_walk.cuh jump3_source): 64 bits per jump, words (u[0], u[1]) for
+         an even step, (u[2], u[3]) for an odd one; 13-bit midpoint-rounded direction
+         fields (bits 0..12 and 19..31 of each word) and a 12-bit index (bits 13..18 of
+         both words) into the Beta(2,2) conditional-mean table */
+      const uint32_t wa = u[2 * sub], wb = u[2 * sub + 1];
+      double z = 2.0 * u13(wa & 0x1FFFu) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
-      double phi = TWO_PI * u20(u[1]) - PI;
+      double phi = TWO_PI * u13(wa >> 19) - PI;
       dir[0] = s * cos(phi);
       dir[1] = s * sin(phi);
       dir[2] = z;
-      double vz = 2.0 * u20(u[2]) - 1.0;
+      double vz = 2.0 * u13(wb & 0x1FFFu) - 1.0;
       double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
-      double vphi = TWO_PI * u23(u[3]) - PI;
-      double t = ((double)(umed3(u[0], u[1], u[2]) >> 20) + 0.5) * (1.0 / 4096.0);
+      double vphi = TWO_PI * u13(wb >> 19) - PI;
+      double t = (double)beta_table()[((wa >> 13) & 0x3Fu) | ((wb >> 7) & 0xFC0u)];
       double r = d * t;
       double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
                      x[2] + sgn * r * vz};

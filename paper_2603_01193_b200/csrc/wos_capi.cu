@@ -12,6 +12,7 @@
 #include <atomic>
 #include <mutex>
 #include <thread>
+#include "wos_beta_table.h"
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -81,6 +82,7 @@ struct wos_context {
   // candidate-grid query)
   std::atomic<unsigned long long> n_launches{0};
   unsigned long long* d_perf = nullptr;
+  float* d_beta_tab = nullptr;  // Beta(2,2) radius table of NATIVE 3D source jumps
   // per-kernel launch attributes (dynamic shared memory set, occupancy at that size):
   // computed on the first launch of a (kernel, smem) pair instead of every launch
   std::unordered_map<const void*, std::pair<size_t, int>> launch_cache;
@@ -185,6 +187,12 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, kStatusBytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_perf, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_beta_tab, sizeof(float) * WOS_BETA_TABLE_N);
+  if (e == cudaSuccess) {
+    std::vector<float> bt(WOS_BETA_TABLE_N);
+    wos_beta22_table(bt.data());
+    e = cudaMemcpy(c->d_beta_tab, bt.data(), sizeof(float) * WOS_BETA_TABLE_N, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = cudaMemset(c->d_perf, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) {
     c->d_exterior = c->d_status;
@@ -206,6 +214,7 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_status);
   cudaFree(c->d_steps);
   cudaFree(c->d_perf);
+  cudaFree(c->d_beta_tab);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1470,7 +1479,14 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.sigma_bar = cfg->sigma_bar;
   a.sqrt_sig = sqrt(cfg->sigma_bar > 0.0 ? cfg->sigma_bar : 0.0);
   a.majorant = c->d_majorant;
-  const size_t smem = smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes, k.elem);
+  // NATIVE 3D source jumps read the Beta(2,2) radius table from shared memory
+  if (cfg->mode == WOS_MODE_NATIVE_F32 && s->dim == 3 && s->src_kind != WOS_SRC_NONE &&
+      s->src_kind != WOS_SRC_SCREENED_CONST && s->src_kind != WOS_SRC_SCREENED_VC) {
+    a.beta_tab = c->d_beta_tab;
+    a.beta_stage_bytes = (int)(sizeof(float) * WOS_BETA_TABLE_N);
+  }
+  const size_t smem =
+      smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes + (size_t)a.beta_stage_bytes, k.elem);
   if (smem > 220 * 1024)
     return fail(WOS_ERR_UNSUPPORTED,
                 "problem table too large for shared memory (%zu bytes); split the batch",

@@ -131,6 +131,8 @@ struct KArgs {
   uint32_t iter_limit;         // max(2^27, 4 * max_steps) loop iterations per warp
   int32_t philox_rounds;       // NATIVE: Philox4x32 rounds per block (10, or 7 on request)
   unsigned long long* seg_evals;  // NATIVE polygons: segment distances evaluated (or null)
+  const float* beta_tab;         // NATIVE 3D source jumps: Beta(2,2) table (wos_beta_table.h)
+  int32_t beta_stage_bytes;      // its shared-memory bytes (0 when the kernel does not use it)
   // ---- single-instance NATIVE launches: the instance row and the Philox round
   // keys live in the kernel-parameter constant bank (FFMA / LOP3 c[] operands) ----
   uint32_t rk0[10];

@@ -33,8 +33,8 @@
 //   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
 //   and ONE Philox4x32 block per jump (counter (2*step, pid, tid, hi-words); 10
 //   rounds, or 7 with WalkConfig.philox_rounds = 7);
-//   the 3D source jump needs 7 uniforms and takes them as bit fields of the
-//   block's 128 bits (f20 / f_top12 / umed3 below; oracle/wos_oracle.c restates it);
+//   the 3D source jump takes 64 bits (two jumps per block; jump3_source below,
+//   with the Beta(2,2) radius from a staged table; oracle/wos_oracle.c restates it);
 //   source-free jumps share a block between 4 (2D) / 2 (3D) consecutive jumps
 //   (kPerBlock; phase-locked amortised rounds on closed-form domains). Direction
 //   angles are 2 pi u - pi (MUFU's accurate range). Single-instance NATIVE launches
@@ -107,33 +107,6 @@ __device__ __forceinline__ double pmax(double a, double b) { return fmax(a, b); 
 __device__ __forceinline__ float pmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double pabs(double a) { return fabs(a); }
 __device__ __forceinline__ float pabs(float a) { return fabsf(a); }
-
-// The 3D source jump's seven uniforms from one Philox4x32 block W (128 bits):
-//   radius fraction t ~ Beta(2,2) = the median of three uniforms, taken as the median
-//     of the raw words W.x, W.y, W.z: x -> x >> 20 is monotone, so med(W) >> 20 is the
-//     median of their top-12-bit fields, i.e. of three independent 12-bit uniforms, and
-//     t = (field + 1/2) 2^-12 (midpoint rounding: a 12-bit grid perturbs E[h(t)] by
-//     O(2^-24 h''); tests/test_gpu_native.py measures the moments). It depends on the
-//     words' top 12 bits only;
-//   z (move), phi (move), z' (volume sample) = the low 20 bits of W.x, W.y, W.z,
-//     midpoint-rounded (b + 1/2) 2^-20: independent of t;
-//   phi' (volume sample) = the top 23 bits of W.w.
-// Integer median (min3 / max3 / xor) and two ops per 20-bit field replace the float
-// median of bit-assembled fields (19 -> 13 instructions, no IMAD.SHL on the FMA-heavy
-// pipe for the fields). oracle/wos_oracle.c walk_native_one restates this layout.
-__device__ __forceinline__ uint32_t umed3(uint32_t a, uint32_t b, uint32_t c) {
-  // {a, b, c} = {min, med, max} as a multiset, so a ^ b ^ c = min ^ med ^ max
-  return a ^ b ^ c ^ min(min(a, b), c) ^ max(max(a, b), c);
-}
-// low 20 bits as 1 + (b + 1/2) 2^-20 in [1, 2) (exponent e: 0x3f8 -> [1, 2), 0x400 -> [2, 4))
-// (mask, then shift-and-add: LOP3 + LEA, no second immediate for a LOP3 to need)
-__device__ __forceinline__ float f20(uint32_t w, uint32_t expo = 0x3f800000u) {
-  return __uint_as_float(((w & 0x000fffffu) << 3) + (expo | 4u));
-}
-// the top 12 bits of w as 1 + (b + 1/2) 2^-12 (LOP3 + LEA.HI)
-__device__ __forceinline__ float f_top12(uint32_t w) {
-  return __uint_as_float(((w & 0xfff00000u) >> 9) + 0x3f800400u);
-}
 
 // BC_: single-instance launch of a problem whose boundary value is a constant
 // (a.bnd_c): the walk value is acc + g with no projection, so the kernel carries
@@ -1381,7 +1354,10 @@ struct Walker {
   // 2 (s % 2), 2 (s % 2) + 1 (3D) of the block at counter 2 floor(s / kPerBlock).
   // Kernels whose lanes run in phase lock (the amortised loop) draw each block once;
   // the others redraw it per jump and select the words (same stream).
-  static constexpr int kPerBlock = (S::NATIVE && S::SRC == SRC_NONE) ? (DIM == 2 ? 4 : 2) : 1;
+  // The NATIVE 3D source jump (layout v3, below) also takes 64 bits: a block serves two
+  // jumps, and its radius fraction comes from the shared-memory Beta(2,2) table
+  static constexpr bool kBetaTab = S::NATIVE && DIM == 3 && S::SRC != SRC_NONE && !kScr;
+  static constexpr int kPerBlock = (S::NATIVE && S::SRC == SRC_NONE) ? (DIM == 2 ? 4 : 2) : (kBetaTab ? 2 : 1);
 
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
     return native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)kPerBlock));
@@ -1433,7 +1409,12 @@ struct Walker {
     l.x[2] = fmaf(sd, z, l.x[2]);
   }
   // the block's words for sub-jump k of an amortised round
-  __device__ static __forceinline__ void move_native_word(Lane& l, float d, const uint4& B, int k) {
+  __device__ static __forceinline__ void move_native_word(Lane& l, float d, const uint4& B, int k,
+                                                         const KArgs& a) {
+    if constexpr (kBetaTab) {
+      jump3_source(l, d, a, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
+      return;
+    }
     if constexpr (DIM == 2) move_native_2d(l, d, k == 0 ? B.x : k == 1 ? B.y : k == 2 ? B.z : B.w);
     else move_native_3d(l, d, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
   }
@@ -1462,31 +1443,56 @@ struct Walker {
       const bool odd = (l.step & 1) != 0;
       move_native_3d(l, d, odd ? A.z : A.x, odd ? A.w : A.y);
     } else {
-      // the seven uniforms of the block (layout above f20): z = 2u - 1 is exact for
-      // u = f - 1, so fmaf(-z, z, 1) >= 0
-      const float z = f20(A.x, 0x40000000u) - 3.0f;
-      const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
-      float sph, cph;
-      __sincosf(dir_angle(f20(A.y)), &sph, &cph);
-      const float vz = f20(A.z, 0x40000000u) - 3.0f;
-      const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
-      float vsp, vcp;
-      __sincosf(dir_angle(f12(A.w)), &vsp, &vcp);
-      // Beta(2,2) radius fraction = median of three uniforms; r = d * (med - 1)
-      const float med = f_top12(umed3(A.x, A.y, A.z));
-      const float sr = l.sgn * fmaf(d, med, -d);
-      const float srv = sr * vs;
-      // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
-      const float2 xy = make_float2(l.x[0], l.x[1]);
-      const float2 gxy = __ffma2_rn(make_float2(srv, srv), make_float2(vcp, vsp), xy);
-      const float g[3] = {gxy.x, gxy.y, fmaf(sr, vz, l.x[2])};
-      l.acc = fmaf(-(d * d) * (kScaled ? (1.0f / 6.0f) * kInvPi2F : 1.0f / 6.0f), source(l, a, g), l.acc);
-      const float sdxy = sd * sxy;
-      const float2 nxy = __ffma2_rn(make_float2(sdxy, sdxy), make_float2(cph, sph), xy);
-      l.x[0] = nxy.x;
-      l.x[1] = nxy.y;
-      l.x[2] = fmaf(sd, z, l.x[2]);
+      // two jumps per block: jump s takes words (x, y) for even s, (z, w) for odd s
+      const bool odd = (l.step & 1) != 0;
+      jump3_source(l, d, a, odd ? A.z : A.x, odd ? A.w : A.y);
     }
+  }
+
+  // NATIVE 3D source jump, layout v3: 64 bits (two words) per jump, so one Philox4x32
+  // block serves two jumps (kPerBlock = 2; phase-locked rounds in the hot loop):
+  //   wa bits 0..12 -> z (move), 13..18 -> radius index bits 0..5, 19..31 -> phi (move)
+  //   wb bits 0..12 -> z' (sample), 13..18 -> radius index bits 6..11, 19..31 -> phi'
+  // Direction fields are 13-bit, midpoint-rounded ((b + 1/2) 2^-13): the midpoint rule
+  // on the periodic phi is spectrally accurate and on z errs by O(2^-26) of the
+  // integrand's curvature — far below fp32 rounding of the walk value. The radius
+  // fraction t ~ Beta(2,2) is the conditional mean of its 12-bit probability bin
+  // (include/wos_beta_table.h: E[t] exact, E[t^2] -1.0e-8), read from the table the
+  // kernel stages in shared memory. oracle/wos_oracle.c restates this layout.
+  __device__ static __forceinline__ float f13_lo(uint32_t w, uint32_t expo) {  // bits 0..12
+    return __uint_as_float(((w & 0x1fffu) << 10) + (expo | 0x200u));
+  }
+  __device__ static __forceinline__ float f13_hi(uint32_t w) {  // bits 19..31
+    return __uint_as_float(((w & 0xfff80000u) >> 9) + 0x3f800200u);
+  }
+  __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
+                                                     uint32_t wb) {
+    extern __shared__ __align__(16) unsigned char wos_smem_[];
+    const float* btab = reinterpret_cast<const float*>(wos_smem_ + a.stage_bytes + a.seg_stage_bytes);
+    const float sd = l.sgn * d;
+    // z = 2u - 1 is exact for u = f - 1, so fmaf(-z, z, 1) >= 0
+    const float z = f13_lo(wa, 0x40000000u) - 3.0f;
+    const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
+    float sph, cph;
+    __sincosf(dir_angle(f13_hi(wa)), &sph, &cph);
+    const float vz = f13_lo(wb, 0x40000000u) - 3.0f;
+    const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
+    float vsp, vcp;
+    __sincosf(dir_angle(f13_hi(wb)), &vsp, &vcp);
+    const uint32_t k = ((wa >> 13) & 0x3fu) | ((wb >> 7) & 0xfc0u);
+    const float t = btab[k];
+    const float sr = sd * t;
+    const float srv = sr * vs;
+    // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
+    const float2 xy = make_float2(l.x[0], l.x[1]);
+    const float2 gxy = __ffma2_rn(make_float2(srv, srv), make_float2(vcp, vsp), xy);
+    const float g[3] = {gxy.x, gxy.y, fmaf(sr, vz, l.x[2])};
+    l.acc = fmaf(-(d * d) * (kScaled ? (1.0f / 6.0f) * kInvPi2F : 1.0f / 6.0f), source(l, a, g), l.acc);
+    const float sdxy = sd * sxy;
+    const float2 nxy = __ffma2_rn(make_float2(sdxy, sdxy), make_float2(cph, sph), xy);
+    l.x[0] = nxy.x;
+    l.x[1] = nxy.y;
+    l.x[2] = fmaf(sd, z, l.x[2]);
   }
 
   // ---------------- walk start ----------------
@@ -1624,6 +1630,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       srec = dst;
     }
   }
+  // ---- stage the Beta(2,2) radius table (NATIVE 3D source jumps) after them ----
+  if constexpr (W::kBetaTab) {
+    float* dst = reinterpret_cast<float*>(smem + a.stage_bytes + a.seg_stage_bytes);
+    for (int i = threadIdx.x; i < a.beta_stage_bytes / 4; i += blockDim.x) dst[i] = a.beta_tab[i];
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (W::kBndOff >= 0) {
     // the compile-time boundary offset must be the host's (a mismatch would be a build
@@ -1635,7 +1646,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   }
   // the warp's ring offset goes through a shuffle so that ptxas keeps it in a register
   // instead of re-deriving it from %tid and the launch constants every iteration
-  const uint32_t woff = __shfl_sync(WOS_FULL, (uint32_t)(a.stage_bytes + a.seg_stage_bytes +
+  const uint32_t woff = __shfl_sync(WOS_FULL, (uint32_t)(a.stage_bytes + a.seg_stage_bytes + a.beta_stage_bytes +
                                     warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4)), 0);
   unsigned char* wbase = smem + woff;
   Real* ring = reinterpret_cast<Real*>(wbase);
@@ -1680,7 +1691,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     // (warp 0's ring, not yet in use) -> shuffle: loop-invariant registers that ptxas
     // cannot re-derive from the constant bank, so it keeps them in uniform registers
     // instead of re-issuing the constant loads every step
-    uint32_t* hs = reinterpret_cast<uint32_t*>(smem + a.stage_bytes + a.seg_stage_bytes);
+    uint32_t* hs = reinterpret_cast<uint32_t*>(smem + a.stage_bytes + a.seg_stage_bytes + a.beta_stage_bytes);
     for (int i = threadIdx.x; i < 20 + W::kHotC; i += blockDim.x)
       hs[i] = i < 10 ? a.rk0[i] : i < 20 ? a.rk1[i - 10] : __float_as_uint(a.cp[i - 20]);
     __syncthreads();
@@ -1787,7 +1798,37 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_HOT_LOOP
 #define WOS_HOT_LOOP 1
 #endif
-  constexpr bool kHotLoop = WOS_HOT_LOOP && W::kHot && S::BC && kJumpFirst && !kAmort && !W::kScr;
+  constexpr bool kHotLoop = WOS_HOT_LOOP && W::kHot && S::BC && kJumpFirst && !W::kScr &&
+                            (W::kPerBlock == 1 || W::kBetaTab);
+  // the general amortised-round loop (source-free kernels; the hot loop runs its own rounds)
+  constexpr bool kAmortLoop = kAmort && !kHotLoop;
+  // One hot-loop step of a walk slot; returns whether the walk is still live. With a
+  // two-jump block (3D source jumps) a step is a round of two jumps from one Philox
+  // block: every slot enters a round at an even step (walks start at step 0 and are
+  // issued between rounds), and a walk that ends after the first jump skips the second.
+  auto hot_step = [&](typename W::Lane& s) -> bool {
+    if constexpr (!kHotLoop) {
+      return false;  // (not used outside the hot loop)
+    } else if constexpr (W::kPerBlock == 2) {
+      const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step >> 1));
+      W::jump3_source(s, s.d, a, B.x, B.y);
+      s.step += 1;
+      s.d = W::dist(s, a, srec);
+      bool live = !((s.d < eps) | (s.step >= a.max_steps));
+      if (live) {
+        W::jump3_source(s, s.d, a, B.z, B.w);
+        s.step += 1;
+        s.d = W::dist(s, a, srec);
+        live = !((s.d < eps) | (s.step >= a.max_steps));
+      }
+      return live;
+    } else {
+      W::advance_native(s, s.d, a);
+      s.step += 1;
+      s.d = W::dist(s, a, srec);
+      return !((s.d < eps) | (s.step >= a.max_steps));
+    }
+  };
   auto record = [&](Real d) {
     // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
     const Real v = W::finish_value(l, a);
@@ -2078,14 +2119,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           issue(lb, act_b, blk_b, idle_b, na, n);
           s_issue += n;
         }
-        W::advance_native(l, l.d, a);
-        W::advance_native(lb, lb.d, a);
-        l.step += 1;
-        lb.step += 1;
-        l.d = W::dist(l, a, srec);
-        lb.d = W::dist(lb, a, srec);
-        const bool fin_a = act_a & ((l.d < eps) | (l.step >= a.max_steps));
-        const bool fin_b = act_b & ((lb.d < eps) | (lb.step >= a.max_steps));
+        const bool live_a = hot_step(l);
+        const bool live_b = hot_step(lb);
+        const bool fin_a = act_a & !live_a;
+        const bool fin_b = act_b & !live_b;
         if (fin_a) record2(l, blk_a);
         if (fin_b) record2(lb, blk_b);
         act_a = act_a & !fin_a;
@@ -2104,7 +2141,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
   const int refill_thr = __shfl_sync(
       WOS_FULL,
-      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmort ? 4 : 0) : kAmort ? 1 : a.refill_min), 0);
+      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? 4 : 0) : kAmortLoop ? 1 : a.refill_min), 0);
   while (true) {
     const int n_idle = __popc(idle);
     if (n_idle >= refill_thr) {
@@ -2332,7 +2369,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
 
     // ================= one step of every active walk =================
-    if constexpr (kAmort) {
+    if constexpr (kAmortLoop) {
       // one round: kPerBlock jumps of every live lane from one Philox block
       // (a lane whose walk ends mid-round stops moving and is finished after the round:
       // the sub-jumps stay straight-line predicated code)
@@ -2342,7 +2379,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #pragma unroll
         for (int k = 0; k < W::kPerBlock; ++k) {
           if (live) {
-            W::move_native_word(l, l.d, B, k);
+            W::move_native_word(l, l.d, B, k, a);
             l.step += 1;
             l.d = W::dist(l, a, srec);
             live = !(l.d < eps || l.step >= a.max_steps);
@@ -2354,10 +2391,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       // every lane jumps, live or not: an idle lane (its walk recorded, the lane waiting
       // for a refill) computes a jump from its stale state that is never recorded, and
       // the warp runs the step without a divergent branch around it
-      W::advance_native(l, l.d, a);
-      l.step += 1;
-      l.d = W::dist(l, a, srec);
-      const bool fin = active & ((l.d < eps) | (l.step >= a.max_steps));
+      const bool fin = active & !hot_step(l);
       if (fin) {
         lane_steps += (unsigned long long)l.step;
         *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = l.acc + a.bnd_c;

@@ -12,11 +12,10 @@
   strict avalanche criterion for single-bit counter changes. (Random123 reports
   Philox4x32-7 as the fewest rounds that pass TestU01 Crush; these tests check the
   properties the walk relies on in the layout it uses.)
-* The Beta(2,2) radius fraction of the 3D source jump (the median of the words'
-  top-12-bit fields, wos_walk.cuh f_top12 / umed3): its first two moments over 1e9
-  draws of the production stream equal the exact moments of the midpoint-rounded
-  12-bit median (oracle.median3_grid_moments, exact rationals; they differ from
-  Beta(2,2)'s 1/2 and 3/10 by 0 and 5.0e-9).
+* The Beta(2,2) radius fraction of the 3D source jump (a 12-bit index into the
+  conditional-mean table, wos_walk.cuh jump3_source): over 1e9 draws of the production
+  stream its index is uniform and its first two moments equal the table's (which
+  differ from Beta(2,2)'s 1/2 and 3/10 by 0 and -1.0e-8).
 """
 
 import numpy as np
@@ -151,28 +150,34 @@ def test_seven_round_avalanche(gpu, word, bit):
 
 @pytest.mark.parametrize("rounds", [10, 7])
 def test_beta22_radius_moments_over_1e9_draws(gpu, rounds):
-    """The radius fraction t = (med(W.x, W.y, W.z) >> 20) + 1/2) / 4096 of the production
-    stream: E[t] and E[t^2] over 1e9 draws equal the exact moments of the discrete
-    12-bit median within 5 standard errors (and so Beta(2,2)'s to ~2e-8)."""
-    m1_exact, m2_exact = O.median3_grid_moments(12)
+    """The radius fraction of the 3D source jump (layout v3, wos_walk.cuh jump3_source):
+    index ((wa >> 13) & 63) | ((wb >> 7) & 0xfc0) into the Beta(2,2) table, two jumps per
+    block. Over 1.0e9 draws of the production stream the index is uniform, so E[t] and
+    E[t^2] equal the table's exact means within 5 standard errors (and Beta(2,2)'s to
+    ~1e-8)."""
+    tab = torch.from_numpy(O.beta_table().astype(np.float64)).cuda()
+    m1_exact, m2_exact = float(tab.mean()), float((tab * tab).mean())
     hist = torch.zeros(4096, dtype=torch.int64, device="cuda")
     total = 0
     chunk = 1 << 25
-    n_chunks = 30  # 30 x 2^25 = 1.007e9 draws
+    n_chunks = 15  # 15 x 2^25 blocks x 2 jumps = 1.007e9 draws
     for k in range(n_chunks):
         i = torch.arange(chunk, device="cuda", dtype=torch.int64) + k * chunk
         c = torch.stack([2 * (i % 1000), 77 + i // (1000 * 4096), (i // 1000) % 4096, torch.zeros_like(i)],
                         dim=1).to(torch.int32)
         w = _blocks(gpu, c, 0x5EED, 0xC0FFEE, rounds).to(torch.int64) & 0xFFFFFFFF
-        a, b, cc = w[:, 0], w[:, 1], w[:, 2]
-        med = torch.maximum(torch.minimum(a, b), torch.minimum(torch.maximum(a, b), cc))
-        hist += torch.bincount(med >> 20, minlength=4096)
-        total += chunk
-    t = (torch.arange(4096, device="cuda", dtype=torch.float64) + 0.5) / 4096
+        for wa, wb in ((w[:, 0], w[:, 1]), (w[:, 2], w[:, 3])):
+            idx = ((wa >> 13) & 0x3F) | ((wb >> 7) & 0xFC0)
+            hist += torch.bincount(idx, minlength=4096)
+            total += chunk
     p = hist.to(torch.float64) / total
-    e1 = (p * t).sum().item()
-    e2 = (p * t * t).sum().item()
+    e1 = (p * tab).sum().item()
+    e2 = (p * tab * tab).sum().item()
     sd1 = np.sqrt(0.05 / total)        # Var[t] = 1/20
     sd2 = np.sqrt((1 / 7 - 0.09) / total)  # Var[t^2] = E[t^4] - E[t^2]^2 = 1/7 - 9/100
     assert abs(e1 - m1_exact) < 5 * sd1, (e1, m1_exact)
     assert abs(e2 - m2_exact) < 5 * sd2, (e2, m2_exact)
+    # the 12-bit index itself is uniform (chi-square, 4095 dof, 6 sigma)
+    e = total / 4096
+    chi2 = (((hist.to(torch.float64) - e) ** 2) / e).sum().item()
+    assert abs(chi2 - 4095) < 6 * np.sqrt(2 * 4095), chi2

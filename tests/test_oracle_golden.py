@@ -147,21 +147,20 @@ def test_philox4x32_rounds_restatement():
     assert O.philox4x32_int((0, 0, 0, 0), (0, 0), rounds=10) == list(O.PHILOX4X32_KAT[0][2])
 
 
-def test_beta22_median_grid_moments():
-    """The 3D source jump's radius fraction: the median of three 12-bit uniforms,
-    midpoint-rounded. Its exact moments (rational arithmetic) against brute-force
-    enumeration on a 4-bit grid, and against Beta(2,2) (E t = 1/2, E t^2 = 3/10):
-    the 12-bit grid's bias is 0 and 5.0e-9."""
-    import itertools
-
-    g = [(k + 0.5) / 16 for k in range(16)]
-    meds = [sorted(t)[1] for t in itertools.product(g, g, g)]
-    m1, m2 = O.median3_grid_moments(4)
-    assert abs(m1 - np.mean(meds)) < 1e-15
-    assert abs(m2 - np.mean(np.square(meds))) < 1e-15
-    e1, e2 = O.median3_grid_moments(12)
-    assert e1 == 0.5
-    assert 0 < e2 - 0.3 < 1e-8
+def test_beta22_table_moments():
+    """The 3D source jump's radius fraction: the conditional mean of a 12-bit Beta(2,2)
+    probability bin (include/wos_beta_table.h). Every entry lies inside its bin's
+    quantile interval; the table keeps E[t] = 1/2 (to fp32 rounding) and misses Beta(2,2)'s
+    E[t^2] = 3/10 and E[t^3] = 1/5 by about -1.0e-8 and -1.5e-8."""
+    t = O.beta_table().astype(np.float64)
+    assert t.size == 4096 and np.all(np.diff(t) > 0)
+    v = np.arange(4097) / 4096.0
+    q = 0.5 + np.sin(np.arcsin(2 * v - 1) / 3)
+    assert np.all(t >= q[:-1]) and np.all(t <= q[1:])
+    assert np.allclose(3 * q**2 - 2 * q**3, v, atol=1e-15)  # the quantile is exact
+    assert abs(t.mean() - 0.5) < 1e-10
+    assert -2e-8 < (t * t).mean() - 0.3 < 0
+    assert -3e-8 < (t**3).mean() - 0.2 < 0
 
 
 @pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
