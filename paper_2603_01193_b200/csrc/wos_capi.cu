@@ -1067,11 +1067,19 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
   }
   s->h_row_n.assign(tn.begin(), tn.begin() + stride);
   s->h_row_n_scaled = s->h_row_n;
-  if (s->dom_kind == WOS_DOM_BOX)  // centre and half extent times pi, from the fp64 row
+  if (s->dom_kind == WOS_DOM_BOX) {  // centre and half extent times pi, from the fp64 row
     for (int k = 0; k < s->dim; ++k) {
       s->h_row_n_scaled[8 + k] = (float)(M_PI * 0.5 * (td[k] + td[4 + k]));
       s->h_row_n_scaled[12 + k] = (float)(M_PI * 0.5 * (td[4 + k] - td[k]));
     }
+    // the scaled-coordinate kernels (monomial sine sources) take the Green weight
+    // 1 / (2 dim) pi^-2 folded into the source coefficients (wos_walk.cuh advance_native)
+    if (s->src_kind == WOS_SRC_SINE && (s->sk_native == 3 || s->sk_native == 4)) {
+      const double w = 1.0 / (2.0 * s->dim * M_PI * M_PI);
+      for (int k = 0; k < ns; ++k)
+        s->h_row_n_scaled[kSrcOff + k] = (float)((double)s->h_row_n[kSrcOff + k] * w);
+    }
+  }
   s->h_nkey1 = hd[0].nkey1;
   std::vector<float> tf(td.size());
   for (size_t k = 0; k < td.size(); ++k) tf[k] = (float)td[k];

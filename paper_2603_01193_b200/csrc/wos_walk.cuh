@@ -1435,7 +1435,8 @@ struct Walker {
         const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
         const float sr = l.sgn * r;
         const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
-        l.acc = fmaf(-(kScaled ? 0.25f * kInvPi2F : 0.25f) * d * d, source(l, a, g), l.acc);
+        // (scaled-coordinate kernels: the host folds the weight 1/4 pi^-2 into the coefficients)
+        l.acc = fmaf(kScaled ? -(d * d) : -0.25f * d * d, source(l, a, g), l.acc);
       }
       l.x[0] = fmaf(sd, cth, l.x[0]);
       l.x[1] = fmaf(sd, sth, l.x[1]);
@@ -1459,16 +1460,28 @@ struct Walker {
   // fraction t ~ Beta(2,2) is the conditional mean of its 12-bit probability bin
   // (include/wos_beta_table.h: E[t] exact, E[t^2] -1.0e-8), read from the table the
   // kernel stages in shared memory. oracle/wos_oracle.c restates this layout.
+  // (the mask and the shift go through inline PTX so that ptxas emits LOP3 + LEA / LEA.HI
+  // rather than rewriting the add as an OR and needing a second LOP3 for the constant)
   __device__ static __forceinline__ float f13_lo(uint32_t w, uint32_t expo) {  // bits 0..12
-    return __uint_as_float(((w & 0x1fffu) << 10) + (expo | 0x200u));
+    uint32_t m;
+    asm("lop3.b32 %0, %1, 0x1fff, 0, 0xc0;" : "=r"(m) : "r"(w));
+    return __uint_as_float((m << 10) + (expo | 0x200u));
   }
   __device__ static __forceinline__ float f13_hi(uint32_t w) {  // bits 19..31
-    return __uint_as_float(((w & 0xfff80000u) >> 9) + 0x3f800200u);
+    uint32_t r;
+    asm("shf.r.clamp.b32 %0, %1, %2, 9;" : "=r"(r) : "r"(w & 0xfff80000u), "r"(0u));
+    return __uint_as_float(r + 0x3f800200u);
+  }
+  __device__ static __forceinline__ const float* beta_tab_smem(const KArgs& a) {
+    extern __shared__ __align__(16) unsigned char wos_smem_[];
+    return reinterpret_cast<const float*>(wos_smem_ + a.stage_bytes + a.seg_stage_bytes);
   }
   __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
                                                      uint32_t wb) {
-    extern __shared__ __align__(16) unsigned char wos_smem_[];
-    const float* btab = reinterpret_cast<const float*>(wos_smem_ + a.stage_bytes + a.seg_stage_bytes);
+    jump3_source(l, d, a, wa, wb, beta_tab_smem(a));
+  }
+  __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
+                                                     uint32_t wb, const float* btab) {
     const float sd = l.sgn * d;
     // z = 2u - 1 is exact for u = f - 1, so fmaf(-z, z, 1) >= 0
     const float z = f13_lo(wa, 0x40000000u) - 3.0f;
@@ -1487,7 +1500,8 @@ struct Walker {
     const float2 xy = make_float2(l.x[0], l.x[1]);
     const float2 gxy = __ffma2_rn(make_float2(srv, srv), make_float2(vcp, vsp), xy);
     const float g[3] = {gxy.x, gxy.y, fmaf(sr, vz, l.x[2])};
-    l.acc = fmaf(-(d * d) * (kScaled ? (1.0f / 6.0f) * kInvPi2F : 1.0f / 6.0f), source(l, a, g), l.acc);
+    // (scaled-coordinate kernels: the host folds the weight 1/6 pi^-2 into the coefficients)
+    l.acc = fmaf(kScaled ? -(d * d) : -(d * d) * (1.0f / 6.0f), source(l, a, g), l.acc);
     const float sdxy = sd * sxy;
     const float2 nxy = __ffma2_rn(make_float2(sdxy, sdxy), make_float2(cph, sph), xy);
     l.x[0] = nxy.x;
@@ -1806,17 +1820,20 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // two-jump block (3D source jumps) a step is a round of two jumps from one Philox
   // block: every slot enters a round at an even step (walks start at step 0 and are
   // issued between rounds), and a walk that ends after the first jump skips the second.
+  // the staged Beta(2,2) table, addressed once (the shared window base is loop-invariant)
+  const float* hot_btab = nullptr;
+  if constexpr (W::kBetaTab) hot_btab = W::beta_tab_smem(a);
   auto hot_step = [&](typename W::Lane& s) -> bool {
     if constexpr (!kHotLoop) {
       return false;  // (not used outside the hot loop)
     } else if constexpr (W::kPerBlock == 2) {
       const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step >> 1));
-      W::jump3_source(s, s.d, a, B.x, B.y);
+      W::jump3_source(s, s.d, a, B.x, B.y, hot_btab);
       s.step += 1;
       s.d = W::dist(s, a, srec);
       bool live = !((s.d < eps) | (s.step >= a.max_steps));
       if (live) {
-        W::jump3_source(s, s.d, a, B.z, B.w);
+        W::jump3_source(s, s.d, a, B.z, B.w, hot_btab);
         s.step += 1;
         s.d = W::dist(s, a, srec);
         live = !((s.d < eps) | (s.step >= a.max_steps));
