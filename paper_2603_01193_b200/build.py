@@ -31,7 +31,10 @@ UNITS = {
     "wos_capi.cu": [],
     "wos_kernels_native.cu": [],
     "wos_kernels_native_est.cu": [],
-    "wos_kernels_native_est_bc.cu": [],
+    # the 10-round hot kernels (cfg4, cfg0) run two walks per lane at 3 CTAs/SM (80
+    # registers): -2 to -3 % against one walk at 4 CTAs/SM; the 7-round ones do not
+    # gain from it (round 2)
+    "wos_kernels_native_est_bc.cu": ["-DWOS_ILP2=1", "-DWOS_NATIVE_MINB=3"],
     "wos_kernels_native_est_r7.cu": [],
     "wos_kernels_native_est_bc_r7.cu": [],
     "wos_kernels_native_rows.cu": [],

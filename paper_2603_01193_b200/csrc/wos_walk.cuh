@@ -1472,16 +1472,29 @@ struct Walker {
     asm("shf.r.clamp.b32 %0, %1, %2, 9;" : "=r"(r) : "r"(w & 0xfff80000u), "r"(0u));
     return __uint_as_float(r + 0x3f800200u);
   }
-  __device__ static __forceinline__ const float* beta_tab_smem(const KArgs& a) {
+  // The table's shared-memory address: the start of the dynamic window in
+  // single-instance box / ball launches (nothing else is staged before it), else after
+  // the instance table and the polygon records. It is read with ld.shared on that 32-bit offset, so no generic address of
+  // the shared window has to be rebuilt inside the loop.
+  static constexpr bool kBetaAtZero = ONE && (S::DOM == DOM_BOX || S::DOM == DOM_BALL);
+  __device__ static __forceinline__ uint32_t beta_tab_offset(const KArgs& a) {
     extern __shared__ __align__(16) unsigned char wos_smem_[];
-    return reinterpret_cast<const float*>(wos_smem_ + a.stage_bytes + a.seg_stage_bytes);
+    // the dynamic window's shared address (a link-time constant) plus what precedes it
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(wos_smem_);
+    if constexpr (kBetaAtZero) return base;
+    else return base + (uint32_t)(a.stage_bytes + a.seg_stage_bytes);
+  }
+  __device__ static __forceinline__ float beta_at(uint32_t off, uint32_t k) {
+    float t;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(off + 4u * k));
+    return t;
   }
   __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
                                                      uint32_t wb) {
-    jump3_source(l, d, a, wa, wb, beta_tab_smem(a));
+    jump3_source(l, d, a, wa, wb, beta_tab_offset(a));
   }
   __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
-                                                     uint32_t wb, const float* btab) {
+                                                     uint32_t wb, uint32_t btab) {
     const float sd = l.sgn * d;
     // z = 2u - 1 is exact for u = f - 1, so fmaf(-z, z, 1) >= 0
     const float z = f13_lo(wa, 0x40000000u) - 3.0f;
@@ -1493,7 +1506,7 @@ struct Walker {
     float vsp, vcp;
     __sincosf(dir_angle(f13_hi(wb)), &vsp, &vcp);
     const uint32_t k = ((wa >> 13) & 0x3fu) | ((wb >> 7) & 0xfc0u);
-    const float t = btab[k];
+    const float t = beta_at(btab, k);
     const float sr = sd * t;
     const float srv = sr * vs;
     // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
@@ -1820,9 +1833,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // two-jump block (3D source jumps) a step is a round of two jumps from one Philox
   // block: every slot enters a round at an even step (walks start at step 0 and are
   // issued between rounds), and a walk that ends after the first jump skips the second.
-  // the staged Beta(2,2) table, addressed once (the shared window base is loop-invariant)
-  const float* hot_btab = nullptr;
-  if constexpr (W::kBetaTab) hot_btab = W::beta_tab_smem(a);
+  // the staged Beta(2,2) table's shared-memory offset
+  uint32_t hot_btab = 0u;
+  if constexpr (W::kBetaTab) hot_btab = W::beta_tab_offset(a);
   auto hot_step = [&](typename W::Lane& s) -> bool {
     if constexpr (!kHotLoop) {
       return false;  // (not used outside the hot loop)
