@@ -1,5 +1,5 @@
-/* Beta(2,2) radius table of the NATIVE 3D source jump (shared by the library and the
- * C oracle, so both walk the same stream).
+/* Radius tables of the NATIVE source jumps (3D: Beta(2,2); 2D: the disk Green's law),
+ * shared by the library and the C oracle, so both walk the same stream.
  *
  * The ball Green's function importance sampler draws the radius fraction t from
  * Beta(2,2), density 6 t (1 - t), CDF F(t) = 3 t^2 - 2 t^3 (greens.py:83-89: the
@@ -35,6 +35,34 @@ static inline void wos_beta22_table(float* out) {
     const double gb = 2.0 * tb * tb * tb - 1.5 * tb * tb * tb * tb;
     out[k] = (float)(n * (gb - ga));
     ta = tb;
+  }
+}
+
+/* The 2D counterpart: the disk Green's function G(r) = ln(R/r) / (2 pi) makes the radius
+ * fraction t = r/R of the importance-sampled source point follow p(t) = 4 t ln(1/t),
+ * F(t) = t^2 (1 - 2 ln t) (greens.py:68-89: mass R^2/4). Entry k is again the
+ * conditional mean of its 12-bit probability bin, N [4/9 t^3 (1 - 3 ln t)] between the
+ * bin's quantiles (found by bisection in double; F has no closed-form inverse). */
+static inline double wos_green2_cdf(double t) { return t <= 0.0 ? 0.0 : t * t * (1.0 - 2.0 * log(t)); }
+
+static inline double wos_green2_quantile(double v) {
+  double lo = 0.0, hi = 1.0;
+  for (int it = 0; it < 200 && hi - lo > 1e-17; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (wos_green2_cdf(mid) < v) lo = mid;
+    else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+static inline void wos_green2_table(float* out) {
+  const double n = (double)WOS_BETA_TABLE_N;
+  double ga = 0.0; /* antiderivative of t dF at t = 0 */
+  for (int k = 0; k < WOS_BETA_TABLE_N; ++k) {
+    const double tb = (k + 1 == WOS_BETA_TABLE_N) ? 1.0 : wos_green2_quantile((k + 1) / n);
+    const double gb = (4.0 / 9.0) * tb * tb * tb * (1.0 - 3.0 * log(tb));
+    out[k] = (float)(n * (gb - ga));
+    ga = gb;
   }
 }
 

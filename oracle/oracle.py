@@ -66,6 +66,7 @@ def load():
         L.oracle_philox4x32_rounds.argtypes = [c_int64, P, c_uint32, c_uint32, c_int, P]
         L.oracle_set_philox_rounds.argtypes = [c_int]
         L.oracle_beta_table.argtypes = [P]
+        L.oracle_green2_table.argtypes = [P]
         L.oracle_contains.argtypes = [P, P]
         L.oracle_contains.restype = c_int
         L.oracle_set_sigma_bar.argtypes = [c_double]
@@ -255,6 +256,13 @@ def beta_table():
     """The NATIVE 3D source jump's Beta(2,2) conditional-mean table (include/wos_beta_table.h)."""
     out = np.empty(4096, dtype=np.float32)
     load().oracle_beta_table(out.ctypes.data)
+    return out
+
+
+def green2_table():
+    """The NATIVE 2D source jump's disk Green's-law radius table (include/wos_beta_table.h)."""
+    out = np.empty(4096, dtype=np.float32)
+    load().oracle_green2_table(out.ctypes.data)
     return out
 
 

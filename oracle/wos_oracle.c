@@ -693,16 +693,28 @@ void oracle_native_keys(uint64_t seed, uint64_t ikey, uint32_t* k0, uint32_t* k1
 static double u13(uint32_t b) { return ((double)(b & 0x1FFFu) + 0.5) * (1.0 / 8192.0); }
 
 /* the Beta(2,2) conditional-mean table of include/wos_beta_table.h, built once */
-static float g_beta_tab[WOS_BETA_TABLE_N];
+static float g_beta_tab[WOS_BETA_TABLE_N], g_green2_tab[WOS_BETA_TABLE_N];
 static pthread_once_t g_beta_once = PTHREAD_ONCE_INIT;
-static void build_beta_table(void) { wos_beta22_table(g_beta_tab); }
+static void build_tables(void) {
+  wos_beta22_table(g_beta_tab);
+  wos_green2_table(g_green2_tab);
+}
 static const float* beta_table(void) {
-  pthread_once(&g_beta_once, build_beta_table);
+  pthread_once(&g_beta_once, build_tables);
   return g_beta_tab;
+}
+static const float* green2_table(void) {
+  pthread_once(&g_beta_once, build_tables);
+  return g_green2_tab;
 }
 
 void oracle_beta_table(float* out) {
   const float* t = beta_table();
+  for (int k = 0; k < WOS_BETA_TABLE_N; ++k) out[k] = t[k];
+}
+
+void oracle_green2_table(float* out) {
+  const float* t = green2_table();
   for (int k = 0; k < WOS_BETA_TABLE_N; ++k) out[k] = t[k];
 }
 
@@ -734,7 +746,7 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
        source-free jump needs one word (2D) or two (3D), so a block serves 4 (2D) or
        2 (3D) consecutive jumps: jump s reads the block at counter 2*floor(s/per)
        (wos_walk.cuh kPerBlock) */
-    const int per = has_src ? (dim == 3 ? 2 : 1) : (dim == 2 ? 4 : 2);
+    const int per = has_src ? 2 : (dim == 2 ? 4 : 2);
     const int sub = (int)(step % per);
     uint32_t u[4];
     {
@@ -747,15 +759,17 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[0] = cos(th);
       dir[1] = sin(th);
     } else if (dim == 2) {
-      double th = TWO_PI * u23(u[0]) - PI;
+      /* layout v3 (wos_walk.cuh jump_source, 2D): words (u[0], u[1]) for an even step,
+         (u[2], u[3]) for an odd one; theta = bits 19..31 and phi = bits 0..12 of the
+         first word, the radius fraction from the disk Green's-law table */
+      const uint32_t wa = u[2 * sub], wb = u[2 * sub + 1];
+      double th = TWO_PI * u13(wa >> 19) - PI;
       dir[0] = cos(th);
       dir[1] = sin(th);
-      if (has_src) {
-        double phi = TWO_PI * u23(u[1]) - PI;
-        double r = d * sqrt(u23(u[2]) * u23(u[3]));
-        double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
-        acc -= (d * d * 0.25) * source(pb, g);
-      }
+      double phi = TWO_PI * u13(wa & 0x1FFFu) - PI;
+      double r = d * (double)green2_table()[((wa >> 13) & 0x3Fu) | ((wb >> 7) & 0xFC0u)];
+      double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
+      acc -= (d * d * 0.25) * source(pb, g);
     } else if (!has_src) {
       double z = 2.0 * u23(u[2 * sub]) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));

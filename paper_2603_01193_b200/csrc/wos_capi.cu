@@ -82,7 +82,8 @@ struct wos_context {
   // candidate-grid query)
   std::atomic<unsigned long long> n_launches{0};
   unsigned long long* d_perf = nullptr;
-  float* d_beta_tab = nullptr;  // Beta(2,2) radius table of NATIVE 3D source jumps
+  float* d_beta_tab = nullptr;    // radius table of NATIVE 3D source jumps: Beta(2,2)
+  float* d_green2_tab = nullptr;  // ... of NATIVE 2D source jumps: the disk Green's law
   // per-kernel launch attributes (dynamic shared memory set, occupancy at that size):
   // computed on the first launch of a (kernel, smem) pair instead of every launch
   std::unordered_map<const void*, std::pair<size_t, int>> launch_cache;
@@ -188,10 +189,14 @@ extern "C" int wos_context_create(int32_t device, wos_context** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->d_steps, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_perf, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_beta_tab, sizeof(float) * WOS_BETA_TABLE_N);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_green2_tab, sizeof(float) * WOS_BETA_TABLE_N);
   if (e == cudaSuccess) {
-    std::vector<float> bt(WOS_BETA_TABLE_N);
+    std::vector<float> bt(WOS_BETA_TABLE_N), gt(WOS_BETA_TABLE_N);
     wos_beta22_table(bt.data());
+    wos_green2_table(gt.data());
     e = cudaMemcpy(c->d_beta_tab, bt.data(), sizeof(float) * WOS_BETA_TABLE_N, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_green2_tab, gt.data(), sizeof(float) * WOS_BETA_TABLE_N, cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaMemset(c->d_perf, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) {
@@ -215,6 +220,7 @@ extern "C" void wos_context_destroy(wos_context* c) {
   cudaFree(c->d_steps);
   cudaFree(c->d_perf);
   cudaFree(c->d_beta_tab);
+  cudaFree(c->d_green2_tab);
   cudaFree(c->d_scratch);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1487,10 +1493,10 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.sigma_bar = cfg->sigma_bar;
   a.sqrt_sig = sqrt(cfg->sigma_bar > 0.0 ? cfg->sigma_bar : 0.0);
   a.majorant = c->d_majorant;
-  // NATIVE 3D source jumps read the Beta(2,2) radius table from shared memory
-  if (cfg->mode == WOS_MODE_NATIVE_F32 && s->dim == 3 && s->src_kind != WOS_SRC_NONE &&
+  // NATIVE source jumps read their radius table from shared memory
+  if (cfg->mode == WOS_MODE_NATIVE_F32 && s->src_kind != WOS_SRC_NONE &&
       s->src_kind != WOS_SRC_SCREENED_CONST && s->src_kind != WOS_SRC_SCREENED_VC) {
-    a.beta_tab = c->d_beta_tab;
+    a.beta_tab = s->dim == 3 ? c->d_beta_tab : c->d_green2_tab;
     a.beta_stage_bytes = (int)(sizeof(float) * WOS_BETA_TABLE_N);
   }
   const size_t smem =

@@ -33,8 +33,8 @@
 //   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
 //   and ONE Philox4x32 block per jump (counter (2*step, pid, tid, hi-words); 10
 //   rounds, or 7 with WalkConfig.philox_rounds = 7);
-//   the 3D source jump takes 64 bits (two jumps per block; jump3_source below,
-//   with the Beta(2,2) radius from a staged table; oracle/wos_oracle.c restates it);
+//   a source jump takes 64 bits (two jumps per block; jump_source below, with the
+//   radius from a staged table; oracle/wos_oracle.c restates it);
 //   source-free jumps share a block between 4 (2D) / 2 (3D) consecutive jumps
 //   (kPerBlock; phase-locked amortised rounds on closed-form domains). Direction
 //   angles are 2 pi u - pi (MUFU's accurate range). Single-instance NATIVE launches
@@ -1356,7 +1356,7 @@ struct Walker {
   // the others redraw it per jump and select the words (same stream).
   // The NATIVE 3D source jump (layout v3, below) also takes 64 bits: a block serves two
   // jumps, and its radius fraction comes from the shared-memory Beta(2,2) table
-  static constexpr bool kBetaTab = S::NATIVE && DIM == 3 && S::SRC != SRC_NONE && !kScr;
+  static constexpr bool kBetaTab = S::NATIVE && S::SRC != SRC_NONE && !kScr;
   static constexpr int kPerBlock = (S::NATIVE && S::SRC == SRC_NONE) ? (DIM == 2 ? 4 : 2) : (kBetaTab ? 2 : 1);
 
   __device__ static __forceinline__ uint4 native_block(const Lane& l, const KArgs& a) {
@@ -1412,7 +1412,7 @@ struct Walker {
   __device__ static __forceinline__ void move_native_word(Lane& l, float d, const uint4& B, int k,
                                                          const KArgs& a) {
     if constexpr (kBetaTab) {
-      jump3_source(l, d, a, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
+      jump_source(l, d, a, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
       return;
     }
     if constexpr (DIM == 2) move_native_2d(l, d, k == 0 ? B.x : k == 1 ? B.y : k == 2 ? B.z : B.w);
@@ -1426,27 +1426,14 @@ struct Walker {
     if constexpr (DIM == 2 && S::SRC == SRC_NONE) {
       const uint32_t k = (uint32_t)l.step & 3u;
       move_native_2d(l, d, k == 0 ? A.x : k == 1 ? A.y : k == 2 ? A.z : A.w);
-    } else if constexpr (DIM == 2) {
-      float sth, cth;
-      __sincosf(dir_angle(f12(A.x)), &sth, &cth);
-      {
-        float sph, cph;
-        __sincosf(dir_angle(f12(A.y)), &sph, &cph);
-        const float r = d * fast_sqrt((f12(A.z) - 1.0f) * (f12(A.w) - 1.0f));
-        const float sr = l.sgn * r;
-        const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
-        // (scaled-coordinate kernels: the host folds the weight 1/4 pi^-2 into the coefficients)
-        l.acc = fmaf(kScaled ? -(d * d) : -0.25f * d * d, source(l, a, g), l.acc);
-      }
-      l.x[0] = fmaf(sd, cth, l.x[0]);
-      l.x[1] = fmaf(sd, sth, l.x[1]);
     } else if constexpr (S::SRC == SRC_NONE) {
       const bool odd = (l.step & 1) != 0;
       move_native_3d(l, d, odd ? A.z : A.x, odd ? A.w : A.y);
     } else {
-      // two jumps per block: jump s takes words (x, y) for even s, (z, w) for odd s
+      // source jumps (2D and 3D): two jumps per block, jump s takes words (x, y) for even
+      // s, (z, w) for odd s
       const bool odd = (l.step & 1) != 0;
-      jump3_source(l, d, a, odd ? A.z : A.x, odd ? A.w : A.y);
+      jump_source(l, d, a, odd ? A.z : A.x, odd ? A.w : A.y);
     }
   }
 
@@ -1489,13 +1476,30 @@ struct Walker {
     asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(off + 4u * k));
     return t;
   }
-  __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
+  __device__ static __forceinline__ void jump_source(Lane& l, float d, const KArgs& a, uint32_t wa,
                                                      uint32_t wb) {
-    jump3_source(l, d, a, wa, wb, beta_tab_offset(a));
+    jump_source(l, d, a, wa, wb, beta_tab_offset(a));
   }
-  __device__ static __forceinline__ void jump3_source(Lane& l, float d, const KArgs& a, uint32_t wa,
+  __device__ static __forceinline__ void jump_source(Lane& l, float d, const KArgs& a, uint32_t wa,
                                                      uint32_t wb, uint32_t btab) {
     const float sd = l.sgn * d;
+    if constexpr (DIM == 2) {
+      // 2D: wa bits 19..31 -> theta (move), bits 0..12 -> phi (sample direction); the
+      // radius index as in 3D, into the disk Green's-law table (wos_green2_table); wb's
+      // other bits are not used
+      float sth, cth;
+      __sincosf(dir_angle(f13_hi(wa)), &sth, &cth);
+      float sph, cph;
+      __sincosf(dir_angle(f13_lo(wa, 0x3f800000u)), &sph, &cph);
+      const uint32_t k = ((wa >> 13) & 0x3fu) | ((wb >> 7) & 0xfc0u);
+      const float sr = sd * beta_at(btab, k);
+      const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
+      // (scaled-coordinate kernels: the host folds the weight 1/4 pi^-2 into the coefficients)
+      l.acc = fmaf(kScaled ? -(d * d) : -0.25f * d * d, source(l, a, g), l.acc);
+      l.x[0] = fmaf(sd, cth, l.x[0]);
+      l.x[1] = fmaf(sd, sth, l.x[1]);
+      return;
+    } else {
     // z = 2u - 1 is exact for u = f - 1, so fmaf(-z, z, 1) >= 0
     const float z = f13_lo(wa, 0x40000000u) - 3.0f;
     const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
@@ -1520,6 +1524,7 @@ struct Walker {
     l.x[0] = nxy.x;
     l.x[1] = nxy.y;
     l.x[2] = fmaf(sd, z, l.x[2]);
+    }
   }
 
   // ---------------- walk start ----------------
@@ -1819,7 +1824,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_AMORT_RNG
 #define WOS_AMORT_RNG 1
 #endif
-  constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1;
+  // (source jumps also take two per block, but outside the hot loop — multi-instance and
+  // rows kernels — holding a block's second half across a jump costs the register file
+  // more than it saves: those kernels redraw the block per jump and select their words)
+  constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1 && S::SRC == SRC_NONE;
   // Branch-free step (single-instance constant-boundary NATIVE kernels with a source:
   // cfg0, cfg4): no deferred recording, so an idle lane holds no state worth keeping
 #ifndef WOS_HOT_LOOP
@@ -1841,12 +1849,12 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       return false;  // (not used outside the hot loop)
     } else if constexpr (W::kPerBlock == 2) {
       const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step >> 1));
-      W::jump3_source(s, s.d, a, B.x, B.y, hot_btab);
+      W::jump_source(s, s.d, a, B.x, B.y, hot_btab);
       s.step += 1;
       s.d = W::dist(s, a, srec);
       bool live = !((s.d < eps) | (s.step >= a.max_steps));
       if (live) {
-        W::jump3_source(s, s.d, a, B.z, B.w, hot_btab);
+        W::jump_source(s, s.d, a, B.z, B.w, hot_btab);
         s.step += 1;
         s.d = W::dist(s, a, srec);
         live = !((s.d < eps) | (s.step >= a.max_steps));

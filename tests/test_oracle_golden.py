@@ -185,3 +185,16 @@ def test_oracle_rows_match_large_reference_sets(cfg):
         assert np.array_equal(s, z["steps"][m])
         assert np.array_equal(h, z["hits"][m])
         np.testing.assert_allclose(v, z["values"][m], rtol=1e-12, atol=1e-15)
+
+
+def test_green2_table_moments():
+    """The 2D source jump's radius fraction: conditional means of 12-bit bins of the disk
+    Green's law p(t) = 4 t ln(1/t) (include/wos_beta_table.h). Entries lie in their bins,
+    E[t] = 4/9 to fp32 rounding, E[t^2] = 1/4 - 9.5e-9."""
+    t = O.green2_table().astype(np.float64)
+    assert t.size == 4096 and np.all(np.diff(t) > 0)
+    F = lambda x: np.where(x > 0, x * x * (1 - 2 * np.log(np.maximum(x, 1e-300))), 0.0)  # noqa: E731
+    k = np.arange(4096)
+    assert np.all(F(t) >= k / 4096 - 1e-7) and np.all(F(t) <= (k + 1) / 4096 + 1e-7)
+    assert abs(t.mean() - 4 / 9) < 1e-9
+    assert -2e-8 < (t * t).mean() - 0.25 < 0
