@@ -557,6 +557,25 @@ def main():
     if rank == 0:
         extras = {}
         full_spw = None
+        if world == 1 and not args.no_extras and args.mode == "native":
+            # the same workload on the other NATIVE stream (10 <-> 7 Philox rounds), timed
+            # the same way, so both streams' numbers come from one run
+            alt = 7 if args.philox_rounds == 10 else 10
+            cfg_alt = dataclasses.replace(w.cfg, philox_rounds=alt)
+            acc_alt = torch.zeros(1, dtype=torch.int64, device=dev)
+            n_alt = min(args.steps, 10)
+            t_alt = _time_estimates(
+                lambda i: estimate_tensors(pset, pts, ids, w.L, cfg_alt, inst_index=inst,
+                                           traj_start=(500 + i) * w.L, out_mean=mean, out_m2=m2,
+                                           total_steps=acc_alt, stream=stream, eps=eps),
+                stream, n_alt, flush)
+            S_alt = int(acc_alt.item()) / n_alt
+            ta = float(np.sum(t_alt)) / n_alt
+            extras["other_stream"] = {
+                "philox_rounds": alt, "ms_per_step": 1e3 * ta, "value": S_alt / ta,
+                "unit": "walk-steps/s", "walks_per_s": w.n_walks / ta,
+                "roofline": roofline(args.config, S_alt, w.n_walks, ta, 0, peaks, n_sm, clk_hz),
+                "timing": f"CUDA events, {n_alt} estimates, L2 flushed before each"}
         if world == 1 and not args.no_extras:
             if args.config == 4 and args.mode == "native":
                 extras["replay_f64"] = replay_f64_record(ctx, 4, flush)

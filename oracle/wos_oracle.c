@@ -575,7 +575,7 @@ static void walk_screened_one(const wos_problem* pb, const double* x0, uint64_t 
     const double surf = qq < 1.0e-6 ? 1.0 - qq * qq / 6.0 : qq / sinh(qq);
     double ue, uz, uphi, ur;
     if (native) {
-      uint32_t ca[4] = {(uint32_t)(2 * step), c1, c2, c3}, u[4];
+      uint32_t ca[4] = {c1, (uint32_t)(2 * step), c2, c3}, u[4];
       philox4x32(ca, k0n, k1n, u);
       ue = u23(u[0]);
       uz = u23(u[1]);
@@ -742,15 +742,14 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       *hit = (uint8_t)shell;
       return;
     }
-    /* one Philox4x32 block per jump at counter (2*step, pid, tid, hi-words); a
-       source-free jump needs one word (2D) or two (3D), so a block serves 4 (2D) or
-       2 (3D) consecutive jumps: jump s reads the block at counter 2*floor(s/per)
-       (wos_walk.cuh kPerBlock) */
+    /* Philox4x32 blocks at counter (pid, 2*floor(s/per), tid, hi-words): a source-free
+       jump needs one word (2D) or two (3D), a source jump two, so a block serves
+       per = 4 / 2 / 2 consecutive jumps (wos_walk.cuh kPerBlock) */
     const int per = has_src ? 2 : (dim == 2 ? 4 : 2);
     const int sub = (int)(step % per);
     uint32_t u[4];
     {
-      uint32_t ca[4] = {(uint32_t)(2 * (step / per)), c1, c2, c3};
+      uint32_t ca[4] = {c1, (uint32_t)(2 * (step / per)), c2, c3};
       philox4x32(ca, k0, k1, u);
     }
     double dir[3];

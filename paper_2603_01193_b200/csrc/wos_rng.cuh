@@ -74,38 +74,50 @@ __device__ __forceinline__ uint4 philox4x32_rk(uint4 c, const uint32_t* rk0, con
   return c;
 }
 
-// A walk draws blocks at counters (2 step, c1, c2, c3) with c1..c3 fixed for the walk.
-// Round 0 multiplies only c0 (varies) and c2 (fixed); its outputs x0 = hi(M1 c2) ^ c1
-// ^ k0 and x1 = lo(M1 c2) are fixed, so round 1's product M0 x0 is fixed as well.
-// Precomputing those words once per walk leaves two of the first four IMAD.WIDE and
-// one XOR per block; the output is bit-identical to philox4x32.
+// A walk draws blocks at counters (c0, b, c2, c3): c0 = low point id, b = the block
+// index (2 floor(step / jumps per block)), c2 = low traj id, c3 = the high words mixed;
+// only b varies along a walk. Philox multiplies words 0 and 2 of its state, so with the
+// varying word in position 1:
+//   round 0 multiplies c0 and c2 — both products are per-walk constants;
+//   round 1 multiplies x0' = hi(M1 c2) ^ b ^ k0 (varies) and x2' (constant);
+//   round 2 multiplies x0'' (constant again) and x2'' (varies).
+// Precomputing the constant products once per walk (four IMAD.WIDE at the walk start)
+// leaves two of the first six multiplies per block; the output is bit-identical to
+// philox4x32 on the counter (c0, b, c2, c3).
 struct PhiloxPre {
-  uint32_t e;   // c3 ^ k1(0)
-  uint32_t bk;  // lo(M1 c2) ^ k0(1)
-  uint32_t hk;  // hi(M0 x0) ^ k1(1)
-  uint32_t lw;  // lo(M0 x0)
+  uint32_t a0;   // hi(M1 c2) ^ k0(0)               x0' = a0 ^ b
+  uint32_t e1;   // lo(M0 c0) ^ k1(1)               x2'' = hi(M0 x0') ^ e1
+  uint32_t b1k;  // lo(M1 x2') ^ k0(2)              state word 0 after round 2 = hi(M1 x2'') ^ b1k
+  uint32_t ch2;  // hi(M0 x0'') ^ k1(2)             state word 2 after round 2 = ch2 ^ lo(M0 x0')
+  uint32_t cl;   // lo(M0 x0'')                     state word 3 after round 2
 };
 
-__device__ __forceinline__ PhiloxPre philox_pre(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k00,
-                                                uint32_t k10, uint32_t k01, uint32_t k11) {
-  const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-  const uint32_t x0 = (uint32_t)(p1 >> 32) ^ c1 ^ k00;
-  const uint64_t p0 = (uint64_t)0xD2511F53u * x0;
-  return PhiloxPre{c3 ^ k10, (uint32_t)p1 ^ k01, (uint32_t)(p0 >> 32) ^ k11, (uint32_t)p0};
+__device__ __forceinline__ PhiloxPre philox_pre(uint32_t c0, uint32_t c2, uint32_t c3, uint32_t k00, uint32_t k10,
+                                                uint32_t k01, uint32_t k11, uint32_t k02, uint32_t k12) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint64_t p1 = (uint64_t)M1 * c2;  // round 0
+  const uint64_t p0 = (uint64_t)M0 * c0;
+  const uint32_t x1 = (uint32_t)p1;
+  const uint32_t x2 = (uint32_t)(p0 >> 32) ^ c3 ^ k10;
+  const uint64_t s = (uint64_t)M1 * x2;  // round 1, word 2 (constant)
+  const uint32_t b0 = (uint32_t)(s >> 32) ^ x1 ^ k01;
+  const uint64_t t = (uint64_t)M0 * b0;  // round 2, word 0 (constant)
+  return PhiloxPre{(uint32_t)(p1 >> 32) ^ k00, (uint32_t)p0 ^ k11, (uint32_t)s ^ k02,
+                   (uint32_t)(t >> 32) ^ k12, (uint32_t)t};
 }
 
-// rounds 0 and 1 from the precomputed words: the state entering round 2
-__device__ __forceinline__ uint4 philox_pre_r01(uint32_t c0, const PhiloxPre& p) {
-  const uint64_t q0 = (uint64_t)0xD2511F53u * c0;                   // round 0, word 0
-  const uint64_t q1 = (uint64_t)0xCD9E8D57u * ((uint32_t)(q0 >> 32) ^ p.e);  // round 1, word 2
-  return make_uint4((uint32_t)(q1 >> 32) ^ p.bk, (uint32_t)q1, p.hk ^ (uint32_t)q0, p.lw);
+// rounds 0-2 from the precomputed words: the state entering round 3
+__device__ __forceinline__ uint4 philox_pre_r012(uint32_t b, const PhiloxPre& p) {
+  const uint64_t q = (uint64_t)0xD2511F53u * (p.a0 ^ b);                // round 1, word 0
+  const uint64_t r = (uint64_t)0xCD9E8D57u * ((uint32_t)(q >> 32) ^ p.e1);  // round 2, word 2
+  return make_uint4((uint32_t)(r >> 32) ^ p.b1k, (uint32_t)r, p.ch2 ^ (uint32_t)q, p.cl);
 }
 
-__device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t c0, const PhiloxPre& p, const uint32_t* rk0,
+__device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t b, const PhiloxPre& p, const uint32_t* rk0,
                                                    const uint32_t* rk1, int rounds) {
-  uint4 c = philox_pre_r01(c0, p);
+  uint4 c = philox_pre_r012(b, p);
 #pragma unroll
-  for (int r = 2; r < kPhiloxRoundsFast; ++r) philox4x32_round(c, rk0[r], rk1[r]);
+  for (int r = 3; r < kPhiloxRoundsFast; ++r) philox4x32_round(c, rk0[r], rk1[r]);
   if (rounds > kPhiloxRoundsFast) {
 #pragma unroll
     for (int r = kPhiloxRoundsFast; r < kPhiloxRoundsDefault; ++r) philox4x32_round(c, rk0[r], rk1[r]);
@@ -113,13 +125,13 @@ __device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t c0, const PhiloxPre&
   return c;
 }
 
-__device__ __forceinline__ uint4 philox4x32_pre(uint32_t c0, const PhiloxPre& p, uint32_t k0, uint32_t k1,
+__device__ __forceinline__ uint4 philox4x32_pre(uint32_t b, const PhiloxPre& p, uint32_t k0, uint32_t k1,
                                                 int rounds) {
-  uint4 c = philox_pre_r01(c0, p);
-  k0 += 2u * 0x9E3779B9u;
-  k1 += 2u * 0xBB67AE85u;
+  uint4 c = philox_pre_r012(b, p);
+  k0 += 3u * 0x9E3779B9u;
+  k1 += 3u * 0xBB67AE85u;
 #pragma unroll
-  for (int r = 2; r < kPhiloxRoundsFast; ++r) {
+  for (int r = 3; r < kPhiloxRoundsFast; ++r) {
     philox4x32_round(c, k0, k1);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;

@@ -28,11 +28,11 @@
 // Numerics per mode:
 //   REPLAY_F64 / REPLAY_F32 follow walker._poisson_generic (walker.py:257-314)
 //   operation by operation, on Philox4x64 draws identical to the reference's.
-//   NATIVE_F32 samples the source term from the ball Green's function
-//   (radius d*sqrt(U1 U2) in 2D, d*Beta(2,2) as the median of three uniforms in
-//   3D) with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2,
-//   and ONE Philox4x32 block per jump (counter (2*step, pid, tid, hi-words); 10
-//   rounds, or 7 with WalkConfig.philox_rounds = 7);
+//   NATIVE_F32 samples the source term from the ball Green's function (radius
+//   fraction from a 12-bit table of the disk Green's law in 2D, of Beta(2,2) in 3D)
+//   with weight r^2/(2 dim) (greens.py:83-89), uses MUFU sin/cos/sqrt/ex2, and
+//   Philox4x32 blocks at counter (pid, 2 floor(step / jumps per block), tid,
+//   hi-words) (10 rounds, or 7 with WalkConfig.philox_rounds = 7);
 //   a source jump takes 64 bits (two jumps per block; jump_source below, with the
 //   radius from a staged table; oracle/wos_oracle.c restates it);
 //   source-free jumps share a block between 4 (2D) / 2 (3D) consecutive jumps
@@ -1370,24 +1370,26 @@ struct Walker {
 #define WOS_HOT_FOLD 1
 #endif
     if constexpr (kHot && WOS_HOT_FOLD) return philox4x32_rk_pre(c0, l.pc, l.hk0, l.hk1, rounds);
-    else if constexpr (kHot) return philox4x32_rk(make_uint4(c0, l.c1, l.c2, l.c3), l.hk0, l.hk1, rounds);
+    else if constexpr (kHot) return philox4x32_rk(make_uint4(l.c1, c0, l.c2, l.c3), l.hk0, l.hk1, rounds);
     else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1, rounds);
     else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1, rounds);
   }
 
-  // the walk's Philox counter words (c1, c2, c3) folded through rounds 0-1 (wos_rng.cuh)
+  // the walk's fixed Philox counter words folded through rounds 0-2 (wos_rng.cuh): the
+  // counter is (c1, block, c2, c3), c1 = low point id, c2 = low traj id, c3 = high words
   __device__ static __forceinline__ void set_counter(Lane& l, const KArgs& a, uint32_t c1, uint32_t c2,
                                                      uint32_t c3) {
     if constexpr (kHot && WOS_HOT_FOLD) {
-      l.pc = philox_pre(c1, c2, c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+      l.pc = philox_pre(c1, c2, c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2], l.hk1[2]);
     } else if constexpr (kHot) {
       l.c1 = c1;
       l.c2 = c2;
       l.c3 = c3;
     }
-    else if constexpr (ONE) l.pc = philox_pre(c1, c2, c3, a.rk0[0], a.rk1[0], a.rk0[1], a.rk1[1]);
+    else if constexpr (ONE) l.pc = philox_pre(c1, c2, c3, a.rk0[0], a.rk1[0], a.rk0[1], a.rk1[1], a.rk0[2], a.rk1[2]);
     else
-      l.pc = philox_pre(c1, c2, c3, a.nkey0, l.k1, a.nkey0 + 0x9E3779B9u, l.k1 + 0xBB67AE85u);
+      l.pc = philox_pre(c1, c2, c3, a.nkey0, l.k1, a.nkey0 + 0x9E3779B9u, l.k1 + 0xBB67AE85u,
+                        a.nkey0 + 2u * 0x9E3779B9u, l.k1 + 2u * 0xBB67AE85u);
   }
 
   // source-free NATIVE jumps from their words of the block (kPerBlock above)
@@ -2100,7 +2102,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const uint32_t blk_new = (cu_k % kSlots) * 4u;
         if (cu_fastc) {
           const uint32_t c2 = cu_c2b + (jr & anti_jmask);
-          const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+          const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2], l.hk1[2]);
           if (take && real) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) s.x[i] = cu_x[i];
@@ -2277,7 +2279,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint32_t blk_new = (cu_k % kSlots) * 4u;
           if (cu_fastc) {
             const uint32_t c2 = cu_c2b + (jr & anti_jmask);
-            const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1]);
+            const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2], l.hk1[2]);
             if (take && real) {
 #pragma unroll
               for (int i = 0; i < DIM; ++i) l.x[i] = cu_x[i];

@@ -6,8 +6,8 @@
 * The opt-in 7-round stream (WalkConfig.philox_rounds = 7) walks exactly like the
   oracle's restatement with 7 rounds, differs from the 10-round stream, and its
   estimates agree with the reference form within combined standard errors.
-* Statistics of the 7-round words in the walk's own counter layout (c0 = 2 step,
-  c1 = point id, c2 = traj id): per-bit frequencies, serial correlation between a
+* Statistics of the 7-round words in the walk's own counter layout (c0 = point id,
+  c1 = 2 x block index, c2 = traj id): per-bit frequencies, serial correlation between a
   walk's consecutive blocks and between neighbouring walks, byte chi-square, and the
   strict avalanche criterion for single-bit counter changes. (Random123 reports
   Philox4x32-7 as the fewest rounds that pass TestU01 Crush; these tests check the
@@ -86,13 +86,13 @@ def test_seven_round_estimates_match_reference_form(gpu, cfg, npts, L):
 
 
 def _walk_counters(n_walks, n_steps, pid0=12345):
-    """Counters of n_walks walks x n_steps blocks in the walk layout (c0 = 2 step,
-    c1 = point id, c2 = traj id, c3 = 0), step-major within a walk."""
+    """Counters of n_walks walks x n_steps blocks in the walk layout (c0 = point id,
+    c1 = 2 x block index, c2 = traj id, c3 = 0), block-major within a walk."""
     s = torch.arange(n_steps, device="cuda", dtype=torch.int64)
     t = torch.arange(n_walks, device="cuda", dtype=torch.int64)
     c = torch.zeros((n_walks, n_steps, 4), dtype=torch.int64, device="cuda")
-    c[:, :, 0] = 2 * s[None, :]
-    c[:, :, 1] = pid0 + (t[:, None] // 256)
+    c[:, :, 1] = 2 * s[None, :]
+    c[:, :, 0] = pid0 + (t[:, None] // 256)
     c[:, :, 2] = t[:, None] % 256
     return c.reshape(-1, 4).to(torch.int32)
 
@@ -163,7 +163,7 @@ def test_beta22_radius_moments_over_1e9_draws(gpu, rounds):
     n_chunks = 15  # 15 x 2^25 blocks x 2 jumps = 1.007e9 draws
     for k in range(n_chunks):
         i = torch.arange(chunk, device="cuda", dtype=torch.int64) + k * chunk
-        c = torch.stack([2 * (i % 1000), 77 + i // (1000 * 4096), (i // 1000) % 4096, torch.zeros_like(i)],
+        c = torch.stack([77 + i // (1000 * 4096), 2 * (i % 1000), (i // 1000) % 4096, torch.zeros_like(i)],
                         dim=1).to(torch.int32)
         w = _blocks(gpu, c, 0x5EED, 0xC0FFEE, rounds).to(torch.int64) & 0xFFFFFFFF
         for wa, wb in ((w[:, 0], w[:, 1]), (w[:, 2], w[:, 3])):
