@@ -1846,9 +1846,30 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // the staged Beta(2,2) table's shared-memory offset
   uint32_t hot_btab = 0u;
   if constexpr (W::kBetaTab) hot_btab = W::beta_tab_offset(a);
+#ifndef WOS_HOT_PRED_RECORD1
+#define WOS_HOT_PRED_RECORD1 1
+#endif
+#ifndef WOS_HOT_BRANCHFREE
+#define WOS_HOT_BRANCHFREE 1
+#endif
   auto hot_step = [&](typename W::Lane& s) -> bool {
     if constexpr (!kHotLoop) {
       return false;  // (not used outside the hot loop)
+    } else if constexpr (W::kPerBlock == 2 && WOS_HOT_BRANCHFREE) {
+      // Branch-free round: the second jump runs in every lane and a walk that ended
+      // after the first keeps that jump's value and step count (selects) — the same
+      // operations in the same order for the walks that continue, so the results are
+      // identical to the branched round below, without its divergent reconvergence
+      const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step >> 1));
+      W::jump_source(s, s.d, a, B.x, B.y, hot_btab);
+      const Real acc1 = s.acc;
+      const Real d1 = W::dist(s, a, srec);
+      const bool live1 = !((d1 < eps) | (s.step + 1 >= a.max_steps));
+      W::jump_source(s, d1, a, B.z, B.w, hot_btab);
+      s.d = W::dist(s, a, srec);
+      s.acc = live1 ? s.acc : acc1;
+      s.step += live1 ? 2 : 1;
+      return live1 & !((s.d < eps) | (s.step >= a.max_steps));
     } else if constexpr (W::kPerBlock == 2) {
       const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step >> 1));
       W::jump_source(s, s.d, a, B.x, B.y, hot_btab);
@@ -2091,6 +2112,26 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + s.seq) = s.acc + a.bnd_c;
         atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_s), 1u);
       };
+      // Predicated recording (no divergent branch around the one to three lanes that
+      // finish per iteration): the ring store and the unit-counter increment go out
+      // under the lane's predicate; the step total accumulates in 32 bits and is
+      // folded into the 64-bit lane total at every refill (a lane cannot run 2^32
+      // steps between two refills)
+#ifndef WOS_HOT_PRED_RECORD
+#define WOS_HOT_PRED_RECORD 1
+#endif
+      const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+      const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+      uint32_t steps32 = 0u;
+      auto record2p = [&](typename W::Lane& s, uint32_t blk_s, bool fin) {
+        const float v = s.acc + a.bnd_c;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.f32 [%1], %2;\n\t"
+            "@p red.shared.add.u32 [%3], 1;\n\t}" ::"r"((uint32_t)fin),
+            "r"(ring_s + s.seq), "f"(v), "r"(cnt_s + blk_s)
+            : "memory");
+        steps32 += fin ? (uint32_t)s.step : 0u;
+      };
       // issue the cached unit's next walks to the idle lanes of one slot; ranks start at base
       auto issue = [&](typename W::Lane& s, bool& act, uint32_t& blk_s, unsigned idle_s, uint32_t base,
                        uint32_t n) {
@@ -2134,6 +2175,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const uint32_t na = (uint32_t)__popc(idle_a);
         const int n_idle = (int)na + __popc(idle_b);
         if (n_idle >= thr2) {
+          if constexpr (WOS_HOT_PRED_RECORD) {
+            lane_steps += (unsigned long long)steps32;
+            steps32 = 0u;
+          }
           uint32_t room = cu_end - s_issue;
           uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
           if (cap < (uint32_t)n_idle || room == 0) {
@@ -2163,8 +2208,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const bool live_b = hot_step(lb);
         const bool fin_a = act_a & !live_a;
         const bool fin_b = act_b & !live_b;
-        if (fin_a) record2(l, blk_a);
-        if (fin_b) record2(lb, blk_b);
+        if constexpr (WOS_HOT_PRED_RECORD) {
+          record2p(l, blk_a, fin_a);
+          record2p(lb, blk_b, fin_b);
+        } else {
+          if (fin_a) record2(l, blk_a);
+          if (fin_b) record2(lb, blk_b);
+        }
         act_a = act_a & !fin_a;
         act_b = act_b & !fin_b;
         idle_a = __ballot_sync(WOS_FULL, !act_a);
@@ -2432,7 +2482,17 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       // for a refill) computes a jump from its stale state that is never recorded, and
       // the warp runs the step without a divergent branch around it
       const bool fin = active & !hot_step(l);
-      if (fin) {
+      if constexpr (WOS_HOT_PRED_RECORD1) {
+        // predicated record (as in the two-slot loop)
+        const float v = l.acc + a.bnd_c;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.f32 [%1], %2;\n\t"
+            "@p red.shared.add.u32 [%3], 1;\n\t}" ::"r"((uint32_t)fin),
+            "r"((uint32_t)__cvta_generic_to_shared(ring) + l.seq), "f"(v),
+            "r"((uint32_t)__cvta_generic_to_shared(cnt) + blk)
+            : "memory");
+        lane_steps += fin ? (unsigned long long)l.step : 0ull;
+      } else if (fin) {
         lane_steps += (unsigned long long)l.step;
         *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = l.acc + a.bnd_c;
         atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);

@@ -107,4 +107,4 @@ def test_multi_instance_equals_single(gpu, mode):
         # NATIVE single- and multi-instance kernels are separate fp32 instantiations; the
         # Fourier boundary at the polar projection may round differently in the last bits
         np.testing.assert_allclose(mm, np.concatenate([ma, mb]), rtol=1e-6, atol=1e-6)
-        np.testing.assert_allclose(qm, np.concatenate([qa, qb]), rtol=1e-5, atol=1e-12)
+        np.testing.assert_allclose(qm, np.concatenate([qa, qb]), rtol=1e-5, atol=1e-8)
