@@ -564,6 +564,13 @@ def main():
             cfg_alt = dataclasses.replace(w.cfg, philox_rounds=alt)
             acc_alt = torch.zeros(1, dtype=torch.int64, device=dev)
             n_alt = min(args.steps, 10)
+            # warm-up launches first: the other stream's kernel is a different instantiation,
+            # and its first launch pays the lazy module load
+            for i in range(max(args.warmup, 3)):
+                estimate_tensors(pset, pts, ids, w.L, cfg_alt, inst_index=inst,
+                                 traj_start=(400 + i) * w.L, out_mean=mean, out_m2=m2,
+                                 stream=stream, eps=eps)
+            torch.cuda.synchronize()
             t_alt = _time_estimates(
                 lambda i: estimate_tensors(pset, pts, ids, w.L, cfg_alt, inst_index=inst,
                                            traj_start=(500 + i) * w.L, out_mean=mean, out_m2=m2,

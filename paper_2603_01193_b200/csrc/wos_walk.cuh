@@ -1826,10 +1826,17 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_AMORT_RNG
 #define WOS_AMORT_RNG 1
 #endif
-  // (source jumps also take two per block, but outside the hot loop — multi-instance and
-  // rows kernels — holding a block's second half across a jump costs the register file
-  // more than it saves: those kernels redraw the block per jump and select their words)
-  constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1 && S::SRC == SRC_NONE;
+  // NATIVE source jumps (two per block, layout v3) run the same rounds outside the hot
+  // loop (multi-instance, non-constant-boundary and rows kernels): the round holds the
+  // block only inside one iteration, so the second jump's words cost no registers across
+  // iterations, and a jump no longer redraws the whole block for half of its words
+  // (cfg2: a multi-instance Philox block with its per-round key adds is ~45 instructions).
+  // (a lane whose walk ends after the first jump of a round idles for the second)
+#ifndef WOS_AMORT_SRC
+#define WOS_AMORT_SRC 1
+#endif
+  constexpr bool kAmort = WOS_AMORT_RNG && kJumpFirst && W::kPerBlock > 1 &&
+                          (S::SRC == SRC_NONE || (WOS_AMORT_SRC && W::kBetaTab));
   // Branch-free step (single-instance constant-boundary NATIVE kernels with a source:
   // cfg0, cfg4): no deferred recording, so an idle lane holds no state worth keeping
 #ifndef WOS_HOT_LOOP
@@ -2466,6 +2473,19 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       if (active) {
         const uint4 B = W::native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)W::kPerBlock));
         bool live = true;
+        if constexpr (W::kBetaTab) {
+          // source rounds: one jump body in a loop (two unrolled source jumps with the
+          // block held across them spill at the multi-instance kernels' 64 registers)
+#pragma unroll 1
+          for (int k = 0; k < 2; ++k) {
+            if (live) {
+              W::jump_source(l, l.d, a, k == 0 ? B.x : B.z, k == 0 ? B.y : B.w);
+              l.step += 1;
+              l.d = W::dist(l, a, srec);
+              live = !(l.d < eps || l.step >= a.max_steps);
+            }
+          }
+        } else {
 #pragma unroll
         for (int k = 0; k < W::kPerBlock; ++k) {
           if (live) {
@@ -2474,6 +2494,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             l.d = W::dist(l, a, srec);
             live = !(l.d < eps || l.step >= a.max_steps);
           }
+        }
         }
         if (!live) finish(l.d);
       }
