@@ -418,17 +418,25 @@ def main():
     from paper_2603_01193_b200.distributed import gather_estimates, shard_indices
     from paper_2603_01193_b200.estimator import estimate_tensors
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # WOS_BENCH_BACKEND / WOS_BENCH_DEVICE exist only to exercise the multi-rank code path
+    # on a one-GPU box (gloo, every rank on one device; each rank's kernels independent):
+    # the measured configuration is NCCL with one GPU per rank
+    backend = os.environ.get("WOS_BENCH_BACKEND", "nccl")
+    dev_index = _env_int("WOS_BENCH_DEVICE", local)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     replicas = args.replicas or 1
     w = configs.build(args.config, mode=args.mode).replicate(replicas)
     w.cfg = dataclasses.replace(w.cfg, philox_rounds=args.philox_rounds)
     idx = shard_indices(w.n_points, rank, world)
     shard = w.subset(idx)
-    ctx = engine.get_context(local)
+    ctx = engine.get_context(dev_index)
     if args.refill_min or args.blocks_per_sm or args.refill_min_deferred:
         ctx.set_tuning(args.refill_min or 5, args.blocks_per_sm or 0, args.refill_min_deferred or 12)
     pset = engine.ProblemSet(ctx, w.problems)
@@ -457,7 +465,7 @@ def main():
         raise RuntimeError(f"estimate flagged an error during warm-up: exterior {first}, watchdog {watchdog}")
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

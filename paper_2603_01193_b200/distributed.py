@@ -60,10 +60,11 @@ def gather_estimates(mean, m2, n_points: int, rank: int, world: int, group=None)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world,) + tuple(buf.shape), dtype=mean.dtype, device=mean.device)
         dist.all_gather_into_tensor(out, buf, group=group)
-    else:
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf, group=group)
-        out = torch.stack(parts)
+    else:  # gloo gathers host tensors
+        host = buf.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        out = torch.stack(parts).to(buf.device)
     return unpack_gathered(out, n_points)
 
 
