@@ -125,6 +125,8 @@ struct wos_problem_set {
   size_t bytes_polar_d = 0, bytes_polar_f = 0;
   std::vector<float> h_row_n;             // NATIVE row of problem 0 (single-instance launches)
   std::vector<float> h_row_n_scaled;      // ... with the box in X = pi x (scaled-coordinate kernels)
+  std::vector<float> h_row_n_cube;        // ... a cube centred at 1/2 in X = pi (x - 1/2) (DOM_CUBE)
+  bool cube = false;                      // problem 0's box is such a cube (and the source monomial)
   double scr_sprime_max = -1.0;           // SRC_SCR_CONST: largest s' of the set (majorant check)
   uint32_t h_nkey1 = 0;                   // its InstHdr::nkey1
 };
@@ -1084,6 +1086,21 @@ extern "C" int wos_problem_set_create(wos_context* ctx, const wos_problem* probs
       const double w = 1.0 / (2.0 * s->dim * M_PI * M_PI);
       for (int k = 0; k < ns; ++k)
         s->h_row_n_scaled[kSrcOff + k] = (float)((double)s->h_row_n[kSrcOff + k] * w);
+      // a cube centred at 1/2: the centred scaled row (centre 0; the monomial coefficient
+      // of c_0^p c_1^q (c_2^r) times (-1)^(p+q(+r)), since cos(pi x) = -sin X)
+      bool cube = true;
+      for (int k = 0; k < s->dim; ++k)
+        cube = cube && td[k] + td[4 + k] == 1.0 && td[4 + k] - td[k] == td[4] - td[0];
+      if (cube) {
+        s->cube = true;
+        s->h_row_n_cube = s->h_row_n_scaled;
+        const int K = s->sk_native;
+        for (int k = 0; k < s->dim; ++k) s->h_row_n_cube[8 + k] = 0.0f;
+        for (int k = 0; k < ns; ++k) {
+          const int deg = s->dim == 2 ? k / K + k % K : k / (K * K) + (k / K) % K + k % K;
+          if (deg & 1) s->h_row_n_cube[kSrcOff + k] = -s->h_row_n_cube[kSrcOff + k];
+        }
+      }
     }
   }
   s->h_nkey1 = hd[0].nkey1;
@@ -1372,10 +1389,11 @@ struct KernelInfo {
   const void* fn;
   size_t elem;  // sizeof(Real)
   bool one;     // single-instance NATIVE launch (parameters in the constant bank)
+  bool cube;    // ... walking a cube centred at 1/2 in centred scaled coordinates (DOM_CUBE)
 };
 
 static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int rounds) {
-  KernelInfo k{nullptr, 8, false};
+  KernelInfo k{nullptr, 8, false, false};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
     k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0, rows);
@@ -1386,7 +1404,10 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int
   } else {
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
     k.one = (s->n == 1 && s->stride <= kCP);
-    k.fn = get_kernel_native(s->dim, dom, s->src_kind, sk, k.one, rows, s->bnd_kind == WOS_BND_CONST, rounds);
+    k.cube = WOS_CENTERED_CUBE && WOS_SCALED_COORDS && k.one && !rows && s->cube &&
+             s->bnd_kind == WOS_BND_CONST;
+    k.fn = get_kernel_native(s->dim, k.cube ? DOM_CUBE : dom, s->src_kind, sk, k.one, rows,
+                             s->bnd_kind == WOS_BND_CONST, rounds);
     k.elem = 4;
   }
   return k;
@@ -1440,7 +1461,8 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
       scaled = WOS_SCALED_COORDS && a.sink == SINK_ESTIMATE && s->bnd_kind == WOS_BND_CONST &&
                s->dom_kind == WOS_DOM_BOX && s->src_kind == WOS_SRC_SINE &&
                (s->sk_native == 3 || s->sk_native == 4);
-      memcpy(a.cp, (scaled ? s->h_row_n_scaled : s->h_row_n).data(), sizeof(float) * s->stride);
+      memcpy(a.cp, (k.cube ? s->h_row_n_cube : scaled ? s->h_row_n_scaled : s->h_row_n).data(),
+             sizeof(float) * s->stride);
       a.bnd_c = s->h_row_n[s->bnd_off];
       const uint32_t k0 = (uint32_t)cfg->rng_seed;
       const uint32_t k1 = (uint32_t)(cfg->rng_seed >> 32) ^ s->h_nkey1;

@@ -5,6 +5,9 @@
 namespace wos {
 
 enum : int { DOM_BALL = 0, DOM_POLAR = 1, DOM_BOX = 2, DOM_POLY = 3, DOM_MESH = 4 };
+// internal NATIVE kernel code (never a problem's domain): a cube centred at 1/2 walked in
+// centred scaled coordinates X = pi (x - 1/2) (wos_walk.cuh Walker::kCentered)
+enum : int { DOM_CUBE = 5 };
 enum : int { SRC_NONE = 0, SRC_CONST = 1, SRC_RBF2 = 2, SRC_SINE = 3, SRC_GAUSS = 4 };
 // delta-tracking (screened) walks: the "source" slot selects the transformed coefficients
 enum : int { SRC_SCR_CONST = 5, SRC_SCR_VC = 6 };
@@ -26,6 +29,10 @@ constexpr int kWarps = kBlock / 32;
 // X = pi x (wos_walk.cuh Walker::kScaled; the host scales box and eps to match)
 #ifndef WOS_SCALED_COORDS
 #define WOS_SCALED_COORDS 1
+#endif
+// cubes centred at 1/2 (BASELINE cfg0 / cfg4) walk in centred scaled coordinates
+#ifndef WOS_CENTERED_CUBE
+#define WOS_CENTERED_CUBE 1
 #endif
 // polygon candidate grids: 16-byte cell records with up to four pair indices inline
 // (one dependent load fewer per query; wos_capi.cu build, wos_walk.cuh poly_grid_scan)

@@ -189,7 +189,7 @@ struct Walker {
   // ---------------- domains ----------------
   // distance to the boundary (positive inside)
   __device__ static __forceinline__ Real dist(Lane& l, const KArgs& a, const float4* srec) {
-    if constexpr (S::DOM == DOM_BALL || S::DOM == DOM_BOX) return dist_at(l, a, l.x);
+    if constexpr (S::DOM == DOM_BALL || S::DOM == DOM_BOX || S::DOM == DOM_CUBE) return dist_at(l, a, l.x);
     else if constexpr (S::DOM == DOM_POLAR) {
       Real qx, qy;
       return polar_query(l, a, srec, l.x[0], l.x[1], &qx, &qy);
@@ -215,6 +215,12 @@ struct Walker {
       }
       if constexpr (S::NATIVE) return domp(l, a, 3) - fast_sqrt(s);
       else return pabs(domp(l, a, 3) - psqrt(s));
+    } else if constexpr (S::DOM == DOM_CUBE) {
+      // centred cube in X = pi (x - 1/2): h - max |X_i| (one FMNMX3 with |.| operands)
+      Real m = fabsf(x[0]);
+#pragma unroll
+      for (int i = 1; i < DIM; ++i) m = fmaxf(m, fabsf(x[i]));
+      return domp(l, a, 12) - m;
     } else {
       static_assert(S::DOM == DOM_BOX, "dist_at: closed-form domains only");
       if constexpr (S::NATIVE) {
@@ -472,6 +478,10 @@ struct Walker {
         const Real dir = (rho == Real(0)) ? (i == 0 ? Real(1) : Real(0)) : u[i] / rho;
         q[i] = domp(l, a, i) + R * dir;
       }
+    } else if constexpr (S::DOM == DOM_CUBE) {
+      // (constant-boundary kernels only: their walk value needs no exit point)
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) q[i] = l.x[i];
     } else if constexpr (S::DOM == DOM_BOX) {
       // first nearest face (axis order, lower before upper) — strict <
       Real best = l.x[0] - domp(l, a, 0), face = domp(l, a, 0);
@@ -635,12 +645,20 @@ struct Walker {
   // source terms sin(k pi x) take MUFU arguments without the pi multiply (three fewer
   // FMUL per 3D jump); the Green weight carries 1/pi^2. The walk value acc + g needs no
   // exit point, so nothing is scaled back. wos_capi.cu launch_walk mirrors this test.
-  static constexpr bool kScaled =
-      WOS_SCALED_COORDS && kMonomial && ONE && S::BC && S::DOM == DOM_BOX && S::SINK == SINK_ESTIMATE;
+  static constexpr bool kScaled = WOS_SCALED_COORDS && kMonomial && ONE && S::BC &&
+                                  (S::DOM == DOM_BOX || S::DOM == DOM_CUBE) && S::SINK == SINK_ESTIMATE;
+  // Centred scaled coordinates (DOM_CUBE: a cube centred at 1/2, BASELINE cfg0 / cfg4):
+  // X = pi (x - 1/2), so the distance is h - max_i |X_i| (FMNMX3 with |.| operands + one
+  // FADD instead of 3 FADD + 3 FADD + FMNMX3 per 3D jump). The source keeps its form:
+  // sin(pi x) = cos X and cos(pi x) = -sin X, so the kernel swaps the sincos outputs and
+  // the host flips the sign of the odd-degree monomial coefficients (wos_capi.cu).
+  static constexpr bool kCentered = S::DOM == DOM_CUBE;
+  static_assert(!kCentered || kScaled, "DOM_CUBE kernels are scaled-coordinate kernels");
   static constexpr float kInvPi2F = 0.10132118364233778f;  // 1 / pi^2
   // a query point's coordinate in the walk's units (already-converted Real values pass)
   __device__ static __forceinline__ Real start_coord(double x) {
-    if constexpr (kScaled) return (Real)(kPi * x);
+    if constexpr (kCentered) return (Real)(kPi * (x - 0.5));
+    else if constexpr (kScaled) return (Real)(kPi * x);
     else return (Real)x;
   }
   __device__ static __forceinline__ Real start_coord(float x) { return x; }
@@ -650,7 +668,10 @@ struct Walker {
     if constexpr (kMonomial) {
       float s[DIM], c[DIM];
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) __sincosf(kScaled ? y[i] : kPiF * y[i], &s[i], &c[i]);
+      for (int i = 0; i < DIM; ++i) {
+        if constexpr (kCentered) __sincosf(y[i], &c[i], &s[i]);  // s <- cos X, c <- sin X
+        else __sincosf(kScaled ? y[i] : kPiF * y[i], &s[i], &c[i]);
+      }
       // Independent Horner chains run two at a time as packed FFMA2 (fma.rn.f32x2,
       // elementwise fma.rn): the same operations in the same order as scalar fmaf, so
       // bit-identical to it, at half the issue slots.
@@ -1465,7 +1486,7 @@ struct Walker {
   // single-instance box / ball launches (nothing else is staged before it), else after
   // the instance table and the polygon records. It is read with ld.shared on that 32-bit offset, so no generic address of
   // the shared window has to be rebuilt inside the loop.
-  static constexpr bool kBetaAtZero = ONE && (S::DOM == DOM_BOX || S::DOM == DOM_BALL);
+  static constexpr bool kBetaAtZero = ONE && (S::DOM == DOM_BOX || S::DOM == DOM_BALL || S::DOM == DOM_CUBE);
   __device__ static __forceinline__ uint32_t beta_tab_offset(const KArgs& a) {
     extern __shared__ __align__(16) unsigned char wos_smem_[];
     // the dynamic window's shared address (a link-time constant) plus what precedes it
@@ -1812,7 +1833,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_JUMP_FIRST
 #define WOS_JUMP_FIRST 1
 #endif
-  constexpr bool kJumpFirst = WOS_JUMP_FIRST && (S::DOM == DOM_BALL || S::DOM == DOM_BOX);
+  constexpr bool kJumpFirst = WOS_JUMP_FIRST && (S::DOM == DOM_BALL || S::DOM == DOM_BOX || S::DOM == DOM_CUBE);
   // Polygons run jump-first in the cached-point refill only: there a unit's start
   // distance (and nearest segment) is queried once per unit, not per walk
 #ifndef WOS_JUMP_FIRST_POLY
