@@ -33,7 +33,8 @@ UNITS = {
     "wos_kernels_native_est.cu": [],
     # the 10-round hot kernels (cfg4, cfg0) run two walks per lane at 3 CTAs/SM (80
     # registers): -2 to -3 % against one walk at 4 CTAs/SM; the 7-round ones do not
-    # gain from it (round 2)
+    # gain from it (round 2). (7-warp CTAs at 4 CTAs/SM, -DWOS_NW=7:
+    # 28 resident warps at 72 registers, were 1.7 % slower on cfg4)
     "wos_kernels_native_est_bc.cu": ["-DWOS_ILP2=1", "-DWOS_NATIVE_MINB=3"],
     "wos_kernels_native_est_r7.cu": [],
     "wos_kernels_native_est_bc_r7.cu": [],

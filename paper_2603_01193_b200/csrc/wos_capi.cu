@@ -1390,10 +1390,11 @@ struct KernelInfo {
   size_t elem;  // sizeof(Real)
   bool one;     // single-instance NATIVE launch (parameters in the constant bank)
   bool cube;    // ... walking a cube centred at 1/2 in centred scaled coordinates (DOM_CUBE)
+  int warps;    // warps per CTA the kernel is built for
 };
 
 static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int rounds) {
-  KernelInfo k{nullptr, 8, false, false};
+  KernelInfo k{nullptr, 8, false, false, kWarps};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
     k.fn = get_kernel_replay_f64(s->dim, dom, s->src_kind, 0, rows);
@@ -1407,7 +1408,7 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int
     k.cube = WOS_CENTERED_CUBE && WOS_SCALED_COORDS && k.one && !rows && s->cube &&
              s->bnd_kind == WOS_BND_CONST;
     k.fn = get_kernel_native(s->dim, k.cube ? DOM_CUBE : dom, s->src_kind, sk, k.one, rows,
-                             s->bnd_kind == WOS_BND_CONST, rounds);
+                             s->bnd_kind == WOS_BND_CONST, rounds, &k.warps);
     k.elem = 4;
   }
   return k;
@@ -1418,8 +1419,8 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int
 #endif
 static const size_t kSegStageMax = WOS_SEG_STAGE_MAX;  // polygon records staged per CTA at most
 
-static size_t smem_bytes(size_t stage, size_t elem) {
-  return stage + (size_t)kWarps * (kRing * elem + kSlots * 4 + kUQ * 4);
+static size_t smem_bytes(size_t stage, size_t elem, int warps) {
+  return stage + (size_t)warps * (kRing * elem + kSlots * 4 + kUQ * 4);
 }
 
 static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_config* cfg,
@@ -1522,7 +1523,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     a.beta_stage_bytes = (int)(sizeof(float) * WOS_BETA_TABLE_N);
   }
   const size_t smem =
-      smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes + (size_t)a.beta_stage_bytes, k.elem);
+      smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes + (size_t)a.beta_stage_bytes, k.elem, k.warps);
   if (smem > 220 * 1024)
     return fail(WOS_ERR_UNSUPPORTED,
                 "problem table too large for shared memory (%zu bytes); split the batch",
@@ -1535,14 +1536,14 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
       per_sm = it->second.second;
     } else {
       CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kBlock, smem));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, 32 * k.warps, smem));
       c->launch_cache[k.fn] = std::make_pair(smem, per_sm);
     }
   }
   if (per_sm < 1) return fail(WOS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   if (c->blocks_per_sm > 0) per_sm = std::min(per_sm, c->blocks_per_sm);
   int64_t grid = (int64_t)c->num_sms * per_sm;
-  grid = std::min<int64_t>(grid, ((int64_t)a.n_units + kWarps - 1) / kWarps);
+  grid = std::min<int64_t>(grid, ((int64_t)a.n_units + k.warps - 1) / k.warps);
   grid = std::max<int64_t>(grid, 1);
   unsigned slot = c->next_counter.fetch_add(1) % kCounterRing;
   a.work_counter = c->d_counters + slot;
@@ -1551,7 +1552,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   CUDA_TRY(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned), st));
   void* args[] = {&a};
   a.seg_evals = c->d_perf;
-  CUDA_TRY(cudaLaunchKernel(k.fn, dim3((unsigned)grid), dim3(kBlock), args, smem, st));
+  CUDA_TRY(cudaLaunchKernel(k.fn, dim3((unsigned)grid), dim3(32 * k.warps), args, smem, st));
   wos_context_count_launch(c);
   return WOS_OK;
 }

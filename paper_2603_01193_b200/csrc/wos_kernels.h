@@ -10,9 +10,10 @@ const void* get_kernel_replay_f32(int dim, int dom, int src, int sk, bool rows);
 // one = single-instance launch (instance row + Philox keys in the kernel parameters);
 // bnd_const = the boundary value is a constant (single-instance estimate kernels
 // then drop the deferred-recording path); rounds = Philox4x32 rounds (10 or 7: the
-// single-instance estimate kernels are compiled for each)
+// single-instance estimate kernels are compiled for each); *warps = the kernel's warps
+// per CTA
 const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const,
-                              int rounds);
+                              int rounds, int* warps);
 // fast-math primitives of the NATIVE kernels on given arguments (returns a cudaError_t)
 int launch_fastmath_probe(int64_t n, const float* x, float* s, float* c, float* q, float* e, void* stream);
 }  // namespace wos

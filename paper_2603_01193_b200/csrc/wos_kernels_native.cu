@@ -9,12 +9,27 @@ const void* get_kernel_native_est_bc(int dim, int dom, int src, int sk, bool one
 const void* get_kernel_native_est_r7(int dim, int dom, int src, int sk, bool one);
 const void* get_kernel_native_est_bc_r7(int dim, int dom, int src, int sk, bool one);
 
+int get_kernel_native_est_warps();
+int get_kernel_native_rows_warps();
+int get_kernel_native_est_bc_warps();
+int get_kernel_native_est_r7_warps();
+int get_kernel_native_est_bc_r7_warps();
+
 const void* get_kernel_native(int dim, int dom, int src, int sk, bool one, bool rows, bool bnd_const,
-                              int rounds) {
-  if (rows) return get_kernel_native_rows(dim, dom, src, sk, one);
-  if (one && rounds == kPhiloxRoundsFast)
+                              int rounds, int* warps) {
+  if (rows) {
+    *warps = get_kernel_native_rows_warps();
+    return get_kernel_native_rows(dim, dom, src, sk, one);
+  }
+  if (one && rounds == kPhiloxRoundsFast) {
+    *warps = bnd_const ? get_kernel_native_est_bc_r7_warps() : get_kernel_native_est_r7_warps();
     return bnd_const ? get_kernel_native_est_bc_r7(dim, dom, src, sk, one) : get_kernel_native_est_r7(dim, dom, src, sk, one);
-  if (one && bnd_const) return get_kernel_native_est_bc(dim, dom, src, sk, one);
+  }
+  if (one && bnd_const) {
+    *warps = get_kernel_native_est_bc_warps();
+    return get_kernel_native_est_bc(dim, dom, src, sk, one);
+  }
+  *warps = get_kernel_native_est_warps();
   return get_kernel_native_est(dim, dom, src, sk, one);
 }
 }  // namespace wos

@@ -2587,8 +2587,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   }
 }
 
-template <class S, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) wos_walk_kernel(const __grid_constant__ KArgs a) {
+// NW warps per CTA (the host reads it per kernel: wos_kernels_native.cu)
+template <class S, int MINB, int NW = kWarps>
+__global__ void __launch_bounds__(32 * NW, MINB) wos_walk_kernel(const __grid_constant__ KArgs a) {
   wos_kernel_body<S>(a);
 }
 
