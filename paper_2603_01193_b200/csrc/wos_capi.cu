@@ -1393,7 +1393,7 @@ struct KernelInfo {
   int warps;    // warps per CTA the kernel is built for
 };
 
-static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int rounds) {
+static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int rounds, bool anti) {
   KernelInfo k{nullptr, 8, false, false, kWarps};
   const int dom = s->dom_kind == WOS_DOM_POLYGON ? DOM_POLY : s->dom_kind;
   if (mode == WOS_MODE_REPLAY_F64) {
@@ -1406,7 +1406,7 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int
     const int sk = s->src_kind == WOS_SRC_SINE ? s->sk_native : 0;
     k.one = (s->n == 1 && s->stride <= kCP);
     k.cube = WOS_CENTERED_CUBE && WOS_SCALED_COORDS && k.one && !rows && s->cube &&
-             s->bnd_kind == WOS_BND_CONST;
+             s->bnd_kind == WOS_BND_CONST && !anti;
     k.fn = get_kernel_native(s->dim, k.cube ? DOM_CUBE : dom, s->src_kind, sk, k.one, rows,
                              s->bnd_kind == WOS_BND_CONST, rounds, &k.warps);
     k.elem = 4;
@@ -1428,7 +1428,7 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   const int rounds = cfg->philox_rounds == 0 ? kPhiloxRoundsDefault : cfg->philox_rounds;
   if (cfg->mode == WOS_MODE_NATIVE_F32 && rounds != kPhiloxRoundsDefault && rounds != kPhiloxRoundsFast)
     return fail(WOS_ERR_INVALID, "philox_rounds must be %d or %d", kPhiloxRoundsDefault, kPhiloxRoundsFast);
-  const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS, rounds);
+  const KernelInfo k = pick_kernel(s, cfg->mode, a.sink == SINK_ROWS, rounds, cfg->antithetic != 0);
   bool scaled = false;  // the walk runs in X = pi x (see below)
   if (!k.fn)
     return fail(WOS_ERR_UNSUPPORTED, "no kernel for dim %d domain %d source %d mode %d", s->dim,

@@ -1505,7 +1505,9 @@ struct Walker {
   }
   __device__ static __forceinline__ void jump_source(Lane& l, float d, const KArgs& a, uint32_t wa,
                                                      uint32_t wb, uint32_t btab) {
-    const float sd = l.sgn * d;
+    // (DOM_CUBE kernels run no antithetic walks — the launcher picks the scaled box
+    // kernel for those — so their sign is +1 and the multiply goes)
+    const float sd = kCentered ? d : l.sgn * d;
     if constexpr (DIM == 2) {
       // 2D: wa bits 19..31 -> theta (move), bits 0..12 -> phi (sample direction); the
       // radius index as in 3D, into the disk Green's-law table (wos_green2_table); wb's
