@@ -19,6 +19,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libwos_b200.so")
+    config.addinivalue_line("markers", "slow: full-size statistical checks (minutes; GPU plus host oracle)")
 
 
 def load_golden(name):
