@@ -758,15 +758,16 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[0] = cos(th);
       dir[1] = sin(th);
     } else if (dim == 2) {
-      /* layout v3 (wos_walk.cuh jump_source, 2D): words (u[0], u[1]) for an even step,
-         (u[2], u[3]) for an odd one; theta = bits 19..31 and phi = bits 0..12 of the
-         first word, the radius fraction from the disk Green's-law table */
+      /* layout v4 (wos_walk.cuh jump_source, 2D): words (u[0], u[1]) for an even step,
+         (u[2], u[3]) for an odd one; theta = bits 19..31 and phi = bits 6..18 of the
+         first word, the radius fraction from the disk Green's-law table at index
+         (wb >> 26) | (wa & 63) << 6 */
       const uint32_t wa = u[2 * sub], wb = u[2 * sub + 1];
       double th = TWO_PI * u13(wa >> 19) - PI;
       dir[0] = cos(th);
       dir[1] = sin(th);
-      double phi = TWO_PI * u13(wa & 0x1FFFu) - PI;
-      double r = d * (double)green2_table()[((wa >> 13) & 0x3Fu) | ((wb >> 7) & 0xFC0u)];
+      double phi = TWO_PI * u13(wa >> 6) - PI;
+      double r = d * (double)green2_table()[(wb >> 26) | ((wa & 0x3Fu) << 6)];
       double g[2] = {x[0] + sgn * r * cos(phi), x[1] + sgn * r * sin(phi)};
       acc -= (d * d * 0.25) * source(pb, g);
     } else if (!has_src) {
@@ -777,12 +778,13 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[1] = s * sin(phi);
       dir[2] = z;
     } else {
-      /* layout v3 (wos_walk.cuh jump3_source): 64 bits per jump, words (u[0], u[1]) for
+      /* layout v4 (wos_walk.cuh jump_source): 64 bits per jump, words (u[0], u[1]) for
          an even step, (u[2], u[3]) for an odd one; 13-bit midpoint-rounded direction
-         fields (bits 0..12 and 19..31 of each word) and a 12-bit index (bits 13..18 of
-         both words) into the Beta(2,2) conditional-mean table */
+         fields (wa: z bits 6..18, phi bits 19..31; wb: z' bits 0..12, phi' bits 13..25)
+         and a 12-bit index (wb >> 26) | (wa & 63) << 6 into the Beta(2,2)
+         conditional-mean table */
       const uint32_t wa = u[2 * sub], wb = u[2 * sub + 1];
-      double z = 2.0 * u13(wa & 0x1FFFu) - 1.0;
+      double z = 2.0 * u13(wa >> 6) - 1.0;
       double s = sqrt(fmax(0.0, 1.0 - z * z));
       double phi = TWO_PI * u13(wa >> 19) - PI;
       dir[0] = s * cos(phi);
@@ -790,8 +792,8 @@ static void walk_native_one(const wos_problem* pb, const double* x0, uint64_t pi
       dir[2] = z;
       double vz = 2.0 * u13(wb & 0x1FFFu) - 1.0;
       double vs = sqrt(fmax(0.0, 1.0 - vz * vz));
-      double vphi = TWO_PI * u13(wb >> 19) - PI;
-      double t = (double)beta_table()[((wa >> 13) & 0x3Fu) | ((wb >> 7) & 0xFC0u)];
+      double vphi = TWO_PI * u13(wb >> 13) - PI;
+      double t = (double)beta_table()[(wb >> 26) | ((wa & 0x3Fu) << 6)];
       double r = d * t;
       double g[3] = {x[0] + sgn * r * (vs * cos(vphi)), x[1] + sgn * r * (vs * sin(vphi)),
                      x[2] + sgn * r * vz};

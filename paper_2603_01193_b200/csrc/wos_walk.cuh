@@ -1375,7 +1375,7 @@ struct Walker {
   // 2 (s % 2), 2 (s % 2) + 1 (3D) of the block at counter 2 floor(s / kPerBlock).
   // Kernels whose lanes run in phase lock (the amortised loop) draw each block once;
   // the others redraw it per jump and select the words (same stream).
-  // The NATIVE 3D source jump (layout v3, below) also takes 64 bits: a block serves two
+  // The NATIVE 3D source jump (layout v4, below) also takes 64 bits: a block serves two
   // jumps, and its radius fraction comes from the shared-memory Beta(2,2) table
   static constexpr bool kBetaTab = S::NATIVE && S::SRC != SRC_NONE && !kScr;
   static constexpr int kPerBlock = (S::NATIVE && S::SRC == SRC_NONE) ? (DIM == 2 ? 4 : 2) : (kBetaTab ? 2 : 1);
@@ -1460,10 +1460,15 @@ struct Walker {
     }
   }
 
-  // NATIVE 3D source jump, layout v3: 64 bits (two words) per jump, so one Philox4x32
+  // NATIVE source jump, layout v4: 64 bits (two words) per jump, so one Philox4x32
   // block serves two jumps (kPerBlock = 2; phase-locked rounds in the hot loop):
-  //   wa bits 0..12 -> z (move), 13..18 -> radius index bits 0..5, 19..31 -> phi (move)
-  //   wb bits 0..12 -> z' (sample), 13..18 -> radius index bits 6..11, 19..31 -> phi'
+  //   wa bits 0..5 -> radius index bits 6..11, 6..18 -> z (move), 19..31 -> phi (move)
+  //   wb bits 0..12 -> z' (sample), 13..25 -> phi' (sample), 26..31 -> radius index
+  //   bits 0..5
+  // (2D: wa bits 6..18 -> phi (sample direction), 19..31 -> theta (move); wb only
+  // lends its radius bits.) The radius index sits where one funnel shift of (wa:wb)
+  // by 24 and one mask give its byte offset into the table (v3 took two shifts, two
+  // masks and a merge per jump).
   // Direction fields are 13-bit, midpoint-rounded ((b + 1/2) 2^-13): the midpoint rule
   // on the periodic phi is spectrally accurate and on z errs by O(2^-26) of the
   // integrand's curvature — far below fp32 rounding of the walk value. The radius
@@ -1476,6 +1481,20 @@ struct Walker {
     uint32_t m;
     asm("lop3.b32 %0, %1, 0x1fff, 0, 0xc0;" : "=r"(m) : "r"(w));
     return __uint_as_float((m << 10) + (expo | 0x200u));
+  }
+  __device__ static __forceinline__ float f13_mid6(uint32_t w, uint32_t expo) {  // bits 6..18
+    uint32_t m;
+    asm("lop3.b32 %0, %1, 0x7ffc0, 0, 0xc0;" : "=r"(m) : "r"(w));
+    return __uint_as_float((m << 4) + (expo | 0x200u));
+  }
+  __device__ static __forceinline__ float f13_mid13(uint32_t w) {  // bits 13..25, in [1, 2)
+    uint32_t r;
+    asm("shf.r.clamp.b32 %0, %1, %2, 3;" : "=r"(r) : "r"(w & 0x3ffe000u), "r"(0u));
+    return __uint_as_float(r + 0x3f800200u);
+  }
+  // byte offset of the radius-table entry: (wb >> 26) | (wa & 63) << 6, times 4
+  __device__ static __forceinline__ uint32_t radius_off(uint32_t wa, uint32_t wb) {
+    return __funnelshift_r(wb, wa, 24) & 0x3ffcu;
   }
   __device__ static __forceinline__ float f13_hi(uint32_t w) {  // bits 19..31
     uint32_t r;
@@ -1494,9 +1513,9 @@ struct Walker {
     if constexpr (kBetaAtZero) return base;
     else return base + (uint32_t)(a.stage_bytes + a.seg_stage_bytes);
   }
-  __device__ static __forceinline__ float beta_at(uint32_t off, uint32_t k) {
+  __device__ static __forceinline__ float beta_at(uint32_t off, uint32_t kbytes) {
     float t;
-    asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(off + 4u * k));
+    asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(off + kbytes));
     return t;
   }
   __device__ static __forceinline__ void jump_source(Lane& l, float d, const KArgs& a, uint32_t wa,
@@ -1515,9 +1534,8 @@ struct Walker {
       float sth, cth;
       __sincosf(dir_angle(f13_hi(wa)), &sth, &cth);
       float sph, cph;
-      __sincosf(dir_angle(f13_lo(wa, 0x3f800000u)), &sph, &cph);
-      const uint32_t k = ((wa >> 13) & 0x3fu) | ((wb >> 7) & 0xfc0u);
-      const float sr = sd * beta_at(btab, k);
+      __sincosf(dir_angle(f13_mid6(wa, 0x3f800000u)), &sph, &cph);
+      const float sr = sd * beta_at(btab, radius_off(wa, wb));
       const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
       // (scaled-coordinate kernels: the host folds the weight 1/4 pi^-2 into the coefficients)
       l.acc = fmaf(kScaled ? -(d * d) : -0.25f * d * d, source(l, a, g), l.acc);
@@ -1526,16 +1544,15 @@ struct Walker {
       return;
     } else {
     // z = 2u - 1 is exact for u = f - 1, so fmaf(-z, z, 1) >= 0
-    const float z = f13_lo(wa, 0x40000000u) - 3.0f;
+    const float z = f13_mid6(wa, 0x40000000u) - 3.0f;
     const float sxy = fast_sqrt(fmaf(-z, z, 1.0f));
     float sph, cph;
     __sincosf(dir_angle(f13_hi(wa)), &sph, &cph);
     const float vz = f13_lo(wb, 0x40000000u) - 3.0f;
     const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
     float vsp, vcp;
-    __sincosf(dir_angle(f13_hi(wb)), &vsp, &vcp);
-    const uint32_t k = ((wa >> 13) & 0x3fu) | ((wb >> 7) & 0xfc0u);
-    const float t = beta_at(btab, k);
+    __sincosf(dir_angle(f13_mid13(wb)), &vsp, &vcp);
+    const float t = beta_at(btab, radius_off(wa, wb));
     const float sr = sd * t;
     const float srv = sr * vs;
     // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
@@ -1849,7 +1866,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_AMORT_RNG
 #define WOS_AMORT_RNG 1
 #endif
-  // NATIVE source jumps (two per block, layout v3) run the same rounds outside the hot
+  // NATIVE source jumps (two per block, layout v4) run the same rounds outside the hot
   // loop (multi-instance, non-constant-boundary and rows kernels): the round holds the
   // block only inside one iteration, so the second jump's words cost no registers across
   // iterations, and a jump no longer redraws the whole block for half of its words

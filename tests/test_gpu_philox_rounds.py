@@ -150,8 +150,8 @@ def test_seven_round_avalanche(gpu, word, bit):
 
 @pytest.mark.parametrize("rounds", [10, 7])
 def test_beta22_radius_moments_over_1e9_draws(gpu, rounds):
-    """The radius fraction of the 3D source jump (layout v3, wos_walk.cuh jump3_source):
-    index ((wa >> 13) & 63) | ((wb >> 7) & 0xfc0) into the Beta(2,2) table, two jumps per
+    """The radius fraction of the source jump (layout v4, wos_walk.cuh jump_source):
+    index (wb >> 26) | (wa & 63) << 6 into the Beta(2,2) table, two jumps per
     block. Over 1.0e9 draws of the production stream the index is uniform, so E[t] and
     E[t^2] equal the table's exact means within 5 standard errors (and Beta(2,2)'s to
     ~1e-8)."""
@@ -167,7 +167,7 @@ def test_beta22_radius_moments_over_1e9_draws(gpu, rounds):
                         dim=1).to(torch.int32)
         w = _blocks(gpu, c, 0x5EED, 0xC0FFEE, rounds).to(torch.int64) & 0xFFFFFFFF
         for wa, wb in ((w[:, 0], w[:, 1]), (w[:, 2], w[:, 3])):
-            idx = ((wa >> 13) & 0x3F) | ((wb >> 7) & 0xFC0)
+            idx = (wb >> 26) | ((wa & 0x3F) << 6)
             hist += torch.bincount(idx, minlength=4096)
             total += chunk
     p = hist.to(torch.float64) / total
