@@ -106,6 +106,31 @@ __device__ __forceinline__ PhiloxPre philox_pre(uint32_t c0, uint32_t c2, uint32
                    (uint32_t)(t >> 32) ^ k12, (uint32_t)t};
 }
 
+// The same fold split once more for walks that share (c0, c3) — a unit's walks differ
+// only in c2: the c2-free part (p0 = M0 c0 and s = M1 x2) once per unit, the rest
+// (two multiplies instead of four) per walk. Bit-identical to philox_pre.
+struct PhiloxUnit {
+  uint32_t e1;   // lo(M0 c0) ^ k1(1)
+  uint32_t b1k;  // lo(M1 x2) ^ k0(2)
+  uint32_t sk;   // hi(M1 x2) ^ k0(1)
+};
+
+__device__ __forceinline__ PhiloxUnit philox_pre_unit(uint32_t c0, uint32_t c3, uint32_t k10, uint32_t k01,
+                                                      uint32_t k11, uint32_t k02) {
+  const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+  const uint32_t x2 = (uint32_t)(p0 >> 32) ^ c3 ^ k10;
+  const uint64_t s = (uint64_t)0xCD9E8D57u * x2;
+  return PhiloxUnit{(uint32_t)p0 ^ k11, (uint32_t)s ^ k02, (uint32_t)(s >> 32) ^ k01};
+}
+
+__device__ __forceinline__ PhiloxPre philox_pre_walk(uint32_t c2, const PhiloxUnit& u, uint32_t k00,
+                                                     uint32_t k12) {
+  const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+  const uint32_t b0 = u.sk ^ (uint32_t)p1;
+  const uint64_t t = (uint64_t)0xD2511F53u * b0;
+  return PhiloxPre{(uint32_t)(p1 >> 32) ^ k00, u.e1, u.b1k, (uint32_t)(t >> 32) ^ k12, (uint32_t)t};
+}
+
 // rounds 0-2 from the precomputed words: the state entering round 3
 __device__ __forceinline__ uint4 philox_pre_r012(uint32_t b, const PhiloxPre& p) {
   const uint64_t q = (uint64_t)0xD2511F53u * (p.a0 ^ b);                // round 1, word 0

@@ -1757,6 +1757,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // single-instance NATIVE: Philox counter words of the cached unit's walk 0; walk
   // j0 + jj has c2 = cu_c2b + jj while cu_fastc (no 32-bit carry inside the unit)
   uint32_t cu_c1 = 0, cu_c2b = 0, cu_c3 = 0;
+  PhiloxUnit cu_pu{0u, 0u, 0u};  // hot kernels: the unit's c2-free Philox fold
   bool cu_fastc = false;
 
   typename W::Lane l;
@@ -2151,6 +2152,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         cu_c1 = (uint32_t)cu_pid;
         cu_c2b = (uint32_t)tid0;
         cu_c3 = (uint32_t)(tid0 >> 32) ^ ((uint32_t)(cu_pid >> 32) * 0x85EBCA6Bu);
+        cu_pu = philox_pre_unit(cu_c1, cu_c3, l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2]);
         cu_fastc = (uint64_t)(uint32_t)tid0 + (cu_jend - cu_j0) <= 0x100000000ull;
         return true;
       };
@@ -2190,7 +2192,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         const uint32_t blk_new = (cu_k % kSlots) * 4u;
         if (cu_fastc) {
           const uint32_t c2 = cu_c2b + (jr & anti_jmask);
-          const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2], l.hk1[2]);
+          const PhiloxPre pc = philox_pre_walk(c2, cu_pu, l.hk0[0], l.hk1[2]);
           if (take && real) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) s.x[i] = cu_x[i];
@@ -2353,6 +2355,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                 cu_c1 = (uint32_t)cu_pid;
                 cu_c2b = (uint32_t)tid0;
                 cu_c3 = (uint32_t)(tid0 >> 32) ^ ((uint32_t)(cu_pid >> 32) * 0x85EBCA6Bu);
+                if constexpr (W::kHot) cu_pu = philox_pre_unit(cu_c1, cu_c3, l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2]);
                 cu_fastc = (uint64_t)(uint32_t)tid0 + (cu_jend - cu_j0) <= 0x100000000ull;
               }
               room = IU;
@@ -2376,7 +2379,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint32_t blk_new = (cu_k % kSlots) * 4u;
           if (cu_fastc) {
             const uint32_t c2 = cu_c2b + (jr & anti_jmask);
-            const PhiloxPre pc = philox_pre(cu_c1, c2, cu_c3, l.hk0[0], l.hk1[0], l.hk0[1], l.hk1[1], l.hk0[2], l.hk1[2]);
+            const PhiloxPre pc = philox_pre_walk(c2, cu_pu, l.hk0[0], l.hk1[2]);
             if (take && real) {
 #pragma unroll
               for (int i = 0; i < DIM; ++i) l.x[i] = cu_x[i];
