@@ -337,11 +337,20 @@ struct Walker {
     const uint32_t e = bytes8 ? (C.x & 0xFFFFu) : C.y;
     *n_pairs = e;
     const uint8_t* idx8 = reinterpret_cast<const uint8_t*>(idx);
+    // byte indices as a 96-bit queue shifted by one byte per pair (one LOP3 and three
+    // funnel shifts instead of selecting the word and the byte lane per pair)
+    uint32_t q0 = C.y, q1 = C.z, q2 = C.w;
     for (uint32_t k = 0; k < e; ++k) {
       int j;
       if (bytes8) {
-        const uint32_t wd = k < 4 ? C.y : (k < 8 ? C.z : C.w);
-        j = k < 12 ? (int)((wd >> (8 * (k & 3))) & 0xFFu) : (int)__ldg(idx8 + (C.x >> 16) + (k - 12));
+        if (k < 12) {
+          j = (int)(q0 & 0xFFu);
+          q0 = __funnelshift_r(q0, q1, 8);
+          q1 = __funnelshift_r(q1, q2, 8);
+          q2 >>= 8;
+        } else {
+          j = (int)__ldg(idx8 + (C.x >> 16) + (k - 12));
+        }
       } else {
         const uint32_t wd = k < 2 ? C.z : C.w;
         j = k < 4 ? (int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)) : (int)__ldg(idx + C.x + (k - 4));
