@@ -53,7 +53,10 @@ static int fail(int code, const char* fmt, ...) {
 // ------------------------------------------------------------------------
 constexpr int kCounterRing = 256;
 constexpr size_t kStatusBytes = 32;
-constexpr int kPipeChunks = 4;                 // host pipeline: point chunks per call (at most)
+#ifndef WOS_PIPE_CHUNKS
+#define WOS_PIPE_CHUNKS 2  // cfg4 e2e/device: 1 chunk 95.0 %, 2 chunks 95.4 %, 3 93.4 %, 4 93.6 %, 8 89.5 %
+#endif
+constexpr int kPipeChunks = WOS_PIPE_CHUNKS;   // host pipeline: point chunks per call (at most)
 constexpr int64_t kPipeMinWork = 1ll << 23;    // walks per chunk (at least)
 
 struct wos_context {
