@@ -215,20 +215,27 @@ def test_long_ensembles_use_chunked_reduction(gpu, mode):
     assert np.all(n == L)
 
 
-@pytest.mark.parametrize("cfg", [0, 2, 4])
-def test_native_estimate_matches_native_oracle(gpu, cfg):
+@pytest.mark.parametrize("cfg,anti", [(0, False), (2, False), (4, False), (0, True), (4, True)])
+def test_native_estimate_matches_native_oracle(gpu, cfg, anti):
     """The estimate kernels themselves (cfg0 / cfg4: the single-instance constant-boundary
-    variants that walk in scaled coordinates X = pi x; cfg2: multi-instance, deferred
-    recording) against the oracle's fp64 estimate of the same native walks."""
+    variants, walking a cube centred at 1/2 in centred scaled coordinates X = pi (x - 1/2)
+    (DOM_CUBE) — antithetic launches take the scaled-box kernel instead, which keeps the
+    sign multiply; cfg2: multi-instance, deferred recording) against the oracle's fp64
+    estimate of the same native walks."""
+    import dataclasses
+
     from paper_2603_01193_b200 import configs, estimate_arrays
 
     w = _subset(configs.build(cfg), 96, seed=20 + cfg)
     L = 64
-    mean, m2, n = estimate_arrays(w.problems, w.points, L, w.cfg, point_ids=w.point_ids,
+    wc = dataclasses.replace(w.cfg, antithetic=anti)
+    mean, m2, n = estimate_arrays(w.problems, w.points, L, wc, point_ids=w.point_ids,
                                   inst_index=w.inst_index if len(w.problems) > 1 else None, traj_start=7)
+    assert np.all(n == (L // 2 if anti else L))
     mo, m2o, _ = O.estimate(w.problems, w.points, L, seed=w.cfg.rng_seed, eps=w.cfg.eps_shell,
                             max_steps=w.cfg.max_steps, point_ids=w.point_ids,
-                            inst_index=w.inst_index if len(w.problems) > 1 else None, traj_start=7, native=True)
+                            inst_index=w.inst_index if len(w.problems) > 1 else None, traj_start=7, native=True,
+                            antithetic=anti)
     rms = float(np.sqrt(np.mean(m2o / L + mo**2)))  # rms walk value
     close = np.abs(mean - mo) <= 1e-4 * rms
     assert close.mean() >= 0.97, f"{close.mean():.3f} of points within 1e-4 rms"
