@@ -1504,6 +1504,8 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   a.antithetic = cfg->antithetic ? 1 : 0;
   a.seed = cfg->rng_seed;
   a.nkey0 = (uint32_t)cfg->rng_seed;
+  if (!k.one)  // multi-instance NATIVE kernels read the launch-uniform k0 schedule too
+    for (int r = 0; r < 10; ++r) a.rk0[r] = a.nkey0 + (uint32_t)r * 0x9E3779B9u;
   a.nkey1_seed = (uint32_t)(cfg->rng_seed >> 32);
   if (s->src_kind == WOS_SRC_SCREENED_CONST || s->src_kind == WOS_SRC_SCREENED_VC) {
     // walker.py:324-325: delta tracking needs a positive majorant; the constant-coefficient

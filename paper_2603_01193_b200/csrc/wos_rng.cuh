@@ -150,6 +150,21 @@ __device__ __forceinline__ uint4 philox4x32_rk_pre(uint32_t b, const PhiloxPre& 
   return c;
 }
 
+// multi-instance walks: the launch-uniform k0 schedule from the kernel parameters (ptxas
+// keeps it in uniform registers), the per-instance k1 bumped per round
+__device__ __forceinline__ uint4 philox4x32_pre_k0(uint32_t b, const PhiloxPre& p, const uint32_t* rk0, uint32_t k1,
+                                                   int rounds) {
+  uint4 c = philox_pre_r012(b, p);
+#pragma unroll
+  for (int r = 3; r < kPhiloxRoundsFast; ++r) philox4x32_round(c, rk0[r], k1 + (uint32_t)r * 0xBB67AE85u);
+  if (rounds > kPhiloxRoundsFast) {
+#pragma unroll
+    for (int r = kPhiloxRoundsFast; r < kPhiloxRoundsDefault; ++r)
+      philox4x32_round(c, rk0[r], k1 + (uint32_t)r * 0xBB67AE85u);
+  }
+  return c;
+}
+
 __device__ __forceinline__ uint4 philox4x32_pre(uint32_t b, const PhiloxPre& p, uint32_t k0, uint32_t k1,
                                                 int rounds) {
   uint4 c = philox_pre_r012(b, p);

@@ -1396,12 +1396,16 @@ struct Walker {
     const int rounds = S::RND ? S::RND : a.philox_rounds;
 // the hot kernels fold too since the jump-first loop made refills cheaper (cfg4 -0.7 %;
 // it had cost +1.7 % with the test-first loop)
+#ifndef WOS_MULTI_K0TAB
+#define WOS_MULTI_K0TAB 1
+#endif
 #ifndef WOS_HOT_FOLD
 #define WOS_HOT_FOLD 1
 #endif
     if constexpr (kHot && WOS_HOT_FOLD) return philox4x32_rk_pre(c0, l.pc, l.hk0, l.hk1, rounds);
     else if constexpr (kHot) return philox4x32_rk(make_uint4(l.c1, c0, l.c2, l.c3), l.hk0, l.hk1, rounds);
     else if constexpr (ONE) return philox4x32_rk_pre(c0, l.pc, a.rk0, a.rk1, rounds);
+    else if constexpr (WOS_MULTI_K0TAB) return philox4x32_pre_k0(c0, l.pc, a.rk0, l.k1, rounds);
     else return philox4x32_pre(c0, l.pc, a.nkey0, l.k1, rounds);
   }
 
