@@ -45,7 +45,10 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
-constexpr int kChunk = 128;       // L > kChunk: work units are kChunk-walk chunks of one point
+#ifndef WOS_CHUNK
+#define WOS_CHUNK 128
+#endif
+constexpr int kChunk = WOS_CHUNK; // L > kChunk: work units are kChunk-walk chunks of one point
 constexpr int kUnitTarget = 128;  // L < 32: whole points per unit up to >= this many walks
 constexpr int kCP = 256;          // floats of single-instance parameters held in the kernel params
 constexpr int kDomOff = 0;        // table row: [0, 8) domain params
