@@ -1525,7 +1525,9 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
   if (cfg->mode == WOS_MODE_NATIVE_F32 && s->src_kind != WOS_SRC_NONE &&
       s->src_kind != WOS_SRC_SCREENED_CONST && s->src_kind != WOS_SRC_SCREENED_VC) {
     a.beta_tab = s->dim == 3 ? c->d_beta_tab : c->d_green2_tab;
-    a.beta_stage_bytes = (int)(sizeof(float) * WOS_BETA_TABLE_N);
+    // (polygon and mesh kernels read it through L1: wos_walk.cuh kBetaGlobal)
+    if (s->dom_kind != WOS_DOM_POLYGON && s->dom_kind != WOS_DOM_MESH)
+      a.beta_stage_bytes = (int)(sizeof(float) * WOS_BETA_TABLE_N);
   }
   const size_t smem =
       smem_bytes((size_t)a.stage_bytes + (size_t)a.seg_stage_bytes + (size_t)a.beta_stage_bytes, k.elem, k.warps);

@@ -1519,6 +1519,10 @@ struct Walker {
   // the instance table and the polygon records. It is read with ld.shared on that 32-bit offset, so no generic address of
   // the shared window has to be rebuilt inside the loop.
   static constexpr bool kBetaAtZero = ONE && (S::DOM == DOM_BOX || S::DOM == DOM_BALL || S::DOM == DOM_CUBE);
+  // Polygon and mesh kernels read the table through L1 instead: their candidate-grid /
+  // BVH records live in L1, and 16 KB of staged table per CTA shrinks L1 by 64 KB at 4
+  // CTAs/SM (cfg3: twice the long-scoreboard stalls, +6 % time)
+  static constexpr bool kBetaGlobal = S::DOM == DOM_POLY || S::DOM == DOM_MESH;
   __device__ static __forceinline__ uint32_t beta_tab_offset(const KArgs& a) {
     extern __shared__ __align__(16) unsigned char wos_smem_[];
     // the dynamic window's shared address (a link-time constant) plus what precedes it
@@ -1540,6 +1544,11 @@ struct Walker {
     // (DOM_CUBE kernels run no antithetic walks — the launcher picks the scaled box
     // kernel for those — so their sign is +1 and the multiply goes)
     const float sd = kCentered ? d : l.sgn * d;
+    auto radius_t = [&](uint32_t off) -> float {
+      if constexpr (kBetaGlobal)
+        return __ldg(reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(a.beta_tab) + off));
+      else return beta_at(btab, off);
+    };
     if constexpr (DIM == 2) {
       // 2D: wa bits 19..31 -> theta (move), bits 0..12 -> phi (sample direction); the
       // radius index as in 3D, into the disk Green's-law table (wos_green2_table); wb's
@@ -1548,7 +1557,7 @@ struct Walker {
       __sincosf(dir_angle(f13_hi(wa)), &sth, &cth);
       float sph, cph;
       __sincosf(dir_angle(f13_mid6(wa, 0x3f800000u)), &sph, &cph);
-      const float sr = sd * beta_at(btab, radius_off(wa, wb));
+      const float sr = sd * radius_t(radius_off(wa, wb));
       const float g[2] = {fmaf(sr, cph, l.x[0]), fmaf(sr, sph, l.x[1])};
       // (scaled-coordinate kernels: the host folds the weight 1/4 pi^-2 into the coefficients)
       l.acc = fmaf(kScaled ? -(d * d) : -0.25f * d * d, source(l, a, g), l.acc);
@@ -1565,7 +1574,7 @@ struct Walker {
     const float vs = fast_sqrt(fmaf(-vz, vz, 1.0f));
     float vsp, vcp;
     __sincosf(dir_angle(f13_mid13(wb)), &vsp, &vcp);
-    const float t = beta_at(btab, radius_off(wa, wb));
+    const float t = radius_t(radius_off(wa, wb));
     const float sr = sd * t;
     const float srv = sr * vs;
     // (x, y) pairs as packed FFMA2: elementwise fma.rn, identical to two fmaf
@@ -1718,7 +1727,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
   }
   // ---- stage the Beta(2,2) radius table (NATIVE 3D source jumps) after them ----
-  if constexpr (W::kBetaTab) {
+  if constexpr (W::kBetaTab && !W::kBetaGlobal) {
     float* dst = reinterpret_cast<float*>(smem + a.stage_bytes + a.seg_stage_bytes);
     for (int i = threadIdx.x; i < a.beta_stage_bytes / 4; i += blockDim.x) dst[i] = a.beta_tab[i];
   }
