@@ -42,7 +42,10 @@ constexpr int kWarps = kBlock / 32;
 #ifndef WOS_GRID_BYTES  // byte pair indices (12 inline) when a polygon has <= 256 pairs
 #define WOS_GRID_BYTES 1
 #endif
-constexpr int kRing = 1024;       // per-warp ring of walk values (estimate sink)
+#ifndef WOS_RING
+#define WOS_RING 512  // 1024 -> 512: cfg3 -2 %, cfg2 -3 % (more L1), others equal; 256 starves cfg4 (+17 %)
+#endif
+constexpr int kRing = WOS_RING;   // per-warp ring of walk values (estimate sink)
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
 #ifndef WOS_CHUNK
