@@ -53,6 +53,9 @@ static int fail(int code, const char* fmt, ...) {
 // ------------------------------------------------------------------------
 constexpr int kCounterRing = 256;
 constexpr size_t kStatusBytes = 32;
+#ifndef WOS_CARVEOUT
+#define WOS_CARVEOUT 1
+#endif
 #ifndef WOS_PIPE_CHUNKS
 #define WOS_PIPE_CHUNKS 2  // cfg4 e2e/device: 1 chunk 95.0 %, 2 chunks 95.4 %, 3 93.4 %, 4 93.6 %, 8 89.5 %
 #endif
@@ -1544,6 +1547,22 @@ static int launch_walk(wos_context* c, const wos_problem_set* s, const wos_walk_
     } else {
       CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, 32 * k.warps, smem));
+#if WOS_CARVEOUT
+      // the smallest shared-memory carve-out that still holds per_sm CTAs (plus the
+      // 1 KB the runtime reserves per CTA): the rest of the 256 KB stays L1 for the
+      // walks' global reads (polygon grids, BVH nodes, query points)
+      if (per_sm > 0) {
+        int smem_sm = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+        const size_t need = (size_t)per_sm * (smem + 1024);
+        const int pct = (int)std::min<size_t>(100, (need * 100 + smem_sm - 1) / smem_sm);
+        CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        int per_sm2 = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k.fn, 32 * k.warps, smem));
+        if (per_sm2 < per_sm)  // the carve-out rounding lost a CTA: let the driver choose
+          CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributePreferredSharedMemoryCarveout, -1));
+      }
+#endif
       c->launch_cache[k.fn] = std::make_pair(smem, per_sm);
     }
   }
