@@ -1416,6 +1416,8 @@ static KernelInfo pick_kernel(const wos_problem_set* s, int mode, bool rows, int
     k.fn = get_kernel_native(s->dim, k.cube ? DOM_CUBE : dom, s->src_kind, sk, k.one, rows,
                              s->bnd_kind == WOS_BND_CONST, rounds, &k.warps);
     k.elem = 4;
+    // exit-ring kernels keep (x, y) in 8-byte ring slots (wos_types.h exit_ring_kernel)
+    if (exit_ring_kernel(true, s->dim, dom, s->src_kind, k.one, !rows, s->bnd_kind == WOS_BND_CONST)) k.elem = 8;
   }
   return k;
 }

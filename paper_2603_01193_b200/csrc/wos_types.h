@@ -46,6 +46,15 @@ constexpr int kWarps = kBlock / 32;
 #define WOS_RING 512  // 1024 -> 512: cfg3 -2 %, cfg2 -3 % (more L1), others equal; 256 starves cfg4 (+17 %)
 #endif
 constexpr int kRing = WOS_RING;   // per-warp ring of walk values (estimate sink)
+// Exit-ring kernels (wos_walk.cuh Walker::kExitRing) keep 8-byte ring slots; the host
+// sizes their shared memory from the same predicate (wos_capi.cu pick_kernel).
+#ifndef WOS_EXIT_RING
+#define WOS_EXIT_RING 1
+#endif
+constexpr bool exit_ring_kernel(bool native, int dim, int dom, int src, bool one, bool est, bool bc) {
+  return WOS_EXIT_RING && native && dim == 2 && (dom == DOM_BALL || dom == DOM_BOX) &&
+         src == SRC_NONE && one && est && !bc;
+}
 constexpr int kSlots = 16;        // per-warp completion counters of live retire blocks
 constexpr int kUQ = 16;           // per-warp queue of grabbed work units
 #ifndef WOS_CHUNK

@@ -140,6 +140,14 @@ struct Walker {
   static constexpr bool kHot = S::NATIVE && ONE && S::DOM != DOM_POLY && S::SINK == SINK_ESTIMATE &&
                                S::SRC != SRC_SCR_CONST && S::SRC != SRC_SCR_VC;
   static constexpr int kHotK = kHot ? 10 : 1;
+  // Exit ring (single-instance source-free 2D estimate kernels with a non-constant
+  // boundary: cfg1): a finishing walk stores its exit position (x, y) in its ring slot
+  // (8 bytes) and the boundary term g(projection) is evaluated when the unit retires,
+  // by all 32 lanes over the unit's slots, instead of by the few lanes that finished
+  // since the last refill. Same finish_value() on the same position: identical values.
+  static constexpr bool kExitRing = exit_ring_kernel(S::NATIVE, DIM, S::DOM, S::SRC, ONE,
+                                                     S::SINK == SINK_ESTIMATE, S::BC);
+  static constexpr int kRS = kExitRing ? 2 : 1;  // ring slot size in Reals
   // hot source coefficients: those the jump reads at compile-time offsets
   static constexpr int kHotSrcN =
       !kHot ? 0
@@ -1675,25 +1683,25 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // Each live unit has a shared-memory completion counter bumped by every finishing
 // walk; at each refill the warp retires the completed units at the head of its
 // stream, in order.
-template <class Real>
+template <int RS = 1, class Real>
 __device__ __forceinline__ double sample_at(const Real* ring, uint32_t base, uint32_t i, bool anti) {
   if (anti)
-    return ((double)ring[(base + 2 * i) % kRing] + (double)ring[(base + 2 * i + 1) % kRing]) / 2.0;
-  return (double)ring[(base + i) % kRing];
+    return ((double)ring[((base + 2 * i) % kRing) * RS] + (double)ring[((base + 2 * i + 1) % kRing) * RS]) / 2.0;
+  return (double)ring[((base + i) % kRing) * RS];
 }
 
 // two-pass moments of n samples starting at ring position `base`, warp-cooperative,
 // fixed order (estimator.py:106-110)
-template <class Real>
+template <int RS = 1, class Real>
 __device__ __forceinline__ void warp_moments(const Real* ring, uint32_t base, uint32_t n, bool anti,
                                              int lane, double* mean, double* m2) {
   double sum = 0.0;
-  for (uint32_t i = lane; i < n; i += 32) sum += sample_at(ring, base, i, anti);
+  for (uint32_t i = lane; i < n; i += 32) sum += sample_at<RS>(ring, base, i, anti);
   sum = warp_sum(sum);
   const double mu = sum / (double)n;
   double q = 0.0;
   for (uint32_t i = lane; i < n; i += 32) {
-    const double v = sample_at(ring, base, i, anti);
+    const double v = sample_at<RS>(ring, base, i, anti);
     q += (v - mu) * (v - mu);
   }
   *mean = mu;
@@ -1706,6 +1714,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   using Real = typename S::Real;
   constexpr int DIM = S::DIM;
   constexpr bool est = S::SINK == SINK_ESTIMATE;
+  constexpr bool kExitRing = W::kExitRing;
+  constexpr int kRS = W::kRS;
+  constexpr uint32_t kSlotBytes = (uint32_t)sizeof(Real) * kRS;  // bytes per ring slot
   extern __shared__ __align__(16) unsigned char smem[];
 
   // ---- stage the instance table into shared memory (multi-instance launches) ----
@@ -1743,10 +1754,10 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // the warp's ring offset goes through a shuffle so that ptxas keeps it in a register
   // instead of re-deriving it from %tid and the launch constants every iteration
   const uint32_t woff = __shfl_sync(WOS_FULL, (uint32_t)(a.stage_bytes + a.seg_stage_bytes + a.beta_stage_bytes +
-                                    warp * (kRing * sizeof(Real) + kSlots * 4 + kUQ * 4)), 0);
+                                    warp * (kRing * kSlotBytes + kSlots * 4 + kUQ * 4)), 0);
   unsigned char* wbase = smem + woff;
   Real* ring = reinterpret_cast<Real*>(wbase);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + kRing * sizeof(Real));
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + kRing * kSlotBytes);
   uint32_t* unitq = cnt + kSlots;
   if (lane < kSlots) cnt[lane] = 0u;
   __syncthreads();
@@ -1802,6 +1813,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     __syncthreads();
   }
   bool active = false;
+  if constexpr (W::kExitRing) {  // (a lane without a walk reads as an ended walk: see the exit-ring round)
+    l.d = Real(-1);
+    l.step = 0;
+    l.sgn = Real(1);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) l.x[i] = Real(0);
+  }
   uint32_t blk = 0;          // byte offset of this lane's unit counter in cnt (ESTIMATE)
   unsigned idle = WOS_FULL;  // warp-uniform: lanes without a walk
   unsigned long long lane_steps = 0ull;
@@ -1812,12 +1830,26 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     __syncwarp();
     while (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) {
       const uint32_t unit = unitq[r_unit % kUQ];
+      if constexpr (kExitRing) {
+        // the unit's slots hold exit positions: evaluate g(projection) for all of them,
+        // 32 at a time, and leave each value in its slot's first word (a null item's
+        // slot holds stale data; its value is computed and never read)
+        for (uint32_t i = lane; i < IU; i += 32) {
+          Real* slot = ring + ((r_seq + i) % kRing) * kRS;
+          typename W::Lane t = l;
+          t.x[0] = slot[0];
+          t.x[1] = slot[1];
+          t.acc = Real(0);
+          slot[0] = W::finish_value(t, a);
+        }
+        __syncwarp();
+      }
       if (split) {
         const uint32_t p = fast_div(unit, a.nc_mul, a.nc_shr);
         const uint32_t c = unit - p * a.n_chunks;
         const uint32_t valid = min((uint32_t)kChunk, L - c * kChunk);
         double mu, q;
-        warp_moments(ring, r_seq, anti ? valid / 2 : valid, anti, lane, &mu, &q);
+        warp_moments<kRS>(ring, r_seq, anti ? valid / 2 : valid, anti, lane, &mu, &q);
         if (lane == 0) {
           a.partials[2 * (size_t)unit] = mu;
           a.partials[2 * (size_t)unit + 1] = q;
@@ -1830,11 +1862,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           if (p < a.n_points) {
             const uint32_t base = r_seq + pl * L;
             double sum = 0.0;
-            for (uint32_t i = 0; i < ns; ++i) sum += sample_at(ring, base, i, anti);
+            for (uint32_t i = 0; i < ns; ++i) sum += sample_at<kRS>(ring, base, i, anti);
             const double mu = sum / (double)ns;
             double q = 0.0;
             for (uint32_t i = 0; i < ns; ++i) {
-              const double v = sample_at(ring, base, i, anti);
+              const double v = sample_at<kRS>(ring, base, i, anti);
               q += (v - mu) * (v - mu);
             }
             a.out_mean[p] = mu;
@@ -1846,7 +1878,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint64_t p = (uint64_t)unit * U + pl;
           if (p >= a.n_points) break;
           double mu, q;
-          warp_moments(ring, r_seq + pl * L, anti ? L / 2 : L, anti, lane, &mu, &q);
+          warp_moments<kRS>(ring, r_seq + pl * L, anti ? L / 2 : L, anti, lane, &mu, &q);
           if (lane == 0) {
             a.out_mean[p] = mu;
             a.out_m2[p] = q;
@@ -1909,6 +1941,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                             (W::kPerBlock == 1 || W::kBetaTab);
   // the general amortised-round loop (source-free kernels; the hot loop runs its own rounds)
   constexpr bool kAmortLoop = kAmort && !kHotLoop;
+  // Exit-ring kernels run the hot loop's lean refill (lazy retirement, branch-light
+  // issue of the cached unit's walks) and branch-free rounds (below)
+#ifndef WOS_EXIT_LEAN
+#define WOS_EXIT_LEAN 1
+#endif
+  constexpr bool kExitLoop = WOS_EXIT_LEAN && kExitRing && kAmortLoop && W::kHot && WOS_HOT_FOLD;
+  constexpr bool kLean = kHotLoop || kExitLoop;
   // One hot-loop step of a walk slot; returns whether the walk is still live. With a
   // two-jump block (3D source jumps) a step is a round of two jumps from one Philox
   // block: every slot enters a round at an even step (walks start at step 0 and are
@@ -1962,8 +2001,16 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   };
   auto record = [&](Real d) {
     // walker.py:275-281: value = acc + g(projection), steps, hit = (d < eps)
-    const Real v = W::finish_value(l, a);
     lane_steps += (unsigned long long)l.step;
+    if constexpr (kExitRing) {
+      // source-free: acc = 0, the value is g(projection of x), evaluated at retirement
+      Real* slot = reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq);
+      *reinterpret_cast<float2*>(slot) = make_float2(l.x[0], l.x[1]);
+      atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
+      active = false;
+      return;
+    }
+    const Real v = W::finish_value(l, a);
     if constexpr (est) {
       *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + l.seq) = v;
       atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk), 1u);
@@ -1984,7 +2031,11 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_DEFER_RECORD
 #define WOS_DEFER_RECORD 1
 #endif
-  const bool defer = WOS_DEFER_RECORD && !S::BC && a.bnd_kind != BND_CONST;
+  // exit-ring launches refill at refill_min + this many idle lanes (between rounds)
+#ifndef WOS_EXIT_REFILL_ADD
+#define WOS_EXIT_REFILL_ADD 0
+#endif
+  const bool defer = WOS_DEFER_RECORD && !kExitRing && !S::BC && a.bnd_kind != BND_CONST;
   bool pend = false;
   auto finish = [&](Real d) {
     if (defer) {
@@ -2302,14 +2353,18 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
   const int refill_thr = __shfl_sync(
       WOS_FULL,
-      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? 4 : 0) : kAmortLoop ? 1 : a.refill_min), 0);
+      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? 4 : 0)
+                  : kExitLoop      ? a.refill_min + WOS_EXIT_REFILL_ADD
+                  : kExitRing      ? a.refill_min
+                  : kAmortLoop     ? 1
+                                   : a.refill_min), 0);
   while (true) {
     const int n_idle = __popc(idle);
     if (n_idle >= refill_thr) {
       flush();  // record the lanes that finished since the last refill
       // retire lazily: the ring holds kRing walks, so completed units only need to be
       // reduced before new walks are issued (one shared-memory check, no vote)
-      if (est && (!kHotLoop || !fast)) {  // (the hot loop's cached-unit refill retires lazily)
+      if (est && (!kLean || !fast)) {  // (the hot loop's cached-unit refill retires lazily)
         __syncwarp();  // order the lanes' counter updates before the check
         if (r_seq + IU <= s_issue && cnt[r_unit % kSlots] == IU) retire();
       }
@@ -2317,7 +2372,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
         // ============ refill, one point per unit: cached point in registers ============
         uint32_t room = cu_end - s_issue;
         uint32_t cap = r_seq + (uint32_t)kRing - s_issue;
-        if constexpr (kHotLoop) {
+        if constexpr (kLean) {
           // the hot loop refills in small batches: it retires only when the ring is
           // short of slots for them or a new unit is due (the unit queue and counter
           // slots must have room); retire() orders the lanes' counter updates itself
@@ -2382,13 +2437,13 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               }
               room = IU;
             } else if (n_idle == 32 && exhausted) {
-              if constexpr (kHotLoop) retire();  // (retirement is lazy there)
+              if constexpr (kLean) retire();  // (retirement is lazy there)
               if (r_seq == s_issue) break;  // no walk left, none running, all retired
             }
           }
         }
         const uint32_t n = min(min((uint32_t)n_idle, room), cap);
-        if constexpr (kHotLoop) {
+        if constexpr (kLean) {
           // Branch-light issue of the cached unit's next walks: the per-lane start state
           // (counter fold, sign, ring slot) is computed by every lane and committed by the
           // lanes that take a walk; the point, its distance and the unit slot are
@@ -2410,7 +2465,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               l.d = cu_d;
               l.pc = pc;
               l.sgn = __int_as_float(0x3f800000 | ((jr & anti_bit) << 31));
-              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+              l.seq = (seq % kRing) * kSlotBytes;
               blk = blk_new;
               active = true;
             }
@@ -2419,12 +2474,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
             W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, (anti && (j & 1u)) ? -1.0 : 1.0);
             l.d = cu_d;
-            l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+            l.seq = (seq % kRing) * kSlotBytes;
             blk = blk_new;
             active = true;
           }
           if (take && !real) atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_new), 1u);
-          if (cu_d < eps && take && real) finish(cu_d);  // the unit's point lies in the shell
+          // the unit's point lies in the shell (an exit-ring round finishes such a walk itself)
+          if constexpr (!kExitLoop)
+            if (cu_d < eps && take && real) finish(cu_d);
         } else if (!active) {
           const uint32_t rank = __popc(idle & lanemask_lt());
           if (rank < n) {
@@ -2447,7 +2504,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
                 const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
                 W::start(l, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, sg);
               }
-              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+              l.seq = (seq % kRing) * kSlotBytes;
               active = true;
               if constexpr (kJumpFirstPoly) {
                 l.d = cu_d;
@@ -2509,7 +2566,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
               const double sg = (anti && (j & 1u)) ? -1.0 : 1.0;
               W::start(l, table, a.hdr, a, a.points + (size_t)p * DIM, inst,
                        a.point_ids ? (uint64_t)a.point_ids[p] : a.id_base + p, tid, sg);
-              l.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+              l.seq = (seq % kRing) * kSlotBytes;
               active = true;
               first_query();
             } else {  // null item padding the last unit: complete at once
@@ -2531,7 +2588,32 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
     }
 
     // ================= one step of every active walk =================
-    if constexpr (kAmortLoop) {
+    if constexpr (kExitLoop) {
+      // Branch-free round of kPerBlock source-free jumps, every lane, live or not: a
+      // walk that has ended (or a lane without one: its stale state is an ended walk's,
+      // d = -1 before the first) jumps by 0, which leaves its position, and with it
+      // the recomputed distance, unchanged, and its step count is not advanced — the
+      // same operations in the same order for the walks that continue, so the results
+      // equal the branched round's below
+      const uint4 B = W::native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)W::kPerBlock));
+#pragma unroll
+      for (int k = 0; k < W::kPerBlock; ++k) {
+        const bool live = !((l.d < eps) | (l.step >= a.max_steps));
+        W::move_native_word(l, live ? l.d : 0.0f, B, k, a);
+        l.step += live ? 1 : 0;
+        l.d = W::dist(l, a, srec);
+      }
+      const bool fin = active & ((l.d < eps) | (l.step >= a.max_steps));
+      // predicated record: the exit position to the walk's ring slot, one more of its unit done
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.v2.f32 [%1], {%2, %3};\n\t"
+          "@p red.shared.add.u32 [%4], 1;\n\t}" ::"r"((uint32_t)fin),
+          "r"((uint32_t)__cvta_generic_to_shared(ring) + l.seq), "f"(l.x[0]), "f"(l.x[1]),
+          "r"((uint32_t)__cvta_generic_to_shared(cnt) + blk)
+          : "memory");
+      lane_steps += fin ? (unsigned long long)l.step : 0ull;
+      active = active & !fin;
+    } else if constexpr (kAmortLoop) {
       // one round: kPerBlock jumps of every live lane from one Philox block
       // (a lane whose walk ends mid-round stops moving and is finished after the round:
       // the sub-jumps stay straight-line predicated code)
