@@ -2033,7 +2033,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #endif
   // exit-ring launches refill at refill_min + this many idle lanes (between rounds)
 #ifndef WOS_EXIT_REFILL_ADD
-#define WOS_EXIT_REFILL_ADD 0
+#define WOS_EXIT_REFILL_ADD 4  // cfg1 x16: 1.566 ms at +0, 1.545 at +4, 1.556 at +7
 #endif
   const bool defer = WOS_DEFER_RECORD && !kExitRing && !S::BC && a.bnd_kind != BND_CONST;
   bool pend = false;

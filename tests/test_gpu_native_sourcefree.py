@@ -127,3 +127,60 @@ def test_deferred_recording_is_tuning_invariant(gpu, dim, dom):
             assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
     finally:
         ctx.set_tuning()
+
+
+def _exit_ring_problem(dom, bnd):
+    from paper_2603_01193_b200 import BallDomain, BoxDomain, Problem, specs
+
+    d = BallDomain([0.1, -0.2], 1.2) if dom == "ball" else BoxDomain([0.0, -0.1], [1.0, 0.7])
+    if bnd == "fourier":
+        M = 8
+        rng = np.random.default_rng(3)
+        bs = (specs.BND_FOURIER, (float(M), 0.2) + tuple(rng.normal(size=2 * M) / (1 + np.arange(2 * M) % M)))
+    else:
+        bs = (specs.BND_LINEAR, (0.3, -0.7, 0.1))
+    return Problem(d, boundary_spec=bs, instance_key=21)
+
+
+@pytest.mark.parametrize("dom,bnd", [("ball", "fourier"), ("ball", "linear"), ("box", "linear")])
+@pytest.mark.parametrize("L", [4, 64, 300])
+@pytest.mark.parametrize("anti", [False, True])
+@pytest.mark.parametrize("max_steps", [3, 1000])
+def test_exit_ring_estimate_equals_rows(gpu, dom, bnd, L, anti, max_steps):
+    """Exit-ring kernels (single-instance source-free 2D, non-constant boundary: a
+    finished walk leaves its exit position in the ring and g(projection) is evaluated
+    when its unit retires; branch-free rounds) against the ROWS sink's walks of the same
+    streams: whole-point units (L = 4: 32 points per unit, L = 64: the cached-point
+    refill), chunks (L = 300), antithetic pairs, walks cut at max_steps, and start
+    points inside the shell (recorded with 0 steps)."""
+    from paper_2603_01193_b200 import WalkConfig, estimate_arrays, walk_poisson_values
+
+    prob = _exit_ring_problem(dom, bnd)
+    P, t0 = 70, 6
+    pts = _points(prob.domain, 2, P - 6, seed=7)
+    # six more points inside the shell (distance < eps from the boundary)
+    if dom == "ball":
+        th = np.linspace(0.3, 5.5, 6)
+        shell = np.array([0.1, -0.2]) + (1.2 - 4e-4) * np.stack([np.cos(th), np.sin(th)], axis=1)
+    else:
+        shell = np.stack([np.linspace(0.1, 0.9, 6), np.full(6, 0.7 - 3e-4)], axis=1)
+    pts = np.concatenate([pts[:30], shell, pts[30:]])
+    cfg = WalkConfig(eps_shell=1e-3, max_steps=max_steps, rng_seed=4, antithetic=anti)
+    mean, m2, n = estimate_arrays([prob], pts, L, cfg, traj_start=t0)
+    j = np.arange(L)
+    tid = t0 + (2 * (j >> 1) if anti else j)
+    sgn = np.where(anti & (j % 2 == 1), -1.0, 1.0)
+    rows_cfg = WalkConfig(eps_shell=1e-3, max_steps=max_steps, rng_seed=4)
+    v, s, _ = walk_poisson_values(prob, np.repeat(pts, L, axis=0), np.repeat(np.arange(P), L),
+                                  np.tile(tid, P), np.tile(sgn, P), rows_cfg)
+    v = v.reshape(P, L)
+    if anti:
+        v = 0.5 * (v[:, 0::2] + v[:, 1::2])
+    assert np.all(n == v.shape[1])
+    mu = v.mean(axis=1)
+    np.testing.assert_allclose(mean, mu, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(m2, ((v - mu[:, None]) ** 2).sum(axis=1), rtol=1e-9, atol=1e-12)
+    s = s.reshape(P, L)
+    assert np.all(s[30:36] == 0) and s.max() <= max_steps
+    if max_steps == 3:
+        assert (s == 3).mean() > 0.3  # most walks are cut
