@@ -2031,6 +2031,12 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_DEFER_RECORD
 #define WOS_DEFER_RECORD 1
 #endif
+  // amortised-round launches with deferred recording refill at refill_min_deferred + this
+  // (4 was cfg1's optimum before its kernel moved to the exit ring; cfg2 x16: 1.705 ms at
+  // +4, 1.666 at +0, 1.663 at -2)
+#ifndef WOS_AMORT_DEFER_ADD
+#define WOS_AMORT_DEFER_ADD 0
+#endif
   // exit-ring launches refill at refill_min + this many idle lanes (between rounds)
 #ifndef WOS_EXIT_REFILL_ADD
 #define WOS_EXIT_REFILL_ADD 4  // cfg1 x16: 1.566 ms at +0, 1.545 at +4, 1.556 at +7
@@ -2353,7 +2359,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
   const int refill_thr = __shfl_sync(
       WOS_FULL,
-      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? 4 : 0)
+      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? WOS_AMORT_DEFER_ADD : 0)
                   : kExitLoop      ? a.refill_min + WOS_EXIT_REFILL_ADD
                   : kExitRing      ? a.refill_min
                   : kAmortLoop     ? 1
