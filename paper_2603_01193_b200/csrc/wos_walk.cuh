@@ -55,6 +55,12 @@
 namespace wos {
 
 #define WOS_FULL 0xffffffffu
+#ifndef WOS_DEEP_STATS
+#define WOS_DEEP_STATS 0
+#endif
+#ifndef WOS_DEEP_T
+#define WOS_DEEP_T 8
+#endif
 
 // ------------------------------------------------------------------------
 // math helpers
@@ -395,7 +401,17 @@ struct Walker {
         uint32_t np;
         best = poly_grid_scan(R, R[-2], G, __float_as_int(H1.y), __float_as_int(H1.z), __float_as_int(H1.w) != 0,
                               reinterpret_cast<const uint32_t*>(a.nodes), l.x[0], l.x[1], &bi, &np);
+#if WOS_DEEP_STATS == 1  // (measurement builds: the warp's longest list instead of the lane's)
+        l.nseg += 2u * __reduce_max_sync(__activemask(), np);
+#elif WOS_DEEP_STATS == 2  // pairs in lists longer than WOS_DEEP_T
+        l.nseg += np > WOS_DEEP_T ? 2u * np : 0u;
+#elif WOS_DEEP_STATS == 3  // queries with lists longer than WOS_DEEP_T
+        l.nseg += np > WOS_DEEP_T ? 2u : 0u;
+#elif WOS_DEEP_STATS == 4  // the warp's longest list among those of at most WOS_DEEP_T pairs
+        l.nseg += 2u * __reduce_max_sync(__activemask(), np > WOS_DEEP_T ? 0u : np);
+#else
         l.nseg += 2u * np;
+#endif
       } else {  // R: shared memory when staged, else global
         best = poly_scan(R, l.n_seg, l.x[0], l.x[1], &bi);
         l.nseg += (uint32_t)(((l.n_seg + 1) >> 1) << 1);
