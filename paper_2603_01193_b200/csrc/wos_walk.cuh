@@ -1978,7 +1978,23 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #define WOS_HOT_BRANCHFREE 1
 #endif
   auto hot_step = [&](typename W::Lane& s) -> bool {
-    if constexpr (!kHotLoop) {
+    if constexpr (kExitLoop) {
+      // Branch-free round of kPerBlock source-free jumps, every lane, live or not: a
+      // walk that has ended (or a lane without one: its stale state is an ended walk's,
+      // d = -1 before the first) jumps by 0, which leaves its position, and with it
+      // the recomputed distance, unchanged, and its step count is not advanced — the
+      // same operations in the same order for the walks that continue, so the results
+      // equal the branched round's of the amortised loop below
+      const uint4 B = W::native_block_at(s, a, 2u * ((uint32_t)s.step / (uint32_t)W::kPerBlock));
+#pragma unroll
+      for (int k = 0; k < W::kPerBlock; ++k) {
+        const bool live = !((s.d < eps) | (s.step >= a.max_steps));
+        W::move_native_word(s, live ? s.d : 0.0f, B, k, a);
+        s.step += live ? 1 : 0;
+        s.d = W::dist(s, a, srec);
+      }
+      return !((s.d < eps) | (s.step >= a.max_steps));
+    } else if constexpr (!kHotLoop) {
       return false;  // (not used outside the hot loop)
     } else if constexpr (W::kPerBlock == 2 && WOS_HOT_BRANCHFREE) {
       // Branch-free round: the second jump runs in every lane and a walk that ended
@@ -2199,8 +2215,19 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 #ifndef WOS_ILP2
 #define WOS_ILP2 0
 #endif
-  if constexpr (WOS_ILP2 && kHotLoop) {
-    if (fast) {
+  // exit-ring kernels run it too (64 registers, 4 CTAs/SM instead of 48 and 5): their
+  // refill, which runs every round, is paid once per two rounds (cfg1 x16 1.542 -> 1.480 ms)
+#ifndef WOS_EXIT_ILP2
+#define WOS_EXIT_ILP2 1
+#endif
+#ifndef WOS_EXIT_ILP2_MIN_UNITS
+#define WOS_EXIT_ILP2_MIN_UNITS 16
+#endif
+  if constexpr ((WOS_ILP2 && kHotLoop) || (WOS_EXIT_ILP2 && kExitLoop)) {
+    // (exit-ring launches with few units per warp keep one walk per lane: with two the
+    // warps' last units run half empty — cfg1 as a single estimate, 5 units per warp:
+    // 0.153 ms with two slots, WOS_EXIT_ILP2_MIN_UNITS decides)
+    if (fast && (!kExitLoop || a.n_units >= (uint32_t)WOS_EXIT_ILP2_MIN_UNITS * gridDim.x * (blockDim.x >> 5))) {
       // ==================================================================
       // Two walks per lane (slots A = l, B = lb): every iteration jumps both, so the
       // two independent dependency chains interleave and the loop / vote / refill
@@ -2212,7 +2239,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       bool act_a = false, act_b = false;
       uint32_t blk_a = 0, blk_b = 0;
       unsigned idle_a = WOS_FULL, idle_b = WOS_FULL;
-      const int thr2 = __shfl_sync(WOS_FULL, min(64, 2 * a.refill_min), 0);
+      const int thr2 = __shfl_sync(WOS_FULL, min(64, 2 * (a.refill_min + (kExitLoop ? WOS_EXIT_REFILL_ADD : 0))), 0);
       // move the cached unit to the next grabbed one; false if none is left
       auto next_unit = [&]() -> bool {
         if (!exhausted && n_grabbed == cu_k + 1u && (n_grabbed - r_unit) < (uint32_t)kUQ) {
@@ -2253,6 +2280,9 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       };
       auto record2 = [&](typename W::Lane& s, uint32_t blk_s) {
         lane_steps += (unsigned long long)s.step;
+        if constexpr (kExitLoop)
+          *reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(ring) + s.seq) = make_float2(s.x[0], s.x[1]);
+        else
         *reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(ring) + s.seq) = s.acc + a.bnd_c;
         atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_s), 1u);
       };
@@ -2268,6 +2298,15 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
       const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
       uint32_t steps32 = 0u;
       auto record2p = [&](typename W::Lane& s, uint32_t blk_s, bool fin) {
+        if constexpr (kExitLoop) {  // the exit position (exit ring)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.v2.f32 [%1], {%2, %3};\n\t"
+              "@p red.shared.add.u32 [%4], 1;\n\t}" ::"r"((uint32_t)fin),
+              "r"(ring_s + s.seq), "f"(s.x[0]), "f"(s.x[1]), "r"(cnt_s + blk_s)
+              : "memory");
+          steps32 += fin ? (uint32_t)s.step : 0u;
+          return;
+        }
         const float v = s.acc + a.bnd_c;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.f32 [%1], %2;\n\t"
@@ -2296,7 +2335,7 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
             s.d = cu_d;
             s.pc = pc;
             s.sgn = __int_as_float(0x3f800000 | ((jr & anti_bit) << 31));
-            s.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+            s.seq = (seq % kRing) * kSlotBytes;
             blk_s = blk_new;
             act = true;
           }
@@ -2305,14 +2344,16 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
           const uint64_t tid = anti ? a.traj_start + 2ull * (j >> 1) : a.traj_start + j;
           W::start(s, table, a.hdr, a, cu_x, cu_inst, cu_pid, tid, (anti && (j & 1u)) ? -1.0 : 1.0);
           s.d = cu_d;
-          s.seq = (seq % kRing) * (uint32_t)sizeof(Real);
+          s.seq = (seq % kRing) * kSlotBytes;
           blk_s = blk_new;
           act = true;
         }
         if (take && !real) atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(cnt) + blk_new), 1u);
-        if (cu_d < eps && take && real) {  // the unit's point lies in the shell
-          record2(s, blk_s);
-          act = false;
+        if constexpr (!kExitLoop) {  // (an exit-ring round finishes such a walk itself)
+          if (cu_d < eps && take && real) {  // the unit's point lies in the shell
+            record2(s, blk_s);
+            act = false;
+          }
         }
       };
       while (true) {
@@ -2611,21 +2652,8 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
 
     // ================= one step of every active walk =================
     if constexpr (kExitLoop) {
-      // Branch-free round of kPerBlock source-free jumps, every lane, live or not: a
-      // walk that has ended (or a lane without one: its stale state is an ended walk's,
-      // d = -1 before the first) jumps by 0, which leaves its position, and with it
-      // the recomputed distance, unchanged, and its step count is not advanced — the
-      // same operations in the same order for the walks that continue, so the results
-      // equal the branched round's below
-      const uint4 B = W::native_block_at(l, a, 2u * ((uint32_t)l.step / (uint32_t)W::kPerBlock));
-#pragma unroll
-      for (int k = 0; k < W::kPerBlock; ++k) {
-        const bool live = !((l.d < eps) | (l.step >= a.max_steps));
-        W::move_native_word(l, live ? l.d : 0.0f, B, k, a);
-        l.step += live ? 1 : 0;
-        l.d = W::dist(l, a, srec);
-      }
-      const bool fin = active & ((l.d < eps) | (l.step >= a.max_steps));
+      // one branch-free round of every lane (hot_step above)
+      const bool fin = active & !hot_step(l);
       // predicated record: the exit position to the walk's ring slot, one more of its unit done
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.v2.f32 [%1], {%2, %3};\n\t"

@@ -184,3 +184,39 @@ def test_exit_ring_estimate_equals_rows(gpu, dom, bnd, L, anti, max_steps):
     assert np.all(s[30:36] == 0) and s.max() <= max_steps
     if max_steps == 3:
         assert (s == 3).mean() > 0.3  # most walks are cut
+
+
+@pytest.mark.parametrize("anti", [False, True])
+def test_exit_ring_two_slot_loop_equals_one_slot_and_rows(gpu, anti):
+    """Exit-ring launches with at least 16 units per warp run two walks per lane
+    (wos_walk.cuh WOS_EXIT_ILP2); smaller ones keep one. With one CTA per SM a 20,000
+    point estimate is above the threshold, with the default grid below it: both must
+    give the same bits, and the ROWS sink's walks of the same streams the same moments."""
+    from paper_2603_01193_b200 import WalkConfig, engine, estimate_arrays, walk_poisson_values
+
+    prob = _exit_ring_problem("ball", "fourier")
+    P, L, t0 = 20000, 32, 3
+    pts = _points(prob.domain, 2, P, seed=11)
+    assert pts.shape[0] == P
+    cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9, antithetic=anti)
+    ctx = engine.get_context(0)
+    one = estimate_arrays([prob], pts, L, cfg, traj_start=t0)
+    try:
+        ctx.set_tuning(blocks_per_sm=1)
+        two = estimate_arrays([prob], pts, L, cfg, traj_start=t0)
+    finally:
+        ctx.set_tuning()
+    assert np.array_equal(one[0], two[0]) and np.array_equal(one[1], two[1])
+    sel = np.arange(0, P, 41)
+    j = np.arange(L)
+    tid = t0 + (2 * (j >> 1) if anti else j)
+    sgn = np.where(anti & (j % 2 == 1), -1.0, 1.0)
+    rows_cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9)
+    v, _, _ = walk_poisson_values(prob, np.repeat(pts[sel], L, axis=0), np.repeat(sel, L),
+                                  np.tile(tid, sel.size), np.tile(sgn, sel.size), rows_cfg)
+    v = v.reshape(sel.size, L)
+    if anti:
+        v = 0.5 * (v[:, 0::2] + v[:, 1::2])
+    mu = v.mean(axis=1)
+    np.testing.assert_allclose(two[0][sel], mu, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(two[1][sel], ((v - mu[:, None]) ** 2).sum(axis=1), rtol=1e-9, atol=1e-12)
