@@ -61,6 +61,9 @@ namespace wos {
 #ifndef WOS_DEEP_T
 #define WOS_DEEP_T 8
 #endif
+#ifndef WOS_POLY_UNROLL4
+#define WOS_POLY_UNROLL4 1
+#endif
 
 // ------------------------------------------------------------------------
 // math helpers
@@ -351,41 +354,65 @@ struct Walker {
     const uint32_t e = bytes8 ? (C.x & 0xFFFFu) : C.y;
     *n_pairs = e;
     const uint8_t* idx8 = reinterpret_cast<const uint8_t*>(idx);
-    // byte indices as a 96-bit queue shifted by one byte per pair (one LOP3 and three
-    // funnel shifts instead of selecting the word and the byte lane per pair)
-    uint32_t q0 = C.y, q1 = C.z, q2 = C.w;
-    for (uint32_t k = 0; k < e; ++k) {
-      int j;
-      if (bytes8) {
-        if (k < 12) {
-          j = (int)(q0 & 0xFFu);
-          q0 = __funnelshift_r(q0, q1, 8);
-          q1 = __funnelshift_r(q1, q2, 8);
-          q2 >>= 8;
-        } else {
-          j = (int)__ldg(idx8 + (C.x >> 16) + (k - 12));
-        }
-      } else {
-        const uint32_t wd = k < 2 ? C.z : C.w;
-        j = k < 4 ? (int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)) : (int)__ldg(idx + C.x + (k - 4));
+#endif
+    // The running minimum moves by pairs and remembers the first pair attaining it
+    // (*bi_out = its first segment): poly_project rescans from there and takes the first
+    // strictly nearest segment, which is the one the segment-by-segment scan records
+    // (its pair's first segment wins a tie inside the pair, an earlier pair a tie between
+    // pairs) — FMNMX, FSETP, FMNMX, SEL per pair instead of a compare and two selects
+    // per segment.
+    int bj = 0;
+    auto eval = [&](int j) {
+      const float2 d = pair_d2(__ldg(R + 2 * j), __ldg(R + 2 * j + 1), __ldg(R + 2 * j + 2), px, py);
+      const float m = fminf(d.x, d.y);
+      bj = m < best ? j : bj;
+      best = fminf(best, m);
+    };
+#if WOS_GRID_INLINE
+    if (bytes8) {
+      // byte indices: the twelve inline ones four per word (one PRMT-class extract each,
+      // no queue shifting), the rest from the index array
+      const uint32_t e0 = min(e, 12u);
+      uint32_t w = C.y, w1 = C.z, w2 = C.w;
+#if !WOS_POLY_UNROLL4
+      for (uint32_t k = 0; k < e0; ++k) {  // (the queue shifted by one byte per pair)
+        eval((int)(w & 0xFFu));
+        w = __funnelshift_r(w, w1, 8);
+        w1 = __funnelshift_r(w1, w2, 8);
+        w2 >>= 8;
       }
 #else
-    const uint32_t* cell = gw + cells_off + cy * G + cx;
-    const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
-    *n_pairs = e - b;
-    for (uint32_t k = b; k < e; ++k) {
-      const int j = __ldg(idx + k);
+      for (uint32_t k = 0; k < e0;) {
+        eval((int)(w & 0xFFu));
+        if (++k >= e0) break;
+        eval((int)((w >> 8) & 0xFFu));
+        if (++k >= e0) break;
+        eval((int)((w >> 16) & 0xFFu));
+        if (++k >= e0) break;
+        eval((int)(w >> 24));
+        ++k;
+        w = w1;
+        w1 = w2;
+      }
 #endif
-      const float2 d = pair_d2(__ldg(R + 2 * j), __ldg(R + 2 * j + 1), __ldg(R + 2 * j + 2), px, py);
-      if (d.x < best) {
-        best = d.x;
-        bi = 2 * j;
+      for (uint32_t k = 12; k < e; ++k) eval((int)__ldg(idx8 + (C.x >> 16) + (k - 12)));
+    } else {
+      const uint32_t e0 = min(e, 4u);
+      for (uint32_t k = 0; k < e0; ++k) {
+        const uint32_t wd = k < 2 ? C.z : C.w;
+        eval((int)((k & 1) ? (wd >> 16) : (wd & 0xFFFFu)));
       }
-      if (d.y < best) {
-        best = d.y;
-        bi = 2 * j + 1;
-      }
+      for (uint32_t k = 4; k < e; ++k) eval((int)__ldg(idx + C.x + (k - 4)));
     }
+#else
+    {
+      const uint32_t* cell = gw + cells_off + cy * G + cx;
+      const uint32_t b = __ldg(cell), e = __ldg(cell + 1);
+      *n_pairs = e - b;
+      for (uint32_t k = b; k < e; ++k) eval((int)__ldg(idx + k));
+    }
+#endif
+    bi = 2 * bj;
     *bi_out = bi;
     return best;
   }
