@@ -186,8 +186,8 @@ def test_exit_ring_estimate_equals_rows(gpu, dom, bnd, L, anti, max_steps):
         assert (s == 3).mean() > 0.3  # most walks are cut
 
 
-@pytest.mark.parametrize("anti", [False, True])
-def test_exit_ring_two_slot_loop_equals_one_slot_and_rows(gpu, anti):
+@pytest.mark.parametrize("anti,rounds", [(False, 10), (True, 10), (False, 7)])
+def test_exit_ring_two_slot_loop_equals_one_slot_and_rows(gpu, anti, rounds):
     """Exit-ring launches with at least 16 units per warp run two walks per lane
     (wos_walk.cuh WOS_EXIT_ILP2); smaller ones keep one. With one CTA per SM a 20,000
     point estimate is above the threshold, with the default grid below it: both must
@@ -198,7 +198,8 @@ def test_exit_ring_two_slot_loop_equals_one_slot_and_rows(gpu, anti):
     P, L, t0 = 20000, 32, 3
     pts = _points(prob.domain, 2, P, seed=11)
     assert pts.shape[0] == P
-    cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9, antithetic=anti)
+    # (rounds = 7: the single-instance estimate kernels compiled for the opt-in stream)
+    cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9, antithetic=anti, philox_rounds=rounds)
     ctx = engine.get_context(0)
     one = estimate_arrays([prob], pts, L, cfg, traj_start=t0)
     try:
@@ -211,7 +212,7 @@ def test_exit_ring_two_slot_loop_equals_one_slot_and_rows(gpu, anti):
     j = np.arange(L)
     tid = t0 + (2 * (j >> 1) if anti else j)
     sgn = np.where(anti & (j % 2 == 1), -1.0, 1.0)
-    rows_cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9)
+    rows_cfg = WalkConfig(eps_shell=1e-3, max_steps=1000, rng_seed=9, philox_rounds=rounds)
     v, _, _ = walk_poisson_values(prob, np.repeat(pts[sel], L, axis=0), np.repeat(sel, L),
                                   np.tile(tid, sel.size), np.tile(sgn, sel.size), rows_cfg)
     v = v.reshape(sel.size, L)
