@@ -477,14 +477,33 @@ struct Walker {
     if constexpr (S::NATIVE) {
       const float4* rec = reinterpret_cast<const float4*>(a.segs) + l.rec_off;
       const int np = ((l.n_seg + 1) >> 1) << 1;  // segments incl. the odd polygon's pad
-      const int i1 = min(i0 + 4, np);
-      float best = 3.0e38f;
       int bi = i0;
-      for (int i = i0; i < i1; ++i) {
-        const float d = seg_at(rec, i, l.x[0], l.x[1]);
-        if (d < best) {
-          best = d;
-          bi = i;
+      if (__float_as_int(__ldg(rec - 1).x) > 0) {
+        // candidate grid: i0 is the first segment of the nearest pair; the second one wins
+        // only if strictly nearer (pair_d2 = seg_d2 bit for bit); the closest point from
+        // the same three records, in seg_at's operation order
+        const int j = i0 >> 1;
+        const float4 A = __ldg(rec + 2 * j), U = __ldg(rec + 2 * j + 1), An = __ldg(rec + 2 * j + 2);
+        const float2 d = pair_d2(A, U, An, l.x[0], l.x[1]);
+        const bool odd = d.y < d.x;
+        const float ax = odd ? A.y : A.x, ay = odd ? A.w : A.z;
+        const float nx = odd ? An.x : A.y, ny = odd ? An.z : A.w;
+        const float ux = odd ? U.y : U.x, uy = odd ? U.w : U.z;
+        const float ex = nx - ax, ey = ny - ay;
+        const float wx = l.x[0] - ax, wy = l.x[1] - ay;
+        const float t = __saturatef(fmaf(wx, ux, wy * uy));
+        q[0] = fmaf(t, ex, ax);
+        q[1] = fmaf(t, ey, ay);
+        return;
+      } else {  // block scan: the first nearest segment of the recorded block of 4
+        const int i1 = min(i0 + 4, np);
+        float best = 3.0e38f;
+        for (int i = i0; i < i1; ++i) {
+          const float d = seg_at(rec, i, l.x[0], l.x[1]);
+          if (d < best) {
+            best = d;
+            bi = i;
+          }
         }
       }
       float qx, qy;
