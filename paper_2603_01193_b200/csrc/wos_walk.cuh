@@ -64,6 +64,13 @@ namespace wos {
 #ifndef WOS_POLY_UNROLL4
 #define WOS_POLY_UNROLL4 1
 #endif
+// polar / mesh walks keep the closest point of their last distance query for project()
+#ifndef WOS_KEEP_CLOSEST
+#define WOS_KEEP_CLOSEST 1
+#endif
+#ifndef WOS_KEEP_CLOSEST_MESH
+#define WOS_KEEP_CLOSEST_MESH 1
+#endif
 
 // ------------------------------------------------------------------------
 // math helpers
@@ -182,6 +189,7 @@ struct Walker {
     uint32_t k1;               // NATIVE multi-instance: the instance key
     int32_t seg_off, n_seg, rec_off;
     int32_t seg_i;  // polygon: nearest segment found by the last distance query
+    Real cq[DIM];   // polar / mesh: closest boundary point found by the last distance query
     uint32_t nseg = 0;  // NATIVE polygon: segment distances evaluated (work counter)
     Real thr;       // delta tracking: throughput (walker.py:365, _kernels.py:539)
     Real sa;        // delta tracking: sqrt(alpha) at the start point (walker.py:352-354)
@@ -208,10 +216,14 @@ struct Walker {
   __device__ static __forceinline__ Real dist(Lane& l, const KArgs& a, const float4* srec) {
     if constexpr (S::DOM == DOM_BALL || S::DOM == DOM_BOX || S::DOM == DOM_CUBE) return dist_at(l, a, l.x);
     else if constexpr (S::DOM == DOM_POLAR) {
+      // (the closest point stays in the lane: a walk ends at the position of its last
+      // query, so project() needs no second scan — run by the few lanes of a deferred batch)
+      if constexpr (WOS_KEEP_CLOSEST) return polar_query(l, a, srec, l.x[0], l.x[1], &l.cq[0], &l.cq[1]);
       Real qx, qy;
       return polar_query(l, a, srec, l.x[0], l.x[1], &qx, &qy);
     } else if constexpr (S::DOM == DOM_MESH) {
       // MeshDomain.boundary_query (geometry.py:527-533): |p - closest|
+      if constexpr (WOS_KEEP_CLOSEST_MESH) return psqrt(mesh_d2(l, a, l.cq));
       Real q[3];
       return psqrt(mesh_d2(l, a, q));
     } else {
@@ -582,10 +594,20 @@ struct Walker {
 #pragma unroll
       for (int i = 0; i < DIM; ++i) q[i] = (i == axis) ? face : l.x[i];
     } else if constexpr (S::DOM == DOM_POLAR) {
-      polar_query(l, a, nullptr, l.x[0], l.x[1], &q[0], &q[1]);
+      if constexpr (WOS_KEEP_CLOSEST) {
+        q[0] = l.cq[0];
+        q[1] = l.cq[1];
+      } else {
+        polar_query(l, a, nullptr, l.x[0], l.x[1], &q[0], &q[1]);
+      }
     } else if constexpr (S::DOM == DOM_MESH) {
-      Lane c = l;
-      mesh_d2(c, a, q);
+      if constexpr (WOS_KEEP_CLOSEST_MESH) {
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) q[i] = l.cq[i];
+      } else {
+        Lane c = l;
+        mesh_d2(c, a, q);
+      }
     } else {
       poly_project(l, a, q);
     }
