@@ -2482,9 +2482,14 @@ __device__ __forceinline__ void wos_kernel_body(const KArgs& a) {
   // instead of reloading it from the constant bank every iteration.
   // (delta tracking: a step costs far more than recording, so the plain threshold;
   // amortised rounds refill only between rounds and batch 4 more: cfg1 -1.9 %)
+  // polar walks keep their closest point, so recording a batch is only the boundary
+  // term: they refill at the plain threshold (sweep 4-12: 17.7 ms at 4, 19.5 at 12 on
+  // the mild curve; meshes, whose start and traversal cost more, keep the deferred one)
+  constexpr bool kCheapRecord = WOS_KEEP_CLOSEST && S::DOM == DOM_POLAR;
   const int refill_thr = __shfl_sync(
       WOS_FULL,
-      min(32, (defer && !W::kScr) ? a.refill_min_deferred + (kAmortLoop ? WOS_AMORT_DEFER_ADD : 0)
+      min(32, (defer && !W::kScr && !kCheapRecord) ? a.refill_min_deferred + (kAmortLoop ? WOS_AMORT_DEFER_ADD : 0)
+                  : kCheapRecord   ? max(1, a.refill_min - 2)  // (sweep 2-7: 3 within 0.5 % of the best)
                   : kExitLoop      ? a.refill_min + WOS_EXIT_REFILL_ADD
                   : kExitRing      ? a.refill_min
                   : kAmortLoop     ? 1
